@@ -45,6 +45,7 @@ def lib():
         L.or_label.argtypes = [ctypes.c_char_p, ctypes.c_int]; L.or_label.restype = ctypes.c_int
         L.or_matrix.argtypes = [ctypes.c_int, p]; L.or_matrix.restype = i64
         L.or_minplus.argtypes = [p, p, p, i64, i64, i64]; L.or_minplus.restype = None
+        L.or_minplus_bt.argtypes = [p, p, p, i64, i64, i64]; L.or_minplus_bt.restype = None
         L.or_minplus_skip.argtypes = [p, p, p, i64, i64, i64]; L.or_minplus_skip.restype = None
         L.or_diag_min.argtypes = [p, i64]; L.or_diag_min.restype = i32
         L.or_shift.argtypes = [p, p, i64, p]; L.or_shift.restype = ctypes.c_int
@@ -106,6 +107,18 @@ def minplus(A: np.ndarray, B: np.ndarray, skip: bool = False) -> np.ndarray:
     assert K == K2
     C = np.empty((M, N), dtype=np.int32)
     (lib().or_minplus_skip if skip else lib().or_minplus)(_ptr(A), _ptr(B), _ptr(C), M, N, K)
+    return C
+
+
+def minplus_bt(A: np.ndarray, BT: np.ndarray) -> np.ndarray:
+    """C = A (x) B given BT = B transposed (N x K): c_ij = min_k(a_ik + bt_jk)."""
+    A = np.ascontiguousarray(A, dtype=np.int32)
+    BT = np.ascontiguousarray(BT, dtype=np.int32)
+    M, K = A.shape
+    N, K2 = BT.shape
+    assert K == K2
+    C = np.empty((M, N), dtype=np.int32)
+    lib().or_minplus_bt(_ptr(A), _ptr(BT), _ptr(C), M, N, K)
     return C
 
 

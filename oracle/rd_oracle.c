@@ -142,6 +142,24 @@ void or_minplus(const int32_t *A, const int32_t *B, int32_t *C, int64_t M, int64
     }
 }
 
+/* The same i-j-k loop reading B through its transpose BT (N x K, BT[j][k] = b_kj), so
+ * the k loop walks both operands contiguously; used for sampled rows of full-size
+ * products (a row costs N*K terms).  c_ij = min_k (a_ik + bt_jk). */
+void or_minplus_bt(const int32_t *A, const int32_t *BT, int32_t *C, int64_t M, int64_t N, int64_t K) {
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t j = 0; j < N; ++j) {
+      int32_t best = OR_INF;
+      for (int64_t k = 0; k < K; ++k) {
+        int32_t a = A[i * K + k], b = BT[j * K + k];
+        if (a == OR_INF || b == OR_INF) continue;
+        int32_t s = a + b;
+        if (s < best) best = s;
+      }
+      C[i * N + j] = best;
+    }
+}
+
 /* The same definition with the terms whose B-operand is INF skipped ahead of time:
  * c_ij = min_{k : b_kj finite} (a_ik + b_kj).  For each column j the finite k of B
  * are listed once; the result is identical to or_minplus (a skipped term is INF and

@@ -270,6 +270,7 @@ def test_skip_form_equals_dense():
     for inf_frac in (0.0, 0.01, 0.5, 0.95, 1.0):
         A, B = _rand(rng, 57, 33, inf_frac, 300), _rand(rng, 33, 41, inf_frac, 300)
         assert (O.minplus(A, B) == O.minplus(A, B, skip=True)).all()
+        assert (O.minplus(A, B) == O.minplus_bt(A, np.ascontiguousarray(B.T))).all()
     A = O.matrix(5)
     X = O.minplus(A, A)
     assert (O.minplus(X, A) == O.minplus(X, A, skip=True)).all()
