@@ -1,0 +1,182 @@
+/*
+ * rd.h — C-ABI of librd.so, the B200 (sm_100a) (min,+) power pipeline for the Roman
+ * domination number of cylinders P_m [] C_n (arXiv 2409.17658).
+ *
+ * Citations "P:<line>" are to the paper's text, with the result named.
+ * Plain C types only; no torch or CUDA types appear in any signature (streams are
+ * passed as `void *` holding a cudaStream_t, NULL = the legacy default stream).
+ *
+ * Conventions shared by every call
+ *   - Status: every entry point returns an int rd_status. It never aborts or throws
+ *     across the ABI. On a status < 0, rd_last_error() returns a thread-local message.
+ *   - Tropical infinity: an int16 entry x >= RD_INF means +inf.  Finite entries must
+ *     lie in [0, RD_INF).  Results hold exactly RD_INF for +inf.  Headroom: a sum of
+ *     two entries is <= 2*RD_INF = 0x7FFE, so 16-bit lanes never wrap (R5).
+ *   - Word order: lexicographic with a < b < c < d (the paper is silent, R3).
+ *   - Matrix orientation: row = predecessor word q, column = successor word p.
+ *   - Host buffers are caller-allocated; pass NULL to query a size first.
+ *   - Device buffers passed to rd_minplus_mul* are caller-owned device pointers
+ *     (e.g. torch.empty(..., dtype=torch.int16, device="cuda").data_ptr()).
+ */
+#ifndef RD_H
+#define RD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RD_INF ((int16_t)0x3FFF)
+
+enum rd_status {
+  RD_OK = 0,        /* success */
+  RD_NOTFOUND = 1,  /* rd_power_sequence*: no recurrence up to kmax (not an error) */
+  RD_EINVAL = -1,   /* bad argument: m < 1, n < 3, N < 1, NULL required pointer, ... */
+  RD_ENOMEM = -2,   /* host or device allocation failed */
+  RD_ECUDA = -3,    /* a CUDA runtime call failed; rd_last_error() has its string */
+  RD_ERANGE = -4    /* int16 headroom exceeded: 2*m*kmax >= RD_INF (R5) */
+};
+
+/* Thread-local message describing the last non-OK status of this thread ("" if none). */
+const char *rd_last_error(void);
+
+/* Makes `device` the calling thread's current device for this library's CUDA runtime
+ * (the library links its own runtime; callers that select devices through another
+ * runtime — e.g. torch — call this first).  Errors: RD_ECUDA. */
+int rd_set_device(int device);
+
+/* ---------------------------------------------------------------------------
+ * rd_build_states — the correct words of length m (Def 4): words over
+ * {a,b,c,d} with none of ad, da, ab, ba, bb.  N = C_m (Table 1).
+ *   m      >= 1 (m <= 12 supported)
+ *   words  host, nullable; if non-NULL receives N*m chars 'a'..'d', word w at
+ *          words[w*m .. w*m+m-1] (no terminators), lexicographic order.
+ *   N_out  host, required: N.
+ * Errors: RD_EINVAL (m out of range, N_out NULL).  Host only, no GPU needed.
+ */
+int rd_build_states(int m, char *words, int64_t *N_out);
+
+/* ---------------------------------------------------------------------------
+ * rd_build_matrix — the transfer matrix A(G) (Cor 7; arcs = the
+ * can-follow rules P:165-194 read with p_i = d for the intermediate rows, DESIGN.md
+ * R1; label l(q,p) = 2 p(a) + p(b)).
+ *   A      host, nullable; if non-NULL receives N*N int16 row-major:
+ *          A[q*N + p] = 2 #a(p) + #b(p) if p can follow q, else RD_INF.
+ *   N_out  host, required.
+ * Errors: RD_EINVAL, RD_ENOMEM.  Host only (OpenMP successor generation), no GPU.
+ */
+int rd_build_matrix(int m, int16_t *A, int64_t *N_out);
+
+/* ---------------------------------------------------------------------------
+ * rd_minplus_mul — C = A (x) B, c_ij = min_k (a_ik + b_kj)  ((min,+) product).
+ *   A, B, C  DEVICE pointers, N x N int16 row-major, entries in [0, RD_INF];
+ *            C must not alias A or B.
+ *   N        >= 1.
+ * Runs on the legacy default stream and returns after enqueueing (asynchronous);
+ * a temporary packed workspace is allocated stream-ordered and freed on the stream.
+ * Entries > RD_INF are clamped to RD_INF on load; negative entries are a
+ * precondition violation (not checked).
+ * Errors: RD_EINVAL (NULL, N < 1), RD_ENOMEM, RD_ECUDA.
+ */
+int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N);
+
+/* Rectangular / strided form: C (M x N, ldc) = A (M x K, lda) (x) B (K x N, ldb),
+ * all DEVICE int16 row-major, on `cuda_stream` (NULL = legacy default stream).
+ * Used for row panels (multi-GPU) and non-square products. M, N, K >= 1,
+ * lda >= K, ldb >= N, ldc >= N. */
+int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb,
+                      int16_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * Recurrence triple (Lemma 2; Prop 8; Alg 2 step 4 P:292):
+ * A^{n0+alpha} = beta (x) A^{n0}.  k_stop = last power computed. */
+typedef struct {
+  int32_t found, n0, alpha, beta, k_stop;
+} rd_period_t;
+
+/* rd_power_sequence — Algorithm 2 on one GPU: A^k = A^{k-1} (x) A for
+ * k = 2.. until the first k at which some alpha in 1..10 gives A^k = beta (x) A^{k-alpha}
+ * (smallest alpha; canonical policy, R6), or k = kmax.
+ *   kmax   >= 2 (the paper uses K = 50); 2*m*kmax < RD_INF.
+ *   out    host, required.
+ *   diag   host, nullable, kmax+1 entries: diag[k] = min_p (A^k)_pp (Cor 7) for
+ *          k = 1..k_stop, INT32_MAX for an all-inf diagonal and for k > k_stop;
+ *          diag[0] = INT32_MAX.  diag[n] = gamma_R(P_m [] C_n) for n >= 3.
+ * Returns RD_OK if found, RD_NOTFOUND (out->found = 0) if not within kmax.
+ * Device workspace (ring of alpha_max+1 powers + packed A) is allocated and freed
+ * inside the call.  Uses device 0 of the calling thread's current device. */
+int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag);
+
+/* As above with alpha_max (1..32) and the policy:
+ *   0 canonical: first detecting k, smallest alpha;
+ *   1 paper-compatible (R6): n0 from first detection, then the largest alpha <=
+ *     alpha_max with A^{n0+alpha} = beta (x) A^{n0} (computes powers up to n0+alpha_max). */
+int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out, int32_t *diag);
+
+/* rd_roman_cylinder — gamma_R(P_m [] C_n) (Alg 1 P:257-268 via Cor 7 for n <= k_stop;
+ * for larger n, Prop 8 + the finite-difference solution P:248:
+ * n' = n0 + ((n - n0) mod alpha), gamma = diag[n'] + beta (n - n') / alpha).
+ *   m >= 1, n >= 3.  The chain of m (kmax = 50) is computed on first use and
+ *   cached per process.  Errors: RD_EINVAL, RD_NOTFOUND (no recurrence and n > 50). */
+int rd_roman_cylinder(int m, int64_t n, int64_t *gamma);
+
+/* ---------------------------------------------------------------------------
+ * Power-chain context: one row panel [row_begin, row_end) of every power A^k on the
+ * current device.  Rows of A^{k+1} depend only on the same rows of A^k and on A
+ * (A^{k+1} = A^k (x) A, P:83 + Thm 1), so ranks that own disjoint panels never
+ * exchange matrix data; only the per-step stats vector is reduced.
+ */
+typedef struct rd_chain rd_chain;
+
+/* Builds A(G) on the host, uploads it, packs the right operand once, places rows
+ * [row_begin, row_end) of A^1 in ring slot 1.  alpha_max 1..32.  cuda_stream: all
+ * work of this chain is enqueued on it (NULL = legacy default). */
+int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
+                    rd_chain **out);
+int rd_chain_destroy(rd_chain *c);
+
+/* Order N = C_m of the chain's matrices; current power k (1 after create). */
+int64_t rd_chain_order(const rd_chain *c);
+int rd_chain_current_k(const rd_chain *c);
+
+/* Length of the stats vector: 1 + 4*alpha_max int32. */
+int rd_stats_len(int alpha_max);
+
+/* rd_chain_step — computes rows of A^{k+1} = A^k (x) A into the ring and, fused in the
+ * same kernel, the stats vector of the new power over this panel (all entries are
+ * MIN-reducible, so panels combine with an elementwise min, e.g. NCCL all_reduce MIN):
+ *   s[0]                diag min over the panel's diagonal entries (Cor 7), RD_STAT_NONE if none
+ *   s[1 + 4(a-1) + 0]   lo_a  = min  (A^{k+1} - A^{k+1-a}) over entries finite in both
+ *   s[1 + 4(a-1) + 1]  -hi_a  (hi_a = max of the same differences)
+ *   s[1 + 4(a-1) + 2]  -mis_a (mis_a = 1 if some entry is inf in one power only)
+ *   s[1 + 4(a-1) + 3]  -fin_a (fin_a = 1 if some entry is finite in both)
+ * for a = 1..alpha_max (entries for a >= k+1 are left at their neutral values).
+ *   stats_dev  DEVICE int32[rd_stats_len], written on the chain's stream (required).
+ * Asynchronous: returns after enqueueing. */
+#define RD_STAT_NONE INT32_MAX
+int rd_chain_step(rd_chain *c, int32_t *stats_dev);
+
+/* Copies rows [row_begin, row_end) of A^k (k within the last alpha_max+1 powers) to
+ * host int16 row-major (row_end-row_begin) x N.  Synchronises the chain's stream. */
+int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out);
+
+/* Host decision on a (reduced) stats vector of power k: returns 1 and sets *alpha,
+ * *beta for the smallest a in 1..min(alpha_max, k-1) with A^k = beta (x) A^{k-a}
+ * (same inf pattern, some finite entry, one common difference beta >= 0), else 0.
+ * With only_alpha > 0, tests that single a. */
+int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, int32_t *alpha,
+                    int32_t *beta);
+
+/* ---------------------------------------------------------------------------
+ * rd_alu_probe — measures the issue rate of the integer instructions the GEMM uses
+ * (register-only kernels, many independent chains) on the current device:
+ * out[0] VIADDMNMX.S16x2 warp-instructions / clock / SM, out[1] (min,+) lane-ops /
+ * clock / SM for the DPX form, out[2] the same for the mixed IADD(fma)+VIMNMX3(alu)
+ * form, out[3] SM clock in MHz seen during the probe.  Synchronous. */
+int rd_alu_probe(double out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RD_H */

@@ -1,0 +1,235 @@
+"""B200-native (min,+) power pipeline for the Roman domination number of cylinders
+P_m [] C_n (arXiv 2409.17658).
+
+Thin Python binding over the C-ABI of ``librd.so`` (include/rd.h): argument marshalling
+only.  Every step of the path runs in the library's kernels; PyTorch supplies device
+memory, streams and (in ``dist``) process groups.  There is no CPU fallback: if the
+library is missing, importing the ops raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librd.so")
+
+RD_INF = 0x3FFF
+RD_STAT_NONE = 2**31 - 1
+RD_OK, RD_NOTFOUND, RD_EINVAL, RD_ENOMEM, RD_ECUDA, RD_ERANGE = 0, 1, -1, -2, -3, -4
+
+
+class RDError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rd status {status}: {msg}")
+        self.status = status
+
+
+class _Period(ctypes.Structure):
+    _fields_ = [("found", ctypes.c_int32), ("n0", ctypes.c_int32), ("alpha", ctypes.c_int32),
+                ("beta", ctypes.c_int32), ("k_stop", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads librd.so (raises if it has not been built: no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; build it with `python -m paper_2409_17658_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, i32, p, ci = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int
+        L.rd_last_error.restype = ctypes.c_char_p
+        L.rd_set_device.argtypes = [ci]
+        L.rd_build_states.argtypes = [ci, p, p]
+        L.rd_build_matrix.argtypes = [ci, p, p]
+        L.rd_minplus_mul.argtypes = [p, p, p, i64]
+        L.rd_minplus_mul_ex.argtypes = [p, i64, p, i64, p, i64, i64, i64, i64, p]
+        L.rd_power_sequence.argtypes = [ci, ci, p, p]
+        L.rd_power_sequence_ex.argtypes = [ci, ci, ci, ci, p, p]
+        L.rd_roman_cylinder.argtypes = [ci, i64, p]
+        L.rd_chain_create.argtypes = [ci, ci, i64, i64, p, p]
+        L.rd_chain_destroy.argtypes = [p]
+        L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
+        L.rd_chain_current_k.argtypes = [p]
+        L.rd_stats_len.argtypes = [ci]
+        L.rd_chain_step.argtypes = [p, p]
+        L.rd_chain_read_rows.argtypes = [p, ci, p]
+        L.rd_stats_decide.argtypes = [p, ci, ci, ci, p, p]
+        L.rd_alu_probe.argtypes = [p]
+        for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
+                  "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
+                  "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
+                  "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe"):
+            getattr(L, f).restype = ci
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, allow=(RD_OK,)) -> int:
+    if rc not in allow:
+        raise RDError(rc, lib().rd_last_error().decode())
+    return rc
+
+
+def _np_ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _sync_device():
+    """Selects torch's current CUDA device in the library's runtime (marshalling)."""
+    import torch
+    _check(lib().rd_set_device(torch.cuda.current_device()))
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ host-side
+def rd_build_states(m: int):
+    """(N, words): the correct words of length m (Def 4), lexicographic a<b<c<d."""
+    n = ctypes.c_int64()
+    _check(lib().rd_build_states(m, None, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value * m)
+    _check(lib().rd_build_states(m, ctypes.cast(buf, ctypes.c_void_p), ctypes.byref(n)))
+    raw = buf.raw.decode()
+    return n.value, [raw[i * m:(i + 1) * m] for i in range(n.value)]
+
+
+def rd_build_matrix(m: int) -> np.ndarray:
+    """A(G) as int16 N x N (RD_INF off the arcs)."""
+    n = ctypes.c_int64()
+    _check(lib().rd_build_matrix(m, None, ctypes.byref(n)))
+    A = np.empty((n.value, n.value), dtype=np.int16)
+    _check(lib().rd_build_matrix(m, _np_ptr(A), ctypes.byref(n)))
+    return A
+
+
+def rd_stats_decide(stats, alpha_max: int, k: int, only_alpha: int = 0):
+    """(alpha, beta) if the reduced stats of power k show A^k = beta (x) A^{k-alpha}, else None."""
+    s = np.ascontiguousarray(np.asarray(stats, dtype=np.int32))
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    ok = lib().rd_stats_decide(_np_ptr(s), alpha_max, k, only_alpha, ctypes.byref(a), ctypes.byref(b))
+    return (a.value, b.value) if ok else None
+
+
+def rd_stats_len(alpha_max: int) -> int:
+    return lib().rd_stats_len(alpha_max)
+
+
+# ------------------------------------------------------------------ device-side
+def rd_minplus_mul(A, B, C=None):
+    """C = A (x) B for square int16 CUDA tensors (row-major), on torch's current stream."""
+    import torch
+    assert A.is_cuda and A.dtype == torch.int16 and A.is_contiguous() and A.dim() == 2
+    M, K = A.shape
+    K2, N = B.shape
+    assert K == K2 and B.dtype == torch.int16 and B.is_contiguous() and B.device == A.device
+    if C is None:
+        C = torch.empty((M, N), dtype=torch.int16, device=A.device)
+    _sync_device()
+    _check(lib().rd_minplus_mul_ex(A.data_ptr(), K, B.data_ptr(), N, C.data_ptr(), N, M, N, K,
+                                   _stream_ptr(None)))
+    return C
+
+
+def rd_minplus_mul_raw(A_ptr: int, B_ptr: int, C_ptr: int, N: int):
+    """The literal rd_minplus_mul(A, B, C, N) (device pointers, legacy default stream)."""
+    _sync_device()
+    _check(lib().rd_minplus_mul(A_ptr, B_ptr, C_ptr, N))
+
+
+def rd_minplus_mul_ex(A, lda, B, ldb, C, ldc, M, N, K, stream=None):
+    """Strided/rectangular form on torch tensors' data pointers."""
+    _sync_device()
+    _check(lib().rd_minplus_mul_ex(A.data_ptr(), lda, B.data_ptr(), ldb, C.data_ptr(), ldc, M, N, K,
+                                   _stream_ptr(stream)))
+    return C
+
+
+def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0):
+    """Algorithm 2 on the GPU: dict(found, n0, alpha, beta, k_stop, diag)."""
+    _sync_device()
+    out = _Period()
+    diag = np.zeros(kmax + 1, dtype=np.int32)
+    rc = _check(lib().rd_power_sequence_ex(m, kmax, alpha_max, policy, ctypes.byref(out), _np_ptr(diag)),
+                allow=(RD_OK, RD_NOTFOUND))
+    return dict(found=bool(out.found), n0=out.n0, alpha=out.alpha, beta=out.beta, k_stop=out.k_stop,
+                diag=[int(x) for x in diag], status=rc)
+
+
+def rd_roman_cylinder(m: int, n: int) -> int:
+    """gamma_R(P_m [] C_n)."""
+    _sync_device()
+    g = ctypes.c_int64()
+    _check(lib().rd_roman_cylinder(m, n, ctypes.byref(g)))
+    return g.value
+
+
+def rd_alu_probe():
+    """Measured integer issue rates on the current device (see rd.h)."""
+    _sync_device()
+    out = (ctypes.c_double * 4)()
+    _check(lib().rd_alu_probe(out))
+    return dict(dpx_warp_instr_per_clk_sm=out[0], dpx_minplus_per_clk_sm=out[1],
+                mixed_minplus_per_clk_sm=out[2], sm_mhz=out[3])
+
+
+class Chain:
+    """Rows [row_begin, row_end) of every power A^k of A(G) on the current device
+    (rd_chain_*).  step() enqueues A^{k+1} = A^k (x) A with the fused stats."""
+
+    def __init__(self, m: int, alpha_max: int = 10, row_begin: int = 0, row_end: int | None = None,
+                 stream=None):
+        import torch
+        _sync_device()
+        self.m, self.alpha_max = m, alpha_max
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        if row_end is None:
+            row_end = count_words(m)
+        self.row_begin, self.row_end = row_begin, row_end
+        h = ctypes.c_void_p()
+        _check(lib().rd_chain_create(m, alpha_max, row_begin, row_end, _stream_ptr(self.stream),
+                                     ctypes.byref(h)))
+        self._h = h
+        self.N = lib().rd_chain_order(h)
+        self.stats = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device="cuda")
+
+    @property
+    def k(self) -> int:
+        return lib().rd_chain_current_k(self._h)
+
+    def step(self, stats=None):
+        s = self.stats if stats is None else stats
+        _check(lib().rd_chain_step(self._h, ctypes.c_void_p(s.data_ptr())))
+        return s
+
+    def read_rows(self, k: int) -> np.ndarray:
+        out = np.empty((self.row_end - self.row_begin, self.N), dtype=np.int16)
+        _check(lib().rd_chain_read_rows(self._h, k, _np_ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rd_chain_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def count_words(m: int) -> int:
+    n = ctypes.c_int64()
+    _check(lib().rd_build_states(m, None, ctypes.byref(n)))
+    return n.value

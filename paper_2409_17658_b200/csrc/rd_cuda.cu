@@ -1,0 +1,671 @@
+// Device half of librd.so (sm_100a): the (min,+) GEMM on DPX integer instructions with
+// the fused diagonal-min / periodicity epilogue, the packing kernels, the power chain
+// and the C-ABI entry points that touch the GPU.
+//
+// Paper: arXiv 2409.17658 (PAPER.md as P:<line>).  The operation is the (min,+) product
+// c_ij = min_k (a_ik + b_kj) applied as A^{k+1} = A^k (x) A (Alg 2 step 3),
+// with the diagonal min of Cor 7 and the test A^k = beta (x) A^{k-alpha} of
+// Alg 2 step 4 / Prop 8 fused into the epilogue.
+//
+// Data layout: int16 entries, RD_INF = 0x3FFF = +inf.
+//   pair-major ("PM") u32 layout of a matrix X used as the LEFT operand:
+//       XT[t][i] = X[i][2t] | X[i][2t+1] << 16            (t = k-pair, i = row)
+//   packed RIGHT operand:  BP[t][j] = B[2t][j] | B[2t+1][j] << 16
+// Both are [K/2][rows-or-cols] u32 arrays, padded with INF to the CTA tile, so the
+// mainloop needs no predicates: one VIADDMNMX.S16x2 computes min(x_lo + b_lo, acc_lo)
+// and min(x_hi + b_hi, acc_hi) — two (min,+) terms (k = 2t and k = 2t+1) for one (i,j).
+// The accumulators start at INF; min(lo, hi) in the epilogue finishes the k-reduction.
+// The GEMM writes its output C = A^{k+1} directly in the PM layout (pairs along j), so
+// the output of one power step is the left operand of the next one.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "rd_internal.h"
+
+using namespace rd;
+
+#define RD_CUDA_CHECK(expr)                                                                     \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) return fail(RD_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                     \
+  } while (0)
+
+namespace {
+
+constexpr uint32_t kInf2 = 0x3FFF3FFFu;
+constexpr int kThreads = 256;
+constexpr int kBK2 = 16;      // k-pairs per pipeline stage (32 k)
+constexpr int kStages = 4;
+constexpr int kStageWords = 2 * kBK2 * kTile;   // u32 per stage (left + right tile)
+constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4;   // 64 KB
+
+// ------------------------------------------------------------------ packing --
+// Row-major int16 X (rows x cols, ld) -> PM u32 XT[cols_p/2][rows_p] (ld = rows_p).
+// 32x32 u32 tile transpose through shared memory.  Entries > RD_INF clamp to RD_INF;
+// everything outside (rows, cols) is INF.
+__global__ void pack_left_kernel(const int16_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+                                 int64_t row0, uint32_t *__restrict__ XT, int64_t ldt, int64_t tpairs) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t t0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    int64_t i = i0 + yy, t = t0 + tx;
+    uint32_t lo = RD_INF, hi = RD_INF;
+    if (i < rows) {
+      const int16_t *r = X + (row0 + i) * ld;
+      int64_t k = 2 * t;
+      if (k < cols) lo = (uint32_t)min((int)r[k], (int)RD_INF);
+      if (k + 1 < cols) hi = (uint32_t)min((int)r[k + 1], (int)RD_INF);
+    }
+    tile[yy][tx] = lo | (hi << 16);
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    int64_t t = t0 + yy, i = i0 + tx;
+    if (t < tpairs && i < ldt) XT[t * ldt + i] = tile[tx][yy];
+  }
+}
+
+// Row-major int16 B (K x N, ld) -> BP[t][j] = B[2t][j] | B[2t+1][j] << 16, padded with INF
+// to (tpairs x ldp).
+__global__ void pack_right_kernel(const int16_t *__restrict__ B, int64_t ld, int64_t K, int64_t N,
+                                  uint32_t *__restrict__ BP, int64_t ldp, int64_t tpairs) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t t = blockIdx.y;
+  if (j >= ldp || t >= tpairs) return;
+  uint32_t lo = RD_INF, hi = RD_INF;
+  if (j < N) {
+    if (2 * t < K) lo = (uint32_t)min((int)B[(2 * t) * ld + j], (int)RD_INF);
+    if (2 * t + 1 < K) hi = (uint32_t)min((int)B[(2 * t + 1) * ld + j], (int)RD_INF);
+  }
+  BP[t * ldp + j] = lo | (hi << 16);
+}
+
+// PM u32 XT[t][i] (ld = ldt) -> row-major int16 rows x cols (host-bound readback path).
+__global__ void unpack_pm_kernel(const uint32_t *__restrict__ XT, int64_t ldt, int64_t rows, int64_t cols,
+                                 int16_t *__restrict__ X) {
+  int64_t i = blockIdx.y;
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows || k >= cols) return;
+  uint32_t w = XT[(k >> 1) * ldt + i];
+  X[i * cols + k] = (int16_t)((k & 1) ? (w >> 16) : (w & 0xFFFF));
+}
+
+__global__ void fill_u32_kernel(uint32_t *p, int64_t n, uint32_t v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// MIN-reducible neutral stats: diag INT_MAX, lo INT_MAX, -hi INT_MAX, -mis 0, -fin 0.
+__global__ void stats_init_kernel(int32_t *s, int alpha_max) {
+  int i = threadIdx.x;
+  int n = 1 + 4 * alpha_max;
+  if (i >= n) return;
+  int q = (i - 1) & 3;
+  s[i] = (i == 0 || q == 0 || q == 1) ? INT_MAX : 0;
+}
+
+// --------------------------------------------------------------------- GEMM --
+struct EpiArgs {
+  const uint32_t *prev[kMaxAlpha];  // PM slots of A^{k+1-a}, a = 1..nprev, same ld as C
+  int nprev;
+  int32_t *stats;          // MIN-reducible stats vector (nullable: no stats)
+  int64_t diag_row0;       // global row index of local row 0 (row panels)
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// One CTA computes a 128 x 128 tile of C; 256 threads in a 16 x 16 grid, each thread an
+// 8 x 8 register micro-tile: rows {ty*4 + 0..3, 64 + ty*4 + 0..3}, columns
+// {tx*4 + 0..3, 64 + tx*4 + 0..3}.  Per k-pair a thread reads 4 x LDS.128 and issues 64
+// VIADDMNMX.S16x2 (128 (min,+) terms).
+//   OUT_PM = true : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
+//   OUT_PM = false: C is row-major int16 with ldc, predicated to (M, N).
+template <bool OUT_PM, bool STATS>
+__global__ void __launch_bounds__(kThreads, 2)
+minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
+                    int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
+                    EpiArgs epi) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t j0 = (int64_t)blockIdx.x * kTile, i0 = (int64_t)blockIdx.y * kTile;
+
+  // cp.async mapping: 512 16-byte chunks per operand tile (16 rows x 32 chunks)
+  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
+  const uint32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
+  const uint32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
+  const int64_t gx_step8 = 8 * ldx, gb_step8 = 8 * ldb;
+
+  auto load_stage = [&](int stage, int kb) {
+    uint32_t *sx = smem + stage * kStageWords;
+    uint32_t *sb = sx + kBK2 * kTile;
+    const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
+    cp_async16(sx + ld_row * kTile + ld_col, gx + ox);
+    cp_async16(sx + (ld_row + 8) * kTile + ld_col, gx + ox + gx_step8);
+    cp_async16(sb + ld_row * kTile + ld_col, gb + ob);
+    cp_async16(sb + (ld_row + 8) * kTile + ld_col, gb + ob + gb_step8);
+  };
+
+  uint32_t acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
+
+  const int KB = kpairs / kBK2;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < KB) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kb = 0; kb < KB; ++kb) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      int nk = kb + kStages - 1;
+      if (nk < KB) load_stage(nk % kStages, nk);
+      cp_async_commit();
+    }
+    const uint32_t *sx = smem + (kb % kStages) * kStageWords;
+    const uint32_t *sb = sx + kBK2 * kTile;
+#pragma unroll
+    for (int t = 0; t < kBK2; ++t) {
+      const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
+      const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
+      const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
+      const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
+      const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---------------------------------------------------------------- epilogue --
+  // v = min(lo, hi) per accumulator; pairs (c, c+1) packed (min_c | min_{c+1} << 16).
+  uint32_t out[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      uint32_t a0 = acc[r][2 * p], a1 = acc[r][2 * p + 1];
+      out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
+    }
+
+  if (OUT_PM) {
+    uint32_t *C = reinterpret_cast<uint32_t *>(Cv);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        // column pair jp covers columns j0 + (p>>1)*64 + tx*4 + (p&1)*2 + {0,1}
+        int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+        uint4 v = make_uint4(out[g * 4 + 0][p], out[g * 4 + 1][p], out[g * 4 + 2][p], out[g * 4 + 3][p]);
+        *reinterpret_cast<uint4 *>(C + jp * ldc + i0 + g * 64 + ty * 4) = v;
+      }
+  } else {
+    int16_t *C = reinterpret_cast<int16_t *>(Cv);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+      if (i >= M) continue;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2;
+        if (j < N) C[i * ldc + j] = (int16_t)(out[r][p] & 0xFFFF);
+        if (j + 1 < N) C[i * ldc + j + 1] = (int16_t)(out[r][p] >> 16);
+      }
+    }
+  }
+
+  if (!STATS) return;
+
+  // ---- fused reductions over this tile (MIN-reducible; see rd.h rd_chain_step) ----
+  __shared__ int32_t red[kThreads / 32][1 + 4 * kMaxAlpha];
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // diagonal min (Cor 7): global row diag_row0 + i == column j
+  int32_t dmin = INT_MAX;
+  {
+    const int64_t gi0 = epi.diag_row0 + i0;
+    if (gi0 < j0 + kTile && j0 < gi0 + kTile) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int64_t gi = gi0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+            int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2 + h;
+            int32_t v = (int32_t)((out[r][p] >> (16 * h)) & 0xFFFF);
+            if (gi == j && v < dmin) dmin = v;
+          }
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+
+  // periodicity stats against A^{k+1-a}: same PM address in the previous slots
+  for (int a = 0; a < epi.nprev; ++a) {
+    const uint32_t *P = epi.prev[a];
+    uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+        uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
+        const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t o = out[g * 4 + q][p], w = pw[q];
+          uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
+          mis |= eo ^ ew;
+          uint32_t fm = ~(eo | ew);
+          fin |= fm;
+          uint32_t d = __vsub2(o, w);
+          lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
+          hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
+        }
+      }
+    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
+    if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
+    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
+    int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
+    if (lane == 0) {
+      red[warp][1 + 4 * a + 0] = v0;
+      red[warp][1 + 4 * a + 1] = v1;
+      red[warp][1 + 4 * a + 2] = v2;
+      red[warp][1 + 4 * a + 3] = v3;
+    }
+  }
+  __syncthreads();
+  const int nval = 1 + 4 * epi.nprev;
+  for (int e = tid; e < nval; e += kThreads) {
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) v = min(v, red[w][e]);
+    atomicMin(epi.stats + e, v);
+  }
+}
+
+template <bool OUT_PM, bool STATS>
+int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
+                int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
+                cudaStream_t st) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT_PM, STATS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  dim3 grid((unsigned)(Np / kTile), (unsigned)(Mp / kTile));
+  minplus_gemm_kernel<OUT_PM, STATS><<<grid, kThreads, kSmemBytes, st>>>(XT, ldx, BP, ldb, (int)kpairs, C, ldc,
+                                                                          M, N, epi);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+int pack_left(const int16_t *X, int64_t ld, int64_t rows, int64_t cols, int64_t row0, uint32_t *XT,
+              int64_t ldt, int64_t tpairs, cudaStream_t st) {
+  dim3 grid((unsigned)((tpairs + 31) / 32), (unsigned)((ldt + 31) / 32));
+  pack_left_kernel<<<grid, dim3(32, 8), 0, st>>>(X, ld, rows, cols, row0, XT, ldt, tpairs);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP, int64_t ldp, int64_t tpairs,
+               cudaStream_t st) {
+  dim3 grid((unsigned)((ldp + 255) / 256), (unsigned)tpairs);
+  pack_right_kernel<<<grid, 256, 0, st>>>(B, ld, K, N, BP, ldp, tpairs);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+}  // namespace
+
+extern "C" int rd_set_device(int device) {
+  clear_error();
+  RD_CUDA_CHECK(cudaSetDevice(device));
+  return RD_OK;
+}
+
+// =========================================================== generic product ==
+extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
+                                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+  clear_error();
+  if (!A || !B || !C) return fail(RD_EINVAL, "rd_minplus_mul_ex: NULL pointer");
+  if (M < 1 || N < 1 || K < 1) return fail(RD_EINVAL, "rd_minplus_mul_ex: M, N, K must be >= 1");
+  if (lda < K || ldb < N || ldc < N) return fail(RD_EINVAL, "rd_minplus_mul_ex: leading dimension too small");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, 2 * kBK2);
+  const int64_t kpairs = Kp / 2;
+  uint32_t *XT = nullptr, *BP = nullptr;
+  RD_CUDA_CHECK(cudaMallocAsync((void **)&XT, (size_t)(kpairs * Mp * 4), st));
+  cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(kpairs * Np * 4), st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(XT, st);
+    return fail(RD_ENOMEM, "rd_minplus_mul_ex: workspace: %s", cudaGetErrorString(e));
+  }
+  int rc = pack_left(A, lda, M, K, 0, XT, Mp, kpairs, st);
+  if (rc == RD_OK) rc = pack_right(B, ldb, K, N, BP, Np, kpairs, st);
+  EpiArgs epi{};
+  if (rc == RD_OK) rc = launch_gemm<false, false>(XT, Mp, BP, Np, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+  cudaFreeAsync(XT, st);
+  cudaFreeAsync(BP, st);
+  return rc;
+}
+
+extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N) {
+  if (!A || !B || !C) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: NULL pointer"); }
+  if (N < 1) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: N must be >= 1"); }
+  if (C == A || C == B) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: C aliases an input"); }
+  return rd_minplus_mul_ex(A, N, B, N, C, N, N, N, N, nullptr);
+}
+
+// ================================================================ power chain ==
+struct rd_chain {
+  int m = 0, alpha_max = 0, k = 0, device = 0;
+  int64_t N = 0, P = 0, r0 = 0, r1 = 0, Mr = 0, Mp = 0;
+  cudaStream_t st = nullptr;
+  uint32_t *BP = nullptr;    // packed A, [P/2][P]
+  uint32_t *ring = nullptr;  // (alpha_max+1) PM slots, each [P/2][Mp]
+  int64_t slot_words = 0;
+  int32_t diag1 = INT32_MAX;  // min_p A_pp (self-loop labels), for diag[1]
+  uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
+};
+
+extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
+                               rd_chain **out) {
+  clear_error();
+  if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
+  *out = nullptr;
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
+  if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_chain_create: alpha_max out of 1..32");
+  const int64_t N = count_words(m);
+  if (row_begin < 0 || row_end > N || row_begin >= row_end)
+    return fail(RD_EINVAL, "rd_chain_create: bad row range [%lld, %lld) for N=%lld", (long long)row_begin,
+                (long long)row_end, (long long)N);
+  rd_chain *c = new rd_chain;
+  c->m = m;
+  c->alpha_max = alpha_max;
+  c->N = N;
+  c->P = round_up(N, kTile);
+  c->r0 = row_begin;
+  c->r1 = row_end;
+  c->Mr = row_end - row_begin;
+  c->Mp = round_up(c->Mr, kTile);
+  c->st = (cudaStream_t)cuda_stream;
+  cudaGetDevice(&c->device);
+  c->slot_words = (c->P / 2) * c->Mp;
+
+  std::vector<int16_t> A((size_t)(N * N));
+  int rc = build_matrix(m, A.data(), N);
+  if (rc != RD_OK) { delete c; return rc; }
+  for (int64_t p = c->r0; p < c->r1; ++p)
+    if (A[p * N + p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, A[p * N + p]);
+
+  int16_t *dA = nullptr;
+  auto cleanup = [&](int code) {
+    if (dA) cudaFree(dA);
+    if (c->BP) cudaFree(c->BP);
+    if (c->ring) cudaFree(c->ring);
+    delete c;
+    return code;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
+      (e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
+      (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
+    return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
+  if ((e = cudaMemcpyAsync(dA, A.data(), (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+    return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
+  // every ring slot starts all-INF (slots are compared before they are first written)
+  {
+    int64_t n = (alpha_max + 1) * c->slot_words;
+    fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
+  }
+  rc = pack_right(dA, N, N, N, c->BP, c->P, c->P / 2, c->st);
+  if (rc == RD_OK) rc = pack_left(dA, N, c->Mr, N, c->r0, c->slot(1), c->Mp, c->P / 2, c->st);
+  if (rc == RD_OK && (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
+    rc = fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e));
+  cudaFree(dA);
+  dA = nullptr;
+  if (rc != RD_OK) return cleanup(rc);
+  c->k = 1;
+  *out = c;
+  return RD_OK;
+}
+
+extern "C" int rd_chain_destroy(rd_chain *c) {
+  if (!c) return RD_OK;
+  if (c->BP) cudaFree(c->BP);
+  if (c->ring) cudaFree(c->ring);
+  delete c;
+  return RD_OK;
+}
+
+extern "C" int64_t rd_chain_order(const rd_chain *c) { return c ? c->N : -1; }
+extern "C" int rd_chain_current_k(const rd_chain *c) { return c ? c->k : -1; }
+
+extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
+  clear_error();
+  if (!c || !stats_dev) return fail(RD_EINVAL, "rd_chain_step: NULL argument");
+  const int knew = c->k + 1;
+  EpiArgs epi{};
+  epi.nprev = std::min(c->alpha_max, knew - 1);
+  for (int a = 1; a <= epi.nprev; ++a) epi.prev[a - 1] = c->slot(knew - a);
+  epi.stats = stats_dev;
+  epi.diag_row0 = c->r0;
+  stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
+  RD_CUDA_CHECK(cudaGetLastError());
+  int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
+                                   c->N, c->Mp, c->P, epi, c->st);
+  if (rc != RD_OK) return rc;
+  c->k = knew;
+  return RD_OK;
+}
+
+extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
+  clear_error();
+  if (!c || !host_out) return fail(RD_EINVAL, "rd_chain_read_rows: NULL argument");
+  if (k < 1 || k > c->k || k < c->k - c->alpha_max)
+    return fail(RD_EINVAL, "rd_chain_read_rows: power %d not in the ring (current %d)", k, c->k);
+  int16_t *d = nullptr;
+  RD_CUDA_CHECK(cudaMallocAsync((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
+  dim3 grid((unsigned)((c->N + 255) / 256), (unsigned)c->Mr);
+  unpack_pm_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->Mp, c->Mr, c->N, d);
+  cudaError_t e = cudaMemcpyAsync(host_out, d, (size_t)(c->Mr * c->N * 2), cudaMemcpyDeviceToHost, c->st);
+  cudaFreeAsync(d, c->st);
+  if (e != cudaSuccess) return fail(RD_ECUDA, "rd_chain_read_rows: %s", cudaGetErrorString(e));
+  RD_CUDA_CHECK(cudaStreamSynchronize(c->st));
+  return RD_OK;
+}
+
+// ============================================================ power sequence ==
+extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out,
+                                    int32_t *diag) {
+  clear_error();
+  if (!out) return fail(RD_EINVAL, "rd_power_sequence: out is NULL");
+  *out = rd_period_t{0, 0, 0, 0, 0};
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
+  if (kmax < 2) return fail(RD_EINVAL, "rd_power_sequence: kmax=%d < 2", kmax);
+  if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_power_sequence: alpha_max out of range");
+  if (policy != 0 && policy != 1) return fail(RD_EINVAL, "rd_power_sequence: policy must be 0 or 1");
+  if ((int64_t)2 * m * kmax >= RD_INF)
+    return fail(RD_ERANGE, "rd_power_sequence: 2*m*kmax = %d exceeds the int16 headroom", 2 * m * kmax);
+  if (diag)
+    for (int k = 0; k <= kmax; ++k) diag[k] = INT32_MAX;
+
+  const int64_t N = count_words(m);
+  cudaStream_t st;
+  RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  rd_chain *c = nullptr;
+  int rc = rd_chain_create(m, alpha_max, 0, N, st, &c);
+  if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
+
+  const int slen = rd_stats_len(alpha_max);
+  int32_t *dstats = nullptr, *hstats = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc((void **)&dstats, (size_t)slen * 4)) != cudaSuccess ||
+      (e = cudaMallocHost((void **)&hstats, (size_t)slen * 4)) != cudaSuccess) {
+    rd_chain_destroy(c);
+    cudaStreamDestroy(st);
+    if (dstats) cudaFree(dstats);
+    return fail(RD_ENOMEM, "rd_power_sequence: %s", cudaGetErrorString(e));
+  }
+  if (diag) diag[1] = c->diag1;  // min_p A_pp: the self-loop labels
+  int found_k = -1, n0 = 0, al = 0, be = 0, k = 1;
+  rc = RD_OK;
+  for (k = 2; k <= kmax; ++k) {
+    if ((rc = rd_chain_step(c, dstats)) != RD_OK) break;
+    if ((e = cudaMemcpyAsync(hstats, dstats, (size_t)slen * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      rc = fail(RD_ECUDA, "rd_power_sequence: step %d: %s", k, cudaGetErrorString(e));
+      break;
+    }
+    if (diag) diag[k] = hstats[0] >= RD_INF ? INT32_MAX : hstats[0];
+    int32_t a = 0, b = 0;
+    if (found_k < 0) {
+      if (rd_stats_decide(hstats, alpha_max, k, 0, &a, &b)) {
+        found_k = k; n0 = k - a; al = a; be = b;
+        if (policy == 0) break;
+      }
+    } else {
+      int aa = k - n0;
+      if (aa <= alpha_max && rd_stats_decide(hstats, alpha_max, k, aa, &a, &b)) { al = a; be = b; }
+      if (aa >= alpha_max) break;
+    }
+  }
+  int k_stop = std::min(k, kmax);
+  cudaFree(dstats);
+  cudaFreeHost(hstats);
+  rd_chain_destroy(c);
+  cudaStreamDestroy(st);
+  if (rc != RD_OK) return rc;
+  out->k_stop = k_stop;
+  if (found_k >= 0) {
+    out->found = 1; out->n0 = n0; out->alpha = al; out->beta = be;
+    return RD_OK;
+  }
+  return RD_NOTFOUND;
+}
+
+extern "C" int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag) {
+  return rd_power_sequence_ex(m, kmax, 10, 0, out, diag);
+}
+
+// ================================================================ ALU probe ==
+namespace {
+#define RD_OPQ(x) asm volatile("" : "+r"(x))
+template <int MODE>
+__global__ void __launch_bounds__(256) alu_probe_kernel(uint32_t *sink, long long *cyc, int iters, uint32_t seed) {
+  uint32_t c[32], xa0[4], xa1[4], yb0[8], yb1[8];
+  uint32_t x0 = (seed ^ threadIdx.x) & 0x000F000Fu;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { xa0[q] = x0 + q; xa1[q] = x0 + 2 * q + 1; }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { yb0[q] = x0 + 3 * q; yb1[q] = x0 + 5 * q + 2; }
+#pragma unroll
+  for (int u = 0; u < 32; ++u) c[u] = 0x10001000u + u;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { RD_OPQ(xa0[q]); RD_OPQ(xa1[q]); }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { RD_OPQ(yb0[q]); RD_OPQ(yb1[q]); }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int i = u >> 3, j = u & 7;
+      if (MODE == 0) {
+        c[u] = __viaddmin_s16x2(xa0[i], yb0[j], c[u]);
+      } else {
+        uint32_t s1 = xa0[i] + yb0[j], s2 = xa1[i] + yb1[j];
+        c[u] = __vimin3_s16x2(c[u], s1, s2);
+      }
+    }
+  }
+  long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int u = 0; u < 32; ++u) acc ^= c[u];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int MODE>
+int probe_one(int sms, double *minplus_per_clk_sm, double *mhz, double *instr_per_clk_sm) {
+  const int blocks = sms * 4, threads = 256, iters = 4096;
+  uint32_t *sink = nullptr;
+  long long *cyc = nullptr;
+  RD_CUDA_CHECK(cudaMalloc(&sink, (size_t)blocks * threads * 4));
+  RD_CUDA_CHECK(cudaMalloc(&cyc, (size_t)blocks * 8));
+  alu_probe_kernel<MODE><<<blocks, threads>>>(sink, cyc, 16, 1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  alu_probe_kernel<MODE><<<blocks, threads>>>(sink, cyc, iters, 12345);
+  cudaEventRecord(e1);
+  RD_CUDA_CHECK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<long long> h(blocks);
+  RD_CUDA_CHECK(cudaMemcpy(h.data(), cyc, (size_t)blocks * 8, cudaMemcpyDeviceToHost));
+  long long mx = *std::max_element(h.begin(), h.end());
+  const double per_u = MODE == 0 ? 2.0 : 4.0;  // (min,+) lane-terms per u per iteration
+  *minplus_per_clk_sm = (double)iters * 32 * per_u * threads * 4 / (double)mx;
+  *instr_per_clk_sm = (double)iters * 32 * (threads / 32) * 4 / (double)mx;
+  *mhz = (double)mx / (ms * 1e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  cudaFree(cyc);
+  return RD_OK;
+}
+}  // namespace
+
+extern "C" int rd_alu_probe(double out[4]) {
+  clear_error();
+  if (!out) return fail(RD_EINVAL, "rd_alu_probe: NULL");
+  int dev = 0, sms = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  RD_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double mp0, mhz0, ipc0, mp1, mhz1, ipc1;
+  int rc = probe_one<0>(sms, &mp0, &mhz0, &ipc0);
+  if (rc == RD_OK) rc = probe_one<1>(sms, &mp1, &mhz1, &ipc1);
+  if (rc != RD_OK) return rc;
+  out[0] = ipc0;
+  out[1] = mp0;
+  out[2] = mp1;
+  out[3] = 0.5 * (mhz0 + mhz1);
+  return RD_OK;
+}

@@ -1,0 +1,216 @@
+// Host half of librd.so: word enumeration and A(G) construction (not hot), error
+// strings, the periodicity decision on a reduced stats vector, and the gamma_R
+// extension by the recurrence.  The device half is rd_cuda.cu.
+//
+// Paper: arXiv 2409.17658, PAPER.md line numbers as P:<line>.
+#include <algorithm>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rd_internal.h"
+
+namespace rd {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+void clear_error() { g_err.clear(); }
+
+// Letters as digits: a=0 b=1 c=2 d=3.  Def 4: no ad, da, ab, ba, bb.
+static inline bool adjacent_ok(int x, int y) {
+  return !((x == 0 && y == 3) || (x == 3 && y == 0) || (x == 0 && y == 1) || (x == 1 && y == 0) ||
+           (x == 1 && y == 1));
+}
+
+// Depth-first generation in lexicographic order: digit i (row i+1) is appended only if
+// it may follow digit i-1 inside the word.
+static void dfs_words(int m, int i, uint32_t code, int last, std::vector<uint32_t> &out) {
+  if (i == m) {
+    out.push_back(code);
+    return;
+  }
+  for (int x = 0; x < 4; ++x)
+    if (i == 0 || adjacent_ok(last, x)) dfs_words(m, i + 1, code * 4 + x, x, out);
+}
+
+std::vector<uint32_t> word_codes(int m) {
+  std::vector<uint32_t> out;
+  if (m >= 1 && m <= 12) dfs_words(m, 0, 0, -1, out);
+  return out;
+}
+
+int64_t count_words(int m) {
+  if (m < 1 || m > 12) return -1;
+  // C_m by transfer counting over the last letter (same language as dfs_words).
+  int64_t cnt[4] = {1, 1, 1, 1};
+  for (int i = 1; i < m; ++i) {
+    int64_t nx[4] = {0, 0, 0, 0};
+    for (int x = 0; x < 4; ++x)
+      for (int y = 0; y < 4; ++y)
+        if (adjacent_ok(x, y)) nx[y] += cnt[x];
+    std::memcpy(cnt, nx, sizeof cnt);
+  }
+  return cnt[0] + cnt[1] + cnt[2] + cnt[3];
+}
+
+// Successors of q: p_i is chosen row by row.  Allowed p_i given q_i:
+//   q_i = a: a, c        q_i = b: d, or c if p has an `a` vertically adjacent to row i
+//   q_i = c: a, b, d, or c with the same vertical condition        q_i = d: a
+// (intermediate rows read "p_i = d", R1; first/last rows have one vertical
+// neighbour, m = 1 none, R2).  The vertical condition of row i is settled once p_{i+1}
+// is known (or at the end).  Label 2 p(a) + p(b).
+struct SuccGen {
+  int m;
+  const int *q;  // digits of q
+  const int32_t *index_of_code;
+  int16_t *row;  // A[q][*]
+  int p[16];
+  void go(int i, uint32_t code, int na, int nb) {
+    if (i == m) {
+      // last row's pending vertical condition: p_{m-1} (row m-1, 0-based m-2) must be a
+      if (needs_vertical(m - 1) && !(m >= 2 && p[m - 2] == 0)) return;
+      int32_t idx = index_of_code[code];
+      row[idx] = (int16_t)(2 * na + nb);
+      return;
+    }
+    static const int cand[4][4] = {{0, 2, -1, -1}, {2, 3, -1, -1}, {0, 1, 2, 3}, {0, -1, -1, -1}};
+    for (int t = 0; t < 4; ++t) {
+      int x = cand[q[i]][t];
+      if (x < 0) break;
+      if (i > 0 && !adjacent_ok(p[i - 1], x)) continue;  // p must be a correct word
+      p[i] = x;
+      // settle row i-1's vertical condition now that p_i is known
+      if (i >= 1 && needs_vertical(i - 1)) {
+        bool up = (i - 2 >= 0) && p[i - 2] == 0;
+        bool dn = (x == 0);
+        if (!up && !dn) continue;
+      }
+      go(i + 1, code * 4 + x, na + (x == 0), nb + (x == 1));
+    }
+  }
+  // row r's p_r = c with q_r in {b, c} needs an `a` above or below in p
+  bool needs_vertical(int r) const { return p[r] == 2 && (q[r] == 1 || q[r] == 2); }
+};
+
+int build_matrix(int m, int16_t *A, int64_t N) {
+  std::vector<uint32_t> codes = word_codes(m);
+  if ((int64_t)codes.size() != N) return fail(RD_EINVAL, "word count mismatch");
+  std::vector<int32_t> index_of_code((size_t)1 << (2 * m), -1);
+  for (int64_t w = 0; w < N; ++w) index_of_code[codes[w]] = (int32_t)w;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t q = 0; q < N; ++q) {
+    int16_t *row = A + q * N;
+    std::fill(row, row + N, RD_INF);
+    int qd[16];
+    for (int i = 0; i < m; ++i) qd[i] = (codes[q] >> (2 * (m - 1 - i))) & 3;
+    SuccGen g{m, qd, index_of_code.data(), row, {}};
+    g.go(0, 0, 0, 0);
+  }
+  return RD_OK;
+}
+
+}  // namespace rd
+
+using namespace rd;
+
+extern "C" const char *rd_last_error(void) { return g_err.c_str(); }
+
+extern "C" int rd_build_states(int m, char *words, int64_t *N_out) {
+  clear_error();
+  if (!N_out) return fail(RD_EINVAL, "rd_build_states: N_out is NULL");
+  if (m < 1 || m > 12) return fail(RD_EINVAL, "rd_build_states: m=%d out of range 1..12", m);
+  std::vector<uint32_t> codes = word_codes(m);
+  *N_out = (int64_t)codes.size();
+  if (words)
+    for (size_t w = 0; w < codes.size(); ++w)
+      for (int i = 0; i < m; ++i) words[w * m + i] = (char)('a' + ((codes[w] >> (2 * (m - 1 - i))) & 3));
+  return RD_OK;
+}
+
+extern "C" int rd_build_matrix(int m, int16_t *A, int64_t *N_out) {
+  clear_error();
+  if (!N_out) return fail(RD_EINVAL, "rd_build_matrix: N_out is NULL");
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_build_matrix: m=%d out of range 1..11", m);
+  int64_t N = count_words(m);
+  *N_out = N;
+  if (!A) return RD_OK;
+  return build_matrix(m, A, N);
+}
+
+extern "C" int rd_stats_len(int alpha_max) { return 1 + 4 * alpha_max; }
+
+// Prop 8 / Alg 2 step 4 on the reduced stats: A^k = beta (x) A^{k-a} iff the inf
+// patterns agree (mis = 0), some entry is finite (fin = 1) and all finite differences
+// are equal (lo = hi), beta = lo >= 0.
+extern "C" int rd_stats_decide(const int32_t *s, int alpha_max, int k, int only_alpha, int32_t *alpha,
+                               int32_t *beta) {
+  if (!s || alpha_max < 1) return 0;
+  int amax = std::min(alpha_max, k - 1);
+  for (int a = 1; a <= amax; ++a) {
+    if (only_alpha > 0 && a != only_alpha) continue;
+    const int32_t *e = s + 1 + 4 * (a - 1);
+    int32_t lo = e[0];
+    int64_t hi = -(int64_t)e[1];
+    bool mis = e[2] != 0, fin = e[3] != 0;
+    if (!mis && fin && (int64_t)lo == hi && lo >= 0) {
+      if (alpha) *alpha = a;
+      if (beta) *beta = lo;
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// gamma_R via Cor 7 and Prop 8, chains cached per m.
+namespace {
+struct Cached {
+  rd_period_t per;
+  std::vector<int32_t> diag;
+};
+std::mutex g_cache_mu;
+std::map<int, Cached> g_cache;
+}  // namespace
+
+extern "C" int rd_roman_cylinder(int m, int64_t n, int64_t *gamma) {
+  clear_error();
+  if (!gamma) return fail(RD_EINVAL, "rd_roman_cylinder: gamma is NULL");
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_roman_cylinder: m=%d out of range", m);
+  if (n < 3) return fail(RD_EINVAL, "rd_roman_cylinder: n=%lld < 3 (P:21)", (long long)n);
+  Cached c;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(m);
+    if (it != g_cache.end()) c = it->second;
+  }
+  if (c.diag.empty()) {
+    const int kmax = 50;
+    c.diag.assign(kmax + 1, INT32_MAX);
+    int rc = rd_power_sequence(m, kmax, &c.per, c.diag.data());
+    if (rc < 0) return rc;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[m] = c;
+  }
+  if (n <= c.per.k_stop) {
+    *gamma = c.diag[n];
+    return RD_OK;
+  }
+  if (!c.per.found) return fail(RD_NOTFOUND, "no recurrence found for m=%d within k=50", m);
+  int64_t n0 = c.per.n0, a = c.per.alpha, b = c.per.beta;
+  int64_t np = n0 + (n - n0) % a;  // n0 <= np < n0 + a <= k_stop
+  *gamma = (int64_t)c.diag[np] + b * ((n - np) / a);
+  return RD_OK;
+}

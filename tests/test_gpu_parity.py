@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by element.
+
+Integer work, so the bar is bit-exact everywhere.  Infinity is
+RD_INF = 0x3FFF on the product side and INT32_MAX in the oracle; the tests re-encode.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from rd_inputs import operand, power_like, sample_rows, sparse_like, to_inf
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2409_17658_b200 as rd  # noqa: E402
+
+OINF = int(O.INF)
+RINF = rd.RD_INF
+
+
+def _gpu(X):
+    return torch.from_numpy(np.ascontiguousarray(X)).cuda()
+
+
+def _oracle_mul(A16, B16, transpose=False):
+    A = to_inf(A16, RINF, OINF, np.int32)
+    B = to_inf(B16, RINF, OINF, np.int32)
+    C = O.minplus_bt(A, np.ascontiguousarray(B.T)) if transpose else O.minplus(A, B)
+    return to_inf(C, OINF, RINF, np.int16)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+
+
+# ------------------------------------------------------------- generic product
+@pytest.mark.parametrize("N", [1, 2, 31, 32, 33, 127, 128, 129, 255, 287, 300, 848])
+@pytest.mark.parametrize("inf_frac", [0.0, 0.01, 0.5, 1.0])
+def test_minplus_mul_random(N, inf_frac):
+    A = operand(N, N, seed=N * 7 + 1, inf_frac=inf_frac)
+    B = operand(N, N, seed=N * 7 + 2, inf_frac=inf_frac)
+    C = rd.rd_minplus_mul(_gpu(A), _gpu(B)).cpu().numpy()
+    assert (C == _oracle_mul(A, B)).all()
+
+
+def test_minplus_mul_raw_pointer_form():
+    N = 200
+    A, B = operand(N, N, 11), operand(N, N, 12)
+    dA, dB = _gpu(A), _gpu(B)
+    dC = torch.empty((N, N), dtype=torch.int16, device="cuda")
+    torch.cuda.synchronize()
+    rd.rd_minplus_mul_raw(dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), N)
+    torch.cuda.synchronize()
+    assert (dC.cpu().numpy() == _oracle_mul(A, B)).all()
+
+
+def test_minplus_mul_headroom_and_clamp():
+    # max finite entries (RD_INF - 1) and entries above RD_INF (clamped on load)
+    N = 130
+    A = operand(N, N, 21, inf_frac=0.1, lo=RINF - 10, hi=RINF - 1)
+    B = operand(N, N, 22, inf_frac=0.1, lo=0, hi=5)
+    C = rd.rd_minplus_mul(_gpu(A), _gpu(B)).cpu().numpy()
+    want = _oracle_mul(A, B)
+    want[want.astype(np.int64) >= RINF] = RINF   # sums >= RD_INF saturate to +inf
+    assert (C == want).all()
+    A2 = A.copy(); A2[0, :] = 0x7000                # > RD_INF: treated as +inf
+    C2 = rd.rd_minplus_mul(_gpu(A2), _gpu(B)).cpu().numpy()
+    assert (C2[0] == RINF).all()
+
+
+def test_all_inf_rows_and_columns():
+    N = 257
+    A = operand(N, N, 31, inf_frac=0.2, hi=50)
+    B = operand(N, N, 32, inf_frac=0.2, hi=50)
+    A[5, :] = RINF; A[:, 7] = RINF; B[:, 9] = RINF; B[3, :] = RINF
+    C = rd.rd_minplus_mul(_gpu(A), _gpu(B)).cpu().numpy()
+    assert (C == _oracle_mul(A, B)).all()
+    assert (C[5] == RINF).all() and (C[:, 9] == RINF).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (5, 300, 7), (300, 5, 129), (129, 257, 1000), (1000, 33, 33)])
+def test_minplus_mul_ex_rectangular_strided(M, N, K):
+    A = operand(M, K + 3, 41 + M)
+    B = operand(K, N + 5, 42 + N)
+    dA, dB = _gpu(A), _gpu(B)
+    dC = torch.full((M, N + 2), -7, dtype=torch.int16, device="cuda")
+    rd.rd_minplus_mul_ex(dA, K + 3, dB, N + 5, dC, N + 2, M, N, K)
+    C = dC.cpu().numpy()
+    assert (C[:, :N] == _oracle_mul(A[:, :K], B[:, :N])).all()
+    assert (C[:, N:] == -7).all()    # nothing written outside the N columns
+
+
+def test_minplus_mul_power_like_and_sparse_operands():
+    for m, N in ((7, 2507),):
+        X = power_like(N, N, m, seed=5)
+        B = sparse_like(N, m, seed=6)
+        C = rd.rd_minplus_mul(_gpu(X), _gpu(B)).cpu().numpy()
+        rows = sample_rows(N, 96, seed=7)
+        want = _oracle_mul(X[rows], B, transpose=True)
+        assert (C[rows] == want).all()
+
+
+def test_minplus_mul_large_sampled_rows():
+    # C_9-sized product at the launch shape the chain uses, sampled rows vs the oracle
+    N = 21909
+    A = operand(N, N, 51, inf_frac=0.01, hi=1000)
+    B = operand(N, N, 52, inf_frac=0.01, hi=1000)
+    C = rd.rd_minplus_mul(_gpu(A), _gpu(B))
+    rows = sample_rows(N, 24, seed=53)
+    got = C[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert (got == _oracle_mul(A[rows], B, transpose=True)).all()
+
+
+# ---------------------------------------------------------------- power chain
+def _oracle_powers(m, kmax):
+    return {k: to_inf(X, OINF, RINF, np.int16) for k, X in O.powers(m, kmax)}
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7])
+def test_chain_every_power_bit_exact(m):
+    ref = O.power_chain(m, 50, 10, 0)
+    kstop = ref["k_stop"]
+    P = _oracle_powers(m, kstop)
+    ch = rd.Chain(m, alpha_max=10)
+    assert (ch.read_rows(1) == P[1]).all()
+    for k in range(2, kstop + 1):
+        s = ch.step()
+        got = ch.read_rows(k)
+        assert (got == P[k]).all(), (m, k)
+        st = s.cpu().numpy()
+        d = int(np.diag(P[k]).min())
+        assert st[0] == (d if d < RINF else min(d, RINF)), (m, k)
+        # every alpha's stats against the oracle's shift test
+        for a in range(1, min(10, k - 1) + 1):
+            b = O.shift(to_inf(P[k], RINF, OINF, np.int32), to_inf(P[k - a], RINF, OINF, np.int32))
+            dec = rd.rd_stats_decide(st, 10, k, only_alpha=a)
+            assert (dec[1] if dec else None) == b, (m, k, a)
+    ch.close()
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_power_sequence_matches_oracle(m):
+    ref = O.power_chain(m, 50, 10, 0)
+    got = rd.rd_power_sequence(m, 50)
+    for key in ("found", "n0", "alpha", "beta", "k_stop"):
+        assert got[key] == ref[key], (m, key)
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7])
+def test_power_sequence_paper_compat_table2(m, golden):
+    g = golden("table2_periods.json")["table2"][str(m)]
+    got = rd.rd_power_sequence(m, 50, alpha_max=5, policy=1)
+    assert (got["n0"], got["alpha"], got["beta"]) == tuple(g)
+    ref = O.power_chain(m, 50, 5, 1)
+    assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                      ref["k_stop"])
+
+
+def test_power_sequence_m9_table2_and_sampled_rows(golden):
+    # full m = 9 chain on the GPU: Table 2's (22, 5, 20) and the V13/formula gammas;
+    # rows of A^k sampled and recomputed by the oracle (row_k = row_{k-1} (x) A)
+    got = rd.rd_power_sequence(9, 50, alpha_max=5)
+    assert (got["n0"], got["alpha"], got["beta"]) == tuple(golden("table2_periods.json")["table2"]["9"])
+    assert got["k_stop"] == 27
+    for n in range(3, 28):
+        assert got["diag"][n] == (4 * n if n % 5 == 0 else 4 * n + 2), n
+
+
+def test_chain_m9_sampled_rows_bit_exact():
+    m, K = 9, 6
+    A = O.matrix(m)
+    rows = sample_rows(A.shape[0], 6, seed=9)
+    ch = rd.Chain(m, alpha_max=5)
+    R = A[rows].copy()
+    for k in range(2, K + 1):
+        ch.step()
+        R = O.minplus(R, A, skip=True)
+    got = ch.read_rows(K)[rows]
+    assert (got == to_inf(R, OINF, RINF, np.int16)).all()
+    ch.close()
+
+
+def test_row_panels_equal_full_chain():
+    # multi-GPU partition emulated sequentially on one device: panels of rows give the same
+    # rows and their MIN-combined stats equal the full chain's stats
+    m, K = 6, 8
+    full = rd.Chain(m, alpha_max=4)
+    N = full.N
+    cuts = [0, 100, 129, 500, N]
+    panels = [rd.Chain(m, alpha_max=4, row_begin=a, row_end=b) for a, b in zip(cuts[:-1], cuts[1:])]
+    for k in range(2, K + 1):
+        sf = full.step().cpu().numpy()
+        sp = np.min(np.stack([p.step().cpu().numpy() for p in panels]), axis=0)
+        assert (sf == sp).all(), k
+        fr = full.read_rows(k)
+        for p, a, b in zip(panels, cuts[:-1], cuts[1:]):
+            assert (p.read_rows(k) == fr[a:b]).all()
+
+
+def test_roman_cylinder_formulas_with_errata():
+    def f7(n):
+        c = (16 * n + 4) // 5
+        return c if n % 5 == 0 else c + 1
+
+    def f8(n):
+        c = (18 * n + 4) // 5
+        return c if n % 5 == 0 else (c + 1 if (n % 5 in (2, 3, 4) or n == 6) else c + 2)
+
+    for n in range(3, 120):
+        assert rd.rd_roman_cylinder(7, n) == (20 if n == 6 else f7(n)), n
+        assert rd.rd_roman_cylinder(8, n) == (13 if n == 3 else f8(n)), n
+        assert rd.rd_roman_cylinder(1, n) == (2 * n + 2) // 3
+    for n in range(3, 60):
+        assert rd.rd_roman_cylinder(3, n) == O.gamma_from_chain(O.power_chain(3), n)
+
+
+def test_roman_cylinder_m9_formula():
+    for n in range(3, 200):
+        assert rd.rd_roman_cylinder(9, n) == (4 * n if n % 5 == 0 else 4 * n + 2), n
+
+
+def test_alu_probe_reports_rates():
+    r = rd.rd_alu_probe()
+    assert 100 < r["dpx_minplus_per_clk_sm"] < 140     # VIADDMNMX.S16x2 at half rate: 128
+    assert r["sm_mhz"] > 500

@@ -1,0 +1,98 @@
+"""librd.so on the CPU: the library loads and exports every symbol include/rd.h
+declares; the host half (rd_build_states, rd_build_matrix, rd_stats_decide, argument
+validation) is bit-exact against the oracle.  No GPU compute is called here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2409_17658_b200 as rd
+from rd_inputs import to_inf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "rd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rd_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = rd.lib()
+    names = _header_functions()
+    assert "rd_minplus_mul" in names and "rd_power_sequence" in names and "rd_roman_cylinder" in names
+    for n in names:
+        assert hasattr(L, n), n
+    # and the .so really is an sm_100a build (fat binary inside)
+    out = os.popen(f"cuobjdump --list-elf {rd.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_build_states_matches_oracle():
+    for m in range(1, 12):
+        n, _ = (rd.count_words(m), None)
+        assert n == O.count_words(m), m
+    for m in range(1, 9):
+        n, words = rd.rd_build_states(m)
+        assert words == O.words(m), m
+
+
+@pytest.mark.parametrize("m", range(1, 9))
+def test_build_matrix_bit_exact(m):
+    A = rd.rd_build_matrix(m)
+    B = to_inf(O.matrix(m), int(O.INF), rd.RD_INF, np.int16)
+    assert A.shape == B.shape
+    assert (A == B).all()
+
+
+@pytest.mark.slow
+def test_build_matrix_bit_exact_m9():
+    A = rd.rd_build_matrix(9)
+    B = to_inf(O.matrix(9), int(O.INF), rd.RD_INF, np.int16)
+    assert (A == B).all()
+
+
+def test_stats_decide_logic():
+    am = 3
+    INT_MAX = 2**31 - 1
+
+    def stats(entries, diag=5):
+        s = [diag]
+        for lo, hi, mis, fin in entries:
+            s += [lo, -hi, -mis, -fin]
+        s += [INT_MAX, INT_MAX, 0, 0] * (am - len(entries))
+        return np.array(s, dtype=np.int32)
+
+    assert rd.rd_stats_decide(stats([(2, 2, 0, 1)]), am, 5) == (1, 2)
+    assert rd.rd_stats_decide(stats([(2, 3, 0, 1), (4, 4, 0, 1)]), am, 5) == (2, 4)
+    assert rd.rd_stats_decide(stats([(2, 2, 1, 1)]), am, 5) is None       # inf pattern differs
+    assert rd.rd_stats_decide(stats([(INT_MAX, -INT_MAX, 0, 0)]), am, 5) is None  # nothing finite
+    assert rd.rd_stats_decide(stats([(-1, -1, 0, 1)]), am, 5) is None     # beta must be natural
+    # alpha is limited to k-1
+    assert rd.rd_stats_decide(stats([(9, 9, 1, 1), (4, 4, 0, 1)]), am, 2) is None
+    assert rd.rd_stats_decide(stats([(2, 2, 0, 1), (4, 4, 0, 1)]), am, 5, only_alpha=2) == (2, 4)
+
+
+def test_argument_validation_host_paths():
+    L = rd.lib()
+    n = ctypes.c_int64()
+    assert L.rd_build_states(0, None, ctypes.byref(n)) == rd.RD_EINVAL
+    assert L.rd_build_states(3, None, None) == rd.RD_EINVAL
+    assert L.rd_build_matrix(13, None, ctypes.byref(n)) == rd.RD_EINVAL
+    assert b"out of range" in L.rd_last_error()
+    per = rd._Period()
+    # headroom: 2*m*kmax >= RD_INF is refused before any device work
+    assert L.rd_power_sequence_ex(9, 1000, 10, 0, ctypes.byref(per), None) == rd.RD_ERANGE
+    assert L.rd_power_sequence_ex(0, 50, 10, 0, ctypes.byref(per), None) == rd.RD_EINVAL
+    assert L.rd_power_sequence_ex(3, 1, 10, 0, ctypes.byref(per), None) == rd.RD_EINVAL
+    assert L.rd_power_sequence_ex(3, 50, 33, 0, ctypes.byref(per), None) == rd.RD_EINVAL
+    assert L.rd_power_sequence_ex(3, 50, 10, 2, ctypes.byref(per), None) == rd.RD_EINVAL
+    g = ctypes.c_int64()
+    assert L.rd_roman_cylinder(3, 2, ctypes.byref(g)) == rd.RD_EINVAL
+    assert L.rd_roman_cylinder(0, 5, ctypes.byref(g)) == rd.RD_EINVAL
+    assert L.rd_minplus_mul(None, None, None, 4) == rd.RD_EINVAL
+    assert L.rd_stats_len(10) == 41
