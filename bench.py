@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark: the (min,+) power step of arXiv 2409.17658 on B200.
+
+A "step" is one pass of the whole hot path over the m = 9 transfer matrix
+(N = C_9 = 21909): A^k = A^{k-1} (x) A on the DPX GEMM with the fused diagonal min and
+periodicity stats (a2-a4), the stats all_reduce(MIN) across ranks, the device->host read
+of the stats and the host decision (a5).  The right operand A is packed once before the
+timed region (a1).  One process per GPU; ranks own 128-row panels of the output.
+
+    python bench.py [--gpus N --steps K --warmup W] [--m 9] [--impl reference]
+
+Prints ONE JSON line on rank 0 (contract in DESIGN.md §Measurement).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_K80_GOPS = {6: 99.6, 7: 156.9, 8: 143.1, 9: 166.2}   # BASELINE.md §1.1 (derived from Table 3)
+SM_COUNT = 148
+DPX_MINPLUS_PER_CLK_SM = 128      # VIADDMNMX.S16x2 at half rate: 64 lanes x 2 (measured)
+SM_MAX_MHZ = 1965.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--m", type=int, default=9)
+    p.add_argument("--alpha-max", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------- clocks --
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled every 100 ms while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------- CPU oracle --
+class OracleSample:
+    """The oracle's dense (min,+) loop (or_minplus_bt: i-j-k, guarded INF, OpenMP over the
+    output) on sampled rows of the same step A^{k-1} (x) A(G): rows of a fully finite
+    A^k-like operand (rd_inputs.power_like, seeded) times the real A(G) of m."""
+
+    def __init__(self, m: int):
+        import numpy as np
+
+        import oracle as O
+        O.build()
+        self.O, self.m = O, m
+        A = O.matrix(m)
+        self.N = A.shape[0]
+        self.BT = np.ascontiguousarray(A.T)
+
+    def calibrate(self, seconds: float) -> int:
+        from rd_inputs import power_like
+        X = power_like(1, self.N, self.m, seed=0).astype("int32")
+        t = time.perf_counter()
+        self.O.minplus_bt(X, self.BT)
+        return max(1, min(4096, int(seconds / max(time.perf_counter() - t, 1e-4))))
+
+    def run(self, rows: int, seed: int = 1):
+        """Returns (Gop/s, seconds) for `rows` output rows."""
+        from rd_inputs import power_like
+        X = power_like(rows, self.N, self.m, seed=seed).astype("int32")
+        t = time.perf_counter()
+        self.O.minplus_bt(X, self.BT)
+        dt = time.perf_counter() - t
+        return rows * self.N * self.N / dt / 1e9, dt
+
+
+def cores_used():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+# ------------------------------------------------------------------- arms --
+def run_reference(args, rank, world):
+    """The oracle as it stands, on the host cores, on a bounded sample of the same
+    workload (each step: a fixed number of sampled output rows); rank 0 only."""
+    if rank != 0:
+        return
+    smp = OracleSample(args.m)
+    N = smp.N
+    rows = smp.calibrate(args.cpu_seconds / max(1, args.steps + args.warmup) * 3)
+    times = []
+    for i in range(args.warmup + args.steps):
+        _, dt = smp.run(rows, seed=1 + i)
+        if i >= args.warmup:
+            times.append(dt)
+    value = rows * N * N * len(times) / sum(times) / 1e9
+    sample = f"{rows} sampled output rows of A^(k-1) (x) A(G) per step, m={args.m}, N={N}, dense i-j-k oracle"
+    line = {
+        "impl": "reference", "metric": "(min,+) Gop/s on A^(k-1) (x) A(G) at order N = C_m (power step with fused diag-min + periodicity test)",
+        "value": round(value, 3), "unit": "Gop/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "i32",
+        "data": "synthetic A^k-like rows (seeded) x deterministic A(G)",
+        "config": {"workload": f"P_{args.m} box C_n: power step A^k = A^(k-1) (x) A(G), N = C_{args.m} = {N}",
+                   "m": args.m, "N": N},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Gop/s", "cores": cores_used(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_17658_b200 as rd
+    from paper_2409_17658_b200 import dist as rdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    m, am = args.m, args.alpha_max
+    N = rd.count_words(m)
+    r0, r1 = rdist.panel_bounds(N, world, rank)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        chain = rd.Chain(m, alpha_max=am, row_begin=r0, row_end=r1, stream=stream) if r1 > r0 else None
+        stats = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device=dev)
+        neutral = torch.from_numpy(rdist.neutral_stats(am)).to(dev)
+        hstats = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    launches_per_step = 2 if chain is not None else 0   # stats init + GEMM (librd kernels)
+
+    k_state = {"k": 1, "found": None}
+
+    def step(ev=None):
+        with torch.cuda.stream(stream):
+            if ev is not None:
+                ev[0].record(stream)
+            if chain is not None:
+                chain.step(stats)
+            else:
+                stats.copy_(neutral)
+            if ev is not None:
+                ev[1].record(stream)
+            if world > 1:
+                dist.all_reduce(stats, op=dist.ReduceOp.MIN)
+            hstats.copy_(stats, non_blocking=True)
+        stream.synchronize()
+        k_state["k"] += 1
+        h = hstats.numpy()
+        if k_state["found"] is None:
+            dec = rd.rd_stats_decide(h, am, k_state["k"])
+            if dec:
+                k_state["found"] = (k_state["k"] - dec[0], dec[0], dec[1])
+
+    for _ in range(args.warmup):
+        step()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    elapsed = t_start.elapsed_time(t_end) * 1e-3
+    gemm_s = statistics.mean(a.elapsed_time(b) for a, b in evs) * 1e-3 if chain is not None else 0.0
+    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tmax = float(t.item())
+    ops_total = float(N) ** 3 * args.steps
+    value = ops_total / tmax / 1e9
+    clocks = clk.summary()
+
+    # roofline of the dominant kernel (the GEMM): algorithmic ops per launch / launch time
+    ops_launch = float(r1 - r0) * N * N
+    achieved = ops_launch / gemm_s / 1e9 if gemm_s > 0 else 0.0
+    peak = SM_COUNT * DPX_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
+    if chain is not None:
+        chain.close()
+
+    # e2e through the public API with host buffers (rd_power_sequence: host build, H2D, chain
+    # to first detection, per-step stats D2H), wall clock, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            res = rdist.power_sequence(m, 50, am)
+        else:
+            res = rd.rd_power_sequence(m, 50, am)
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        prods = res["k_stop"] - 1
+        e2e = {"value": round(prods * float(N) ** 3 / te / 1e9, 3), "unit": "Gop/s",
+               "h2d_bytes_per_step": int(2 * N * N), "d2h_bytes_per_step": int(prods * rd.rd_stats_len(am) * 4),
+               "step": "one rd_power_sequence(m, 50) call: build + upload A, chain to first detection",
+               "seconds": round(te, 3), "k_stop": res["k_stop"],
+               "triple": [res["n0"], res["alpha"], res["beta"]]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        smp = OracleSample(m)
+        rows = smp.calibrate(args.cpu_seconds)
+        rate, dt = smp.run(rows)
+        cpu = {"value": round(rate, 3), "unit": "Gop/s", "cores": cores_used(), "kind": "oracle",
+               "sample": f"{rows} sampled output rows of A^(k-1) (x) A(G), m={m}, dense i-j-k oracle, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "(min,+) Gop/s on A^(k-1) (x) A(G) at order N = C_m (power step with fused diag-min + periodicity test)",
+            "value": round(value, 3), "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(tmax / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": round(value / PAPER_K80_GOPS[m], 2) if m in PAPER_K80_GOPS else None,
+            "dtype": "i16",
+            "data": "deterministic A(G) of P_m (no dataset); powers computed in the timed steps",
+            "config": {"workload": f"P_{m} box C_n: power step A^k = A^(k-1) (x) A(G), N = C_{m} = {N}",
+                       "m": m, "N": N, "alpha_max": am, "parallelism": f"row panels x{world}",
+                       "l2": "operands (2N^2 B = %.0f MB each) exceed L2; no flush" % (2 * N * N / 1e6),
+                       "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
+            "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "minplus_gemm_kernel<PM,STATS>",
+                         "peak_basis": "148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2, measured) x 1965 MHz"},
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps * world,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "paper_context": {"k80_cumatrixtrop_gops_derived": PAPER_K80_GOPS.get(m),
+                              "source": "BASELINE.md 1.1, 49 N^3 / Table 3 kernel time"},
+        }
+        if k_state["found"]:
+            line["config"]["detected"] = list(k_state["found"])
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

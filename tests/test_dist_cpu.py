@@ -1,0 +1,131 @@
+"""Multi-rank row-panel driver on CPU: world_size 2 (and 3) over gloo.
+
+The partition, the MIN-reduction of the stats vector and the shared decision loop of
+paper_2409_17658_b200.dist.power_sequence run unchanged; only the per-panel product is
+replaced by an oracle-backed panel (test code) since there is no GPU here.  The result
+must equal the oracle's single-process chain (and Table 2).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2409_17658_b200 import dist as rdist
+
+OINF = int(O.INF)
+RINF = 0x3FFF
+
+
+class OraclePanel:
+    """Rows [r0, r1) of A^k by the oracle, with the stats vector in the library's
+    MIN-reducible layout (rd.h rd_chain_step)."""
+
+    def __init__(self, m, alpha_max, r0, r1):
+        self.A = O.matrix(m)
+        self.r0, self.r1, self.am = r0, r1, alpha_max
+        self.k = 1
+        self.ring = {1: self.A[r0:r1].copy()}
+
+    def step(self):
+        k = self.k + 1
+        X = O.minplus(self.ring[self.k], self.A, skip=True)
+        self.ring[k] = X
+        s = rdist.neutral_stats(self.am)
+        n = X.shape[0]
+        d = [X[i, self.r0 + i] for i in range(n)]
+        s[0] = min(min(d), RINF) if d else 2**31 - 1
+        for a in range(1, min(self.am, k - 1) + 1):
+            P = self.ring[k - a]
+            fx, fp = X != OINF, P != OINF
+            both = fx & fp
+            diff = X[both].astype(np.int64) - P[both].astype(np.int64)
+            e = 1 + 4 * (a - 1)
+            if diff.size:
+                s[e], s[e + 1] = int(diff.min()), -int(diff.max())
+            s[e + 2] = -1 if (fx != fp).any() else 0
+            s[e + 3] = -1 if both.any() else 0
+        self.ring.pop(k - self.am - 1, None)
+        self.k = k
+        return torch.from_numpy(s)
+
+    def close(self):
+        pass
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, m, policy, alpha_max, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = O.matrix(m)
+        d = np.diag(A)
+        res = rdist.power_sequence(m, 50, alpha_max, policy,
+                                   chain_factory=lambda m_, am_, a, b: OraclePanel(m_, am_, a, b),
+                                   diag1=int(d[d != OINF].min()))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, m, policy=0, alpha_max=10):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, m, policy, alpha_max, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_panel_bounds_cover_and_balance():
+    for N in (1, 33, 127, 128, 129, 2507, 21909):
+        for W in (1, 2, 3, 4, 8):
+            b = [rdist.panel_bounds(N, W, r) for r in range(W)]
+            assert b[0][0] == 0 and b[-1][1] == N
+            for (a0, a1), (c0, c1) in zip(b, b[1:]):
+                assert a1 == c0
+            tiles = [(e - s + 127) // 128 for s, e in b]
+            assert max(tiles) - min(tiles) <= 1
+            assert all(s % 128 == 0 for s, e in b if e > s)
+
+
+def test_neutral_stats_is_min_identity():
+    s = rdist.neutral_stats(3)
+    x = np.array([7, 2, -2, -1, -1] + [5, -5, 0, -1] * 2, dtype=np.int32)
+    assert (np.minimum(s, x) == x).all()
+
+
+@pytest.mark.parametrize("m", [3, 5])
+def test_gloo_world2_equals_single_process(m):
+    out = _run(2, m)
+    ref = O.power_chain(m, 50, 10, 0)
+    for r in (0, 1):
+        res = out[r]
+        assert (res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                         ref["k_stop"])
+        assert res["diag"][1:res["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+def test_gloo_world3_paper_compat_table2(golden):
+    # m = 4: 97 rows -> one 128-row tile -> ranks 1 and 2 hold empty panels
+    out = _run(3, 4, policy=1, alpha_max=5)
+    want = tuple(golden("table2_periods.json")["table2"]["4"])
+    for r in range(3):
+        assert (out[r]["n0"], out[r]["alpha"], out[r]["beta"]) == want

@@ -1,0 +1,23 @@
+#!/bin/bash
+# One GPU session: bench (both arms), ncu launch list, ncu --set full of the GEMM.
+# usage: tools/gpu_round.sh <tag>   (outputs under gpurun_out/<tag>_*)
+set -u
+TAG=${1:-r01}
+O=gpurun_out
+mkdir -p $O
+python -m paper_2409_17658_b200.build > $O/${TAG}_build.log 2>&1
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > $O/${TAG}_clocks.csv &
+SMI=$!
+python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
+echo "bench rc=$?"
+kill $SMI
+python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err
+echo "ref rc=$?"
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+$CMD > $O/${TAG}_plain.log 2>&1 &&
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv $CMD > $O/${TAG}_ncu_launches.log 2>&1
+echo "launches rc=$?"
+$CMD > $O/${TAG}_plain2.log 2>&1 &&
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:minplus_gemm -s 1 -c 1 -o $O/${TAG}_gemm $CMD > $O/${TAG}_ncu_full.log 2>&1
+echo "full rc=$?"
+tail -3 $O/${TAG}_bench.json $O/${TAG}_bench_ref.json
