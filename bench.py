@@ -28,6 +28,9 @@ PAPER_K80_GOPS = {6: 99.6, 7: 156.9, 8: 143.1, 9: 166.2}   # BASELINE.md §1.1 (
 SM_COUNT = 148
 DPX_MINPLUS_PER_CLK_SM = 128      # VIADDMNMX.S16x2 at half rate: 64 lanes x 2 (measured)
 SM_MAX_MHZ = 1965.0
+# dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
+# (profiles/), by m; None where not captured for the current kernel
+TRAFFIC = {}
 
 
 def parse():
@@ -41,6 +44,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8, 9])
     return p.parse_args()
 
 
@@ -184,6 +188,7 @@ def run_ours(args, rank, world, local_rank):
         neutral = torch.from_numpy(rdist.neutral_stats(am)).to(dev)
         hstats = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, pin_memory=True)
     torch.cuda.synchronize()
+    probe = rd.rd_alu_probe()          # live issue rates of the GEMM's instruction forms
     launches_per_step = 2 if chain is not None else 0   # stats init + GEMM (librd kernels)
 
     k_state = {"k": 1, "found": None}
@@ -238,6 +243,7 @@ def run_ours(args, rank, world, local_rank):
     ops_launch = float(r1 - r0) * N * N
     achieved = ops_launch / gemm_s / 1e9 if gemm_s > 0 else 0.0
     peak = SM_COUNT * DPX_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
+    mix_peak = SM_COUNT * probe["mixed_minplus_per_clk_sm"] * SM_MAX_MHZ * 1e6 / 1e9
     if chain is not None:
         chain.close()
 
@@ -265,6 +271,23 @@ def run_ours(args, rank, world, local_rank):
                "seconds": round(te, 3), "k_stop": res["k_stop"],
                "triple": [res["n0"], res["alpha"], res["beta"]]}
 
+    # time to periodicity per m (Alg 2 to first detection): build (words, A(G), upload,
+    # packing) and chain (products + fused checks + per-step stats decision), max over ranks
+    ttp = {}
+    if not args.no_e2e:
+        for mm in args.ttp_m:
+            if world > 1:
+                dist.barrier()
+            res = rdist.power_sequence(mm, 50, am)
+            tt = torch.tensor([res["t_build"], res["t_chain"]], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            nn = rd.count_words(mm)
+            ttp[str(mm)] = {"build_s": round(float(tt[0]), 4), "chain_s": round(float(tt[1]), 4),
+                            "total_s": round(float(tt[0] + tt[1]), 4), "k_stop": res["k_stop"],
+                            "triple": [res["n0"], res["alpha"], res["beta"]],
+                            "chain_gops": round((res["k_stop"] - 1) * float(nn) ** 3 / float(tt[1]) / 1e9, 1)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSample(m)
@@ -287,13 +310,17 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "operands (2N^2 B = %.0f MB each) exceed L2; no flush" % (2 * N * N / 1e6),
                        "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "minplus_gemm_kernel<PM,STATS>",
-                         "peak_basis": "148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2, measured) x 1965 MHz"},
+                         "frac": round(achieved / peak, 4), "traffic": TRAFFIC.get(m),
+                         "kernel": "minplus_gemm_kernel<PM,STATS,3>",
+                         "peak_basis": "DPX issue peak: 148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2 at 2 warp-instr/clk/SM, measured) x 1965 MHz",
+                         "mix_ceiling": round(mix_peak, 1), "frac_of_mix_ceiling": round(achieved / mix_peak, 4),
+                         "mix_ceiling_basis": "register-tile probe of the GEMM's DPX+IMAD/VIMNMX3 mix (rd_alu_probe, live) x 148 SMs x 1965 MHz",
+                         "probe": {k: round(v, 2) for k, v in probe.items()}},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps * world,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "time_to_periodicity": ttp,
             "paper_context": {"k80_cumatrixtrop_gops_derived": PAPER_K80_GOPS.get(m),
                               "source": "BASELINE.md 1.1, 49 N^3 / Table 3 kernel time"},
         }

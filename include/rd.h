@@ -169,11 +169,21 @@ int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, 
                     int32_t *beta);
 
 /* ---------------------------------------------------------------------------
- * rd_alu_probe — measures the issue rate of the integer instructions the GEMM uses
- * (register-only kernels, many independent chains) on the current device:
- * out[0] VIADDMNMX.S16x2 warp-instructions / clock / SM, out[1] (min,+) lane-ops /
- * clock / SM for the DPX form, out[2] the same for the mixed IADD(fma)+VIMNMX3(alu)
- * form, out[3] SM clock in MHz seen during the probe.  Synchronous. */
+ * rd_set_gemm_variant — tuning knob of the GEMM mainloop (process-wide, not thread-safe;
+ * set it before launching work).  dpx_cols in {0, 2, 3, 4, 8}: of each thread's 8
+ * accumulator columns, that many use one VIADDMNMX.S16x2 (alu pipe) per k-pair; the rest
+ * use two IMAD packed adds (fma pipe) + one VIMNMX3.S16x2 (alu) per two k-pairs
+ * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
+int rd_set_gemm_variant(int dpx_cols);
+
+/* ---------------------------------------------------------------------------
+ * rd_alu_probe — measures, on the current device, the issue rate of the integer
+ * instructions the GEMM uses (register-only kernels):
+ * out[0] VIADDMNMX.S16x2 warp-instructions / clock / SM (independent chains);
+ * out[1] (min,+) lane-terms / clock / SM of that DPX-only form (the DPX issue peak);
+ * out[2] (min,+) lane-terms / clock / SM of the GEMM's 8x8 accumulator tile with its
+ *        default DPX + IMAD/VIMNMX3 mix, operands in registers (the mix's ceiling);
+ * out[3] SM clock in MHz seen during the probe.  Synchronous. */
 int rd_alu_probe(double out[4]);
 
 #ifdef __cplusplus

@@ -61,10 +61,11 @@ def lib():
         L.rd_chain_read_rows.argtypes = [p, ci, p]
         L.rd_stats_decide.argtypes = [p, ci, ci, ci, p, p]
         L.rd_alu_probe.argtypes = [p]
+        L.rd_set_gemm_variant.argtypes = [ci]
         for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
-                  "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe"):
+                  "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -172,6 +173,11 @@ def rd_roman_cylinder(m: int, n: int) -> int:
     g = ctypes.c_int64()
     _check(lib().rd_roman_cylinder(m, n, ctypes.byref(g)))
     return g.value
+
+
+def rd_set_gemm_variant(dpx_cols: int):
+    """Mainloop instruction mix (rd.h): dpx_cols in {0, 2, 3, 4, 8}."""
+    _check(lib().rd_set_gemm_variant(dpx_cols))
 
 
 def rd_alu_probe():

@@ -42,6 +42,7 @@ constexpr uint32_t kInf2 = 0x3FFF3FFFu;
 constexpr int kThreads = 256;
 constexpr int kBK2 = 16;      // k-pairs per pipeline stage (32 k)
 constexpr int kStages = 4;
+constexpr int kGroup = 8;     // row-tiles per rasterisation group
 constexpr int kStageWords = 2 * kBK2 * kTile;   // u32 per stage (left + right tile)
 constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4;   // 64 KB
 
@@ -139,15 +140,33 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // VIADDMNMX.S16x2 (128 (min,+) terms).
 //   OUT_PM = true : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
 //   OUT_PM = false: C is row-major int16 with ldc, predicated to (M, N).
-template <bool OUT_PM, bool STATS>
+//
+// Two instruction forms share the mainloop: for accumulator columns
+// c < DPXC each k-pair costs one VIADDMNMX.S16x2 (alu pipe); for c >= DPXC two k-pairs
+// (t, t+1) cost two packed adds s = x + b on IMAD (fma pipe; exact: lane sums <= 0x7FFE
+// never carry) and one VIMNMX3.S16x2 (alu) folding both into the accumulator.  The mix
+// balances the alu pipe, the fma pipe and the issue slot.  `one` is a kernel argument
+// equal to 1, opaque to the compiler so that the add stays an IMAD.
+// Tiles are rasterised in groups of kGroup row-tiles so CTAs resident together share
+// right-operand panels in L2.
+template <bool OUT_PM, bool STATS, int DPXC>
 __global__ void __launch_bounds__(kThreads, 2)
 minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
                     int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
-                    EpiArgs epi) {
+                    int nti, int ntj, uint32_t one, EpiArgs epi) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const int64_t j0 = (int64_t)blockIdx.x * kTile, i0 = (int64_t)blockIdx.y * kTile;
+  int64_t i0, j0;
+  {
+    const int bid = blockIdx.x;
+    const int per_group = kGroup * ntj;
+    const int g = bid / per_group, first = g * kGroup;
+    const int gsz = min(nti - first, kGroup);
+    const int w = bid - g * per_group;
+    i0 = (int64_t)(first + w % gsz) * kTile;
+    j0 = (int64_t)(w / gsz) * kTile;
+  }
 
   // cp.async mapping: 512 16-byte chunks per operand tile (16 rows x 32 chunks)
   const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
@@ -188,18 +207,54 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     }
     const uint32_t *sx = smem + (kb % kStages) * kStageWords;
     const uint32_t *sb = sx + kBK2 * kTile;
+    if (DPXC >= 8) {
 #pragma unroll
-    for (int t = 0; t < kBK2; ++t) {
-      const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
-      const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
-      const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
-      const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
-      const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-      const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+      for (int t = 0; t < kBK2; ++t) {
+        const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
+        const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
+        const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
+        const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
+        const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+        const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
+          for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < kBK2; t += 2) {
+        uint32_t x0[8], x1[8], b0[8], b1[8];
+        {
+          const uint4 p = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
+          const uint4 q = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
+          const uint4 u = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + ty * 4);
+          const uint4 v = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
+          x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
+          x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
+        }
+        {
+          const uint4 p = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
+          const uint4 q = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
+          const uint4 u = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + tx * 4);
+          const uint4 v = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
+          b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
+          b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (c < DPXC) {
+              acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+              acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+            } else {
+              const uint32_t s0 = x0[r] * one + b0[c];
+              const uint32_t s1 = x1[r] * one + b1[c];
+              acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
+            }
+          }
+      }
     }
   }
   cp_async_wait<0>();
@@ -315,23 +370,38 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   }
 }
 
-template <bool OUT_PM, bool STATS>
-int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
-                int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                cudaStream_t st) {
+int g_dpx_cols = 3;   // rd_set_gemm_variant (default: measured best)
+
+template <bool OUT_PM, bool STATS, int DPXC>
+int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
+                  int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
+                  cudaStream_t st) {
   static bool attr_set[64] = {};
   int dev = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT_PM, STATS>,
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT_PM, STATS, DPXC>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  dim3 grid((unsigned)(Np / kTile), (unsigned)(Mp / kTile));
-  minplus_gemm_kernel<OUT_PM, STATS><<<grid, kThreads, kSmemBytes, st>>>(XT, ldx, BP, ldb, (int)kpairs, C, ldc,
-                                                                          M, N, epi);
+  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
+  minplus_gemm_kernel<OUT_PM, STATS, DPXC><<<(unsigned)(nti * ntj), kThreads, kSmemBytes, st>>>(
+      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
+}
+
+template <bool OUT_PM, bool STATS>
+int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
+                int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
+                cudaStream_t st) {
+  switch (g_dpx_cols) {
+    case 0: return launch_gemm_v<OUT_PM, STATS, 0>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+    case 2: return launch_gemm_v<OUT_PM, STATS, 2>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+    case 3: return launch_gemm_v<OUT_PM, STATS, 3>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+    case 4: return launch_gemm_v<OUT_PM, STATS, 4>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+    default: return launch_gemm_v<OUT_PM, STATS, 8>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+  }
 }
 
 int pack_left(const int16_t *X, int64_t ld, int64_t rows, int64_t cols, int64_t row0, uint32_t *XT,
@@ -351,6 +421,14 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 }
 
 }  // namespace
+
+extern "C" int rd_set_gemm_variant(int dpx_cols) {
+  clear_error();
+  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
+    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
+  g_dpx_cols = dpx_cols;
+  return RD_OK;
+}
 
 extern "C" int rd_set_device(int device) {
   clear_error();
@@ -586,44 +664,73 @@ extern "C" int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *dia
 // ================================================================ ALU probe ==
 namespace {
 #define RD_OPQ(x) asm volatile("" : "+r"(x))
+// MODE 0: independent VIADDMNMX.S16x2 chains (the DPX issue rate).
+// MODE 1: the GEMM's 8x8 accumulator tile with its default instruction mix (3 of 8
+//         columns DPX, 5 via IMAD(uniform one) + VIMNMX3), operands from registers made
+//         opaque each iteration: the ceiling of the mix without shared-memory traffic.
 template <int MODE>
-__global__ void __launch_bounds__(256) alu_probe_kernel(uint32_t *sink, long long *cyc, int iters, uint32_t seed) {
-  uint32_t c[32], xa0[4], xa1[4], yb0[8], yb1[8];
-  uint32_t x0 = (seed ^ threadIdx.x) & 0x000F000Fu;
+__global__ void __launch_bounds__(256, 2) alu_probe_kernel(uint32_t *sink, long long *cyc, int iters, uint32_t one) {
+  long long t0 = 0, t1 = 0;
+  uint32_t h = 0;
+  if (MODE == 0) {
+    uint32_t c[32], xa0[4], yb0[8];
+    uint32_t x0 = (one ^ threadIdx.x) & 0x000F000Fu;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) { xa0[q] = x0 + q; xa1[q] = x0 + 2 * q + 1; }
+    for (int q = 0; q < 4; ++q) xa0[q] = x0 + q;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) { yb0[q] = x0 + 3 * q; yb1[q] = x0 + 5 * q + 2; }
+    for (int q = 0; q < 8; ++q) yb0[q] = x0 + 3 * q;
 #pragma unroll
-  for (int u = 0; u < 32; ++u) c[u] = 0x10001000u + u;
-  long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) {
+    for (int u = 0; u < 32; ++u) c[u] = 0x10001000u + u;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) { RD_OPQ(xa0[q]); RD_OPQ(xa1[q]); }
+      for (int q = 0; q < 4; ++q) RD_OPQ(xa0[q]);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) { RD_OPQ(yb0[q]); RD_OPQ(yb1[q]); }
+      for (int q = 0; q < 8; ++q) RD_OPQ(yb0[q]);
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int i = u >> 3, j = u & 7;
-      if (MODE == 0) {
-        c[u] = __viaddmin_s16x2(xa0[i], yb0[j], c[u]);
-      } else {
-        uint32_t s1 = xa0[i] + yb0[j], s2 = xa1[i] + yb1[j];
-        c[u] = __vimin3_s16x2(c[u], s1, s2);
-      }
+      for (int u = 0; u < 32; ++u) c[u] = __viaddmin_s16x2(xa0[u >> 3], yb0[u & 7], c[u]);
     }
-  }
-  long long t1 = clock64();
-  uint32_t acc = 0;
+    t1 = clock64();
 #pragma unroll
-  for (int u = 0; u < 32; ++u) acc ^= c[u];
-  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    for (int u = 0; u < 32; ++u) h ^= c[u];
+  } else {
+    uint32_t acc[8][8], x0[8], x1[8], b0[8], b1[8];
+    uint32_t s = threadIdx.x * 0x00010001u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { x0[i] = s + i; x1[i] = s + 2 * i; b0[i] = s + 3 * i; b1[i] = s + 5 * i; }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { RD_OPQ(x0[i]); RD_OPQ(x1[i]); RD_OPQ(b0[i]); RD_OPQ(b1[i]); }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < 3) {
+            acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+            acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+          } else {
+            acc[r][c] = __vimin3_s16x2(acc[r][c], x0[r] * one + b0[c], x1[r] * one + b1[c]);
+          }
+        }
+    }
+    t1 = clock64();
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) h ^= acc[r][c];
+  }
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = h;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
 template <int MODE>
 int probe_one(int sms, double *minplus_per_clk_sm, double *mhz, double *instr_per_clk_sm) {
-  const int blocks = sms * 4, threads = 256, iters = 4096;
+  const int blocks = sms * 2, threads = 256, iters = MODE == 0 ? 8192 : 2000;
   uint32_t *sink = nullptr;
   long long *cyc = nullptr;
   RD_CUDA_CHECK(cudaMalloc(&sink, (size_t)blocks * threads * 4));
@@ -641,9 +748,10 @@ int probe_one(int sms, double *minplus_per_clk_sm, double *mhz, double *instr_pe
   std::vector<long long> h(blocks);
   RD_CUDA_CHECK(cudaMemcpy(h.data(), cyc, (size_t)blocks * 8, cudaMemcpyDeviceToHost));
   long long mx = *std::max_element(h.begin(), h.end());
-  const double per_u = MODE == 0 ? 2.0 : 4.0;  // (min,+) lane-terms per u per iteration
-  *minplus_per_clk_sm = (double)iters * 32 * per_u * threads * 4 / (double)mx;
-  *instr_per_clk_sm = (double)iters * 32 * (threads / 32) * 4 / (double)mx;
+  // (min,+) lane-terms per thread per iteration: MODE 0 32 DPX x 2; MODE 1 64 acc x 2 k-pairs x 2
+  const double terms = MODE == 0 ? 64.0 : 256.0;
+  *minplus_per_clk_sm = (double)iters * terms * threads * 2 / (double)mx;
+  *instr_per_clk_sm = MODE == 0 ? (double)iters * 32 * (threads / 32) * 2 / (double)mx : 0.0;
   *mhz = (double)mx / (ms * 1e3);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

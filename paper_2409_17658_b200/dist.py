@@ -67,11 +67,14 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
     panel's stats tensor (default: paper_2409_17658_b200.Chain on the current GPU);
     diag1 = min_p A_pp (default: from rd_build_matrix).
     """
+    import time
+
     import torch
     import torch.distributed as dist
 
     from . import count_words, rd_build_matrix, rd_stats_decide, RD_INF
 
+    t0 = time.perf_counter()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     N = count_words(m)
@@ -88,6 +91,9 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
         d = np.diag(A).astype(np.int64)
         diag1 = int(d[d < RD_INF].min()) if (d < RD_INF).any() else 2**31 - 1
 
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+    t1 = time.perf_counter()
     diag = [2**31 - 1] * (kmax + 1)
     diag[1] = diag1
     found_k, n0, al, be, k = -1, 0, 0, 0, 1
@@ -111,5 +117,7 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
                     al, be = dec
             if aa >= alpha_max:
                 break
+    t2 = time.perf_counter()
     chain.close()
-    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag)
+    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
+                t_build=t1 - t0, t_chain=t2 - t1)

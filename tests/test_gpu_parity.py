@@ -223,7 +223,34 @@ def test_roman_cylinder_m9_formula():
         assert rd.rd_roman_cylinder(9, n) == (4 * n if n % 5 == 0 else 4 * n + 2), n
 
 
+@pytest.mark.parametrize("variant", [0, 2, 3, 4, 8])
+def test_every_gemm_variant_bit_exact(variant):
+    try:
+        rd.rd_set_gemm_variant(variant)
+        for N, f in ((1, 0.0), (129, 0.3), (300, 0.01), (1000, 0.0)):
+            A = operand(N, N, 61 + N, inf_frac=f, hi=RINF - 1 if N == 129 else 1000)
+            B = operand(N, N, 62 + N, inf_frac=f)
+            C = rd.rd_minplus_mul(_gpu(A), _gpu(B)).cpu().numpy()
+            want = _oracle_mul(A, B)
+            want[want.astype(np.int64) >= RINF] = RINF
+            assert (C == want).all(), (variant, N)
+        ref = O.power_chain(6, 50, 10, 0)
+        got = rd.rd_power_sequence(6, 50)
+        assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                          ref["k_stop"])
+        assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+        P = _oracle_powers(7, 5)
+        ch = rd.Chain(7, alpha_max=3)
+        for _ in range(4):
+            ch.step()
+        assert (ch.read_rows(5) == P[5]).all()
+        ch.close()
+    finally:
+        rd.rd_set_gemm_variant(3)
+
+
 def test_alu_probe_reports_rates():
     r = rd.rd_alu_probe()
     assert 100 < r["dpx_minplus_per_clk_sm"] < 140     # VIADDMNMX.S16x2 at half rate: 128
+    assert 100 < r["mixed_minplus_per_clk_sm"] < 200   # the DPX/IMAD mix: ~142 measured
     assert r["sm_mhz"] > 500

@@ -7,8 +7,11 @@ import torch
 sys.path.insert(0, ".")
 import paper_2409_17658_b200 as rd  # noqa: E402
 
+import os
 ms = [int(x) for x in sys.argv[1:]] or [7, 8, 9]
-for m in ms:
+variants = [int(v) for v in os.environ.get("VARIANTS", "8").split(",")]
+for v, m in [(v, m) for v in variants for m in ms]:
+    rd.rd_set_gemm_variant(v)
     t0 = time.time()
     ch = rd.Chain(m, alpha_max=10, stream=torch.cuda.current_stream())
     torch.cuda.synchronize()
@@ -25,7 +28,7 @@ for m in ms:
     e1.record()
     torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) / reps * 1e-3
-    print(f"m={m} N={N} build={tb:.2f}s step={dt*1e3:.3f} ms  {N**3/dt/1e12:.2f} T minplus/s  "
+    print(f"variant={v} m={m} N={N} build={tb:.2f}s step={dt*1e3:.3f} ms  {N**3/dt/1e12:.2f} T minplus/s  "
           f"({N**3/dt/(148*128*1.965e9):.3f} of DPX peak @1965MHz)", flush=True)
     ch.close()
 print(rd.rd_alu_probe())
