@@ -140,6 +140,10 @@ int rd_chain_destroy(rd_chain *c);
 int64_t rd_chain_order(const rd_chain *c);
 int rd_chain_current_k(const rd_chain *c);
 
+/* min over the panel's rows p of A_pp (the self-loop labels; diag[1] of Cor 7),
+ * INT32_MAX if the panel has no finite diagonal entry.  MIN-reducible across panels. */
+int32_t rd_chain_diag1(const rd_chain *c);
+
 /* Length of the stats vector: 1 + 4*alpha_max int32. */
 int rd_stats_len(int alpha_max);
 

@@ -56,6 +56,7 @@ def lib():
         L.rd_chain_destroy.argtypes = [p]
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
+        L.rd_chain_diag1.argtypes = [p]; L.rd_chain_diag1.restype = i32
         L.rd_stats_len.argtypes = [ci]
         L.rd_chain_step.argtypes = [p, p]
         L.rd_chain_read_rows.argtypes = [p, ci, p]
@@ -208,6 +209,11 @@ class Chain:
         self._h = h
         self.N = lib().rd_chain_order(h)
         self.stats = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device="cuda")
+
+    @property
+    def diag1(self) -> int:
+        """min over this panel's rows of A_pp (INT32_MAX if none)."""
+        return lib().rd_chain_diag1(self._h)
 
     @property
     def k(self) -> int:

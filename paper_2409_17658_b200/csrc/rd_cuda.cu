@@ -553,6 +553,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
 
 extern "C" int64_t rd_chain_order(const rd_chain *c) { return c ? c->N : -1; }
 extern "C" int rd_chain_current_k(const rd_chain *c) { return c ? c->k : -1; }
+extern "C" int32_t rd_chain_diag1(const rd_chain *c) { return c ? c->diag1 : INT32_MAX; }
 
 extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   clear_error();

@@ -41,6 +41,8 @@ def neutral_stats(alpha_max: int) -> np.ndarray:
 class _EmptyPanel:
     """A rank without rows (more ranks than row tiles) still joins every collective."""
 
+    diag1 = 2**31 - 1
+
     def __init__(self, alpha_max: int, device):
         import torch
         self.alpha_max = alpha_max
@@ -72,7 +74,7 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
     import torch
     import torch.distributed as dist
 
-    from . import count_words, rd_build_matrix, rd_stats_decide, RD_INF
+    from . import count_words, rd_stats_decide, RD_INF
 
     t0 = time.perf_counter()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -87,9 +89,12 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
     device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
     chain = chain_factory(m, alpha_max, r0, r1) if r1 > r0 else _EmptyPanel(alpha_max, device)
     if diag1 is None:
-        A = rd_build_matrix(m)
-        d = np.diag(A).astype(np.int64)
-        diag1 = int(d[d < RD_INF].min()) if (d < RD_INF).any() else 2**31 - 1
+        d1 = getattr(chain, "diag1", 2**31 - 1)
+        if world > 1:
+            t = torch.tensor([d1], dtype=torch.int64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            d1 = int(t.item())
+        diag1 = d1
 
     if torch.cuda.is_available():
         torch.cuda.synchronize()

@@ -6,6 +6,11 @@ TAG=${1:-r01}
 O=gpurun_out
 mkdir -p $O
 python -m paper_2409_17658_b200.build > $O/${TAG}_build.log 2>&1
+if [ "${SKIP_TESTS:-0}" != "1" ]; then
+  timeout 1200 python -m pytest tests -m gpu -q -x > $O/${TAG}_pytest_gpu.log 2>&1
+  echo "pytest rc=$?"; tail -3 $O/${TAG}_pytest_gpu.log
+  timeout 300 python __graft_entry__.py > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
+fi
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > $O/${TAG}_clocks.csv &
 SMI=$!
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
@@ -20,4 +25,4 @@ echo "launches rc=$?"
 $CMD > $O/${TAG}_plain2.log 2>&1 &&
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:minplus_gemm -s 1 -c 1 -o $O/${TAG}_gemm $CMD > $O/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?"
-tail -3 $O/${TAG}_bench.json $O/${TAG}_bench_ref.json
+cat $O/${TAG}_bench.json; cat $O/${TAG}_bench_ref.json
