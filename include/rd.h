@@ -88,6 +88,25 @@ int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N);
 int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb,
                       int16_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream);
 
+/* Accumulating form: C = min(C, A (x) B) elementwise (the (min,+) product distributes
+ * over min, so a product split over k-chunks is the min of the chunk products:
+ * A (x) B = min_s A[:, K_s] (x) B[K_s, :]).  Same arguments and errors as
+ * rd_minplus_mul_ex; C must hold entries in [0, RD_INF] (e.g. all RD_INF to start).
+ * Used by the all-gather distributed product, which consumes B's k-panels as they
+ * arrive over NVLink. */
+int rd_minplus_mul_acc(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb,
+                       int16_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream);
+
+/* rd_panel_stats — the standalone (HBM-bound) form of the fused epilogue reductions:
+ * the stats vector (layout of rd_chain_step) of the row-major int16 panel `cur`
+ * (rows x cols, ld; global row index of local row 0 = diag_row0) against nprev earlier
+ * panels prev[a-1] = A^{k-a} (same shape and ld), a = 1..nprev.  alpha_max sizes the
+ * vector (1 + 4*alpha_max int32, DEVICE, overwritten).  prev is a HOST array of DEVICE
+ * pointers.  Asynchronous on cuda_stream.  Errors: RD_EINVAL, RD_ECUDA. */
+int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, int nprev, int64_t rows,
+                   int64_t cols, int64_t ld, int64_t diag_row0, int alpha_max, int32_t *stats_dev,
+                   void *cuda_stream);
+
 /* ---------------------------------------------------------------------------
  * Recurrence triple (Lemma 2; Prop 8; Alg 2 step 4 P:292):
  * A^{n0+alpha} = beta (x) A^{n0}.  k_stop = last power computed. */

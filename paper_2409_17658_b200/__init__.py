@@ -49,6 +49,8 @@ def lib():
         L.rd_build_matrix.argtypes = [ci, p, p]
         L.rd_minplus_mul.argtypes = [p, p, p, i64]
         L.rd_minplus_mul_ex.argtypes = [p, i64, p, i64, p, i64, i64, i64, i64, p]
+        L.rd_minplus_mul_acc.argtypes = [p, i64, p, i64, p, i64, i64, i64, i64, p]
+        L.rd_panel_stats.argtypes = [p, p, ci, i64, i64, i64, i64, ci, p, p]
         L.rd_power_sequence.argtypes = [ci, ci, p, p]
         L.rd_power_sequence_ex.argtypes = [ci, ci, ci, ci, p, p]
         L.rd_roman_cylinder.argtypes = [ci, i64, p]
@@ -66,7 +68,8 @@ def lib():
         for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
-                  "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant"):
+                  "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
+                  "rd_minplus_mul_acc", "rd_panel_stats"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -155,6 +158,25 @@ def rd_minplus_mul_ex(A, lda, B, ldb, C, ldc, M, N, K, stream=None):
     _check(lib().rd_minplus_mul_ex(A.data_ptr(), lda, B.data_ptr(), ldb, C.data_ptr(), ldc, M, N, K,
                                    _stream_ptr(stream)))
     return C
+
+
+def rd_minplus_mul_acc(A, lda, B, ldb, C, ldc, M, N, K, stream=None, a_offset=0, b_offset=0):
+    """C = min(C, A (x) B) on int16 CUDA tensors (offsets in elements into A / B)."""
+    _sync_device()
+    _check(lib().rd_minplus_mul_acc(A.data_ptr() + 2 * a_offset, lda, B.data_ptr() + 2 * b_offset, ldb,
+                                    C.data_ptr(), ldc, M, N, K, _stream_ptr(stream)))
+    return C
+
+
+def rd_panel_stats(cur, prevs, diag_row0: int, alpha_max: int, stats, stream=None):
+    """Stats vector (rd_chain_step layout) of row-major int16 panel `cur` against `prevs`
+    (list of same-shape CUDA tensors, A^{k-1}, A^{k-2}, ...), written into `stats`."""
+    _sync_device()
+    rows, cols = cur.shape
+    arr = (ctypes.c_void_p * max(1, len(prevs)))(*[t.data_ptr() for t in prevs])
+    _check(lib().rd_panel_stats(cur.data_ptr(), arr, len(prevs), rows, cols, cur.stride(0), diag_row0,
+                                alpha_max, stats.data_ptr(), _stream_ptr(stream)))
+    return stats
 
 
 def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0):

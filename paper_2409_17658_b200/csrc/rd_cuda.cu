@@ -118,6 +118,7 @@ struct EpiArgs {
   int nprev;
   int32_t *stats;          // MIN-reducible stats vector (nullable: no stats)
   int64_t diag_row0;       // global row index of local row 0 (row panels)
+  int accumulate;          // row-major output only: C = min(C, X (x) B)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -290,8 +291,13 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2;
-        if (j < N) C[i * ldc + j] = (int16_t)(out[r][p] & 0xFFFF);
-        if (j + 1 < N) C[i * ldc + j + 1] = (int16_t)(out[r][p] >> 16);
+        int v0 = (int)(out[r][p] & 0xFFFF), v1 = (int)(out[r][p] >> 16);
+        if (epi.accumulate) {
+          if (j < N) v0 = min(v0, min((int)C[i * ldc + j], (int)RD_INF));
+          if (j + 1 < N) v1 = min(v1, min((int)C[i * ldc + j + 1], (int)RD_INF));
+        }
+        if (j < N) C[i * ldc + j] = (int16_t)v0;
+        if (j + 1 < N) C[i * ldc + j + 1] = (int16_t)v1;
       }
     }
   }
@@ -437,12 +443,13 @@ extern "C" int rd_set_device(int device) {
 }
 
 // =========================================================== generic product ==
-extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
-                                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, int accumulate,
+                            const char *who) {
   clear_error();
-  if (!A || !B || !C) return fail(RD_EINVAL, "rd_minplus_mul_ex: NULL pointer");
-  if (M < 1 || N < 1 || K < 1) return fail(RD_EINVAL, "rd_minplus_mul_ex: M, N, K must be >= 1");
-  if (lda < K || ldb < N || ldc < N) return fail(RD_EINVAL, "rd_minplus_mul_ex: leading dimension too small");
+  if (!A || !B || !C) return fail(RD_EINVAL, "%s: NULL pointer", who);
+  if (M < 1 || N < 1 || K < 1) return fail(RD_EINVAL, "%s: M, N, K must be >= 1", who);
+  if (lda < K || ldb < N || ldc < N) return fail(RD_EINVAL, "%s: leading dimension too small", who);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, 2 * kBK2);
   const int64_t kpairs = Kp / 2;
@@ -451,15 +458,121 @@ extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B
   cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(kpairs * Np * 4), st);
   if (e != cudaSuccess) {
     cudaFreeAsync(XT, st);
-    return fail(RD_ENOMEM, "rd_minplus_mul_ex: workspace: %s", cudaGetErrorString(e));
+    return fail(RD_ENOMEM, "%s: workspace: %s", who, cudaGetErrorString(e));
   }
   int rc = pack_left(A, lda, M, K, 0, XT, Mp, kpairs, st);
   if (rc == RD_OK) rc = pack_right(B, ldb, K, N, BP, Np, kpairs, st);
   EpiArgs epi{};
+  epi.accumulate = accumulate;
   if (rc == RD_OK) rc = launch_gemm<false, false>(XT, Mp, BP, Np, kpairs, C, ldc, M, N, Mp, Np, epi, st);
   cudaFreeAsync(XT, st);
   cudaFreeAsync(BP, st);
   return rc;
+}
+
+extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
+                                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+  return minplus_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, 0, "rd_minplus_mul_ex");
+}
+
+extern "C" int rd_minplus_mul_acc(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
+                                  int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+  return minplus_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, 1, "rd_minplus_mul_acc");
+}
+
+// ------------------------------------------------------- standalone stats --
+// Stats of a row-major int16 panel `cur` (rows x cols, ld) against up to kMaxAlpha
+// earlier panels of the same shape, in the MIN-reducible layout of rd_chain_step
+// (the standalone form of the fused epilogue; HBM-bound).
+struct PanelStatsArgs {
+  const int16_t *prev[kMaxAlpha];
+  int nprev;
+};
+
+// One pass handles alphas [a0, a0 + 8) so the per-alpha state stays in registers.
+__global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
+                                                          int64_t cols, int64_t ld, int64_t diag_row0,
+                                                          PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
+  __shared__ int32_t red[8][1 + 4 * 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int na = min(8, pa.nprev - a0);
+  int32_t dmin = INT_MAX;
+  int32_t lo[8], nhi[8], nmis[8], nfin[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) { lo[a] = INT_MAX; nhi[a] = INT_MAX; nmis[a] = 0; nfin[a] = 0; }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / cols, j = e - i * cols;
+    const int64_t off = i * ld + j;
+    const int v = min((int)cur[off], (int)RD_INF);
+    if (a0 == 0 && diag_row0 + i == j) dmin = min(dmin, v);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      if (a < na) {
+        const int w = min((int)pa.prev[a0 + a][off], (int)RD_INF);
+        const bool iv = v == RD_INF, iw = w == RD_INF;
+        if (iv != iw) nmis[a] = -1;
+        if (!iv && !iw) {
+          nfin[a] = -1;
+          lo[a] = min(lo[a], v - w);
+          nhi[a] = min(nhi[a], w - v);
+        }
+      }
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    int32_t v0 = __reduce_min_sync(0xffffffffu, lo[a]);
+    int32_t v1 = __reduce_min_sync(0xffffffffu, nhi[a]);
+    int32_t v2 = __reduce_min_sync(0xffffffffu, nmis[a]);
+    int32_t v3 = __reduce_min_sync(0xffffffffu, nfin[a]);
+    if (lane == 0) {
+      red[warp][1 + 4 * a] = v0; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1 + 4 * na; e += blockDim.x) {
+    int32_t v = red[0][e];
+    for (int w = 1; w < 8; ++w) v = min(v, red[w][e]);
+    if (e == 0) {
+      if (a0 == 0) atomicMin(stats, v);
+    } else {
+      atomicMin(stats + 4 * a0 + e, v);
+    }
+  }
+}
+
+extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, int nprev, int64_t rows,
+                              int64_t cols, int64_t ld, int64_t diag_row0, int alpha_max, int32_t *stats_dev,
+                              void *cuda_stream) {
+  clear_error();
+  if (!cur || !stats_dev || (nprev > 0 && !prev)) return fail(RD_EINVAL, "rd_panel_stats: NULL argument");
+  if (alpha_max < 1 || alpha_max > kMaxAlpha || nprev < 0 || nprev > alpha_max)
+    return fail(RD_EINVAL, "rd_panel_stats: need 0 <= nprev <= alpha_max <= 32");
+  if (rows < 0 || cols < 1 || ld < cols) return fail(RD_EINVAL, "rd_panel_stats: bad shape");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  PanelStatsArgs pa{};
+  pa.nprev = nprev;
+  for (int a = 0; a < nprev; ++a) {
+    if (!prev[a]) return fail(RD_EINVAL, "rd_panel_stats: prev[%d] is NULL", a);
+    pa.prev[a] = prev[a];
+  }
+  stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, st>>>(stats_dev, alpha_max);
+  RD_CUDA_CHECK(cudaGetLastError());
+  if (rows == 0) return RD_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t want = (rows * cols + 255) / 256;
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+  for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 8) {
+    panel_stats_kernel<<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    RD_CUDA_CHECK(cudaGetLastError());
+  }
+  return RD_OK;
 }
 
 extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N) {
@@ -611,39 +724,60 @@ extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, 
   int rc = rd_chain_create(m, alpha_max, 0, N, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
 
+  // Speculative depth: up to `depth` power steps are enqueued ahead of the host decision,
+  // each with its own stats slot and async D2H copy, so launch and sync latency overlap the
+  // GEMMs of small orders.  Steps issued past the detecting power are discarded (their
+  // results are never read).  Large orders use depth 1: a step there is 10-300 ms.
+  const int depth = N >= 7000 ? 1 : (N >= 2000 ? 2 : 8);
   const int slen = rd_stats_len(alpha_max);
   int32_t *dstats = nullptr, *hstats = nullptr;
+  std::vector<cudaEvent_t> ev(depth, nullptr);
   cudaError_t e;
-  if ((e = cudaMalloc((void **)&dstats, (size_t)slen * 4)) != cudaSuccess ||
-      (e = cudaMallocHost((void **)&hstats, (size_t)slen * 4)) != cudaSuccess) {
+  if ((e = cudaMalloc((void **)&dstats, (size_t)slen * 4 * depth)) != cudaSuccess ||
+      (e = cudaMallocHost((void **)&hstats, (size_t)slen * 4 * depth)) != cudaSuccess) {
     rd_chain_destroy(c);
     cudaStreamDestroy(st);
     if (dstats) cudaFree(dstats);
     return fail(RD_ENOMEM, "rd_power_sequence: %s", cudaGetErrorString(e));
   }
+  for (int q = 0; q < depth; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
   if (diag) diag[1] = c->diag1;  // min_p A_pp: the self-loop labels
-  int found_k = -1, n0 = 0, al = 0, be = 0, k = 1;
+  int found_k = -1, n0 = 0, al = 0, be = 0, k = 1, issued = 1;
   rc = RD_OK;
   for (k = 2; k <= kmax; ++k) {
-    if ((rc = rd_chain_step(c, dstats)) != RD_OK) break;
-    if ((e = cudaMemcpyAsync(hstats, dstats, (size_t)slen * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    while (issued < kmax && issued - (k - 1) < depth) {
+      const int q = (issued + 1) % depth;
+      if ((rc = rd_chain_step(c, dstats + q * slen)) != RD_OK) break;
+      if ((e = cudaMemcpyAsync(hstats + q * slen, dstats + q * slen, (size_t)slen * 4, cudaMemcpyDeviceToHost,
+                               st)) != cudaSuccess ||
+          (e = cudaEventRecord(ev[q], st)) != cudaSuccess) {
+        rc = fail(RD_ECUDA, "rd_power_sequence: step %d: %s", issued + 1, cudaGetErrorString(e));
+        break;
+      }
+      ++issued;
+    }
+    if (rc != RD_OK) break;
+    const int q = k % depth;
+    if ((e = cudaEventSynchronize(ev[q])) != cudaSuccess) {
       rc = fail(RD_ECUDA, "rd_power_sequence: step %d: %s", k, cudaGetErrorString(e));
       break;
     }
-    if (diag) diag[k] = hstats[0] >= RD_INF ? INT32_MAX : hstats[0];
+    const int32_t *hs = hstats + q * slen;
+    if (diag) diag[k] = hs[0] >= RD_INF ? INT32_MAX : hs[0];
     int32_t a = 0, b = 0;
     if (found_k < 0) {
-      if (rd_stats_decide(hstats, alpha_max, k, 0, &a, &b)) {
+      if (rd_stats_decide(hs, alpha_max, k, 0, &a, &b)) {
         found_k = k; n0 = k - a; al = a; be = b;
         if (policy == 0) break;
       }
     } else {
       int aa = k - n0;
-      if (aa <= alpha_max && rd_stats_decide(hstats, alpha_max, k, aa, &a, &b)) { al = a; be = b; }
+      if (aa <= alpha_max && rd_stats_decide(hs, alpha_max, k, aa, &a, &b)) { al = a; be = b; }
       if (aa >= alpha_max) break;
     }
   }
+  cudaStreamSynchronize(st);
+  for (int q = 0; q < depth; ++q) cudaEventDestroy(ev[q]);
   int k_stop = std::min(k, kmax);
   cudaFree(dstats);
   cudaFreeHost(hstats);

@@ -126,3 +126,124 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
     chain.close()
     return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
                 t_build=t1 - t0, t_chain=t2 - t1)
+
+
+# ----------------------------------------------------------- all-gather form --
+def minplus_mul_allgather(A_rows, B_panel, k_bounds, group=None, acc=None):
+    """Generic distributed product (the north star's all-gather form).
+
+    Rank r holds A_rows = A[R_r, :] (M_r x K) and B_panel = B[K_r, :] (its k-rows); it
+    returns C[R_r, :] = A[R_r, :] (x) B.  B's panels travel around a ring of P2P
+    transfers (NCCL on GPUs): at step t the rank multiplies the panel of rank r - t into
+    C (C = min(C, A[:, K_{r-t}] (x) B[K_{r-t}, :]), rd_minplus_mul_acc) while the panel of
+    rank r - t - 1 is in flight, so the gather overlaps the product chunk by chunk.
+    k_bounds[s] = (k0, k1) of rank s.  acc(A_rows, k0, k1, chunk, C) overrides the
+    accumulating product (CPU tests use an oracle-backed one).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    M, K = A_rows.shape
+    N = B_panel.shape[1]
+    from . import RD_INF
+    if acc is None:
+        from . import rd_minplus_mul_acc
+
+        def acc(A_, k0, k1, chunk, C_):
+            if k1 > k0 and M > 0:
+                rd_minplus_mul_acc(A_, K, chunk, N, C_, N, M, N, k1 - k0, a_offset=k0)
+    C = torch.full((M, N), RD_INF, dtype=torch.int16, device=A_rows.device)
+    kmax_rows = max(k1 - k0 for k0, k1 in k_bounds)
+    cur = torch.empty((kmax_rows, N), dtype=B_panel.dtype, device=B_panel.device)
+    cur[:B_panel.shape[0]].copy_(B_panel)
+    nxt = torch.empty_like(cur)
+    for t in range(world):
+        src = (rank - t) % world
+        reqs = []
+        if t < world - 1:
+            ops = [dist.P2POp(dist.isend, cur, (rank + 1) % world, group),
+                   dist.P2POp(dist.irecv, nxt, (rank - 1) % world, group)]
+            reqs = dist.batch_isend_irecv(ops)
+        k0, k1 = k_bounds[src]
+        acc(A_rows, k0, k1, cur[:k1 - k0], C)
+        for q in reqs:
+            q.wait()
+        cur, nxt = nxt, cur
+    return C
+
+
+def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0, group=None,
+                             acc=None, stats=None, A=None):
+    """Algorithm 2 with the left-multiplied step A^{k+1} = A (x) A^k (powers of A commute):
+    rank r keeps the fixed panel A[R_r, :] and computes rows R_r of every power, gathering
+    all of A^k each step through minplus_mul_allgather.  Stats of the own rows against the
+    own rows of the previous powers (rd_panel_stats), all_reduce(MIN), shared decision.
+    Same result dict as power_sequence.  acc / stats override the device ops (CPU tests);
+    A (host int16 matrix, RD_INF = inf) skips the host build."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import RD_INF, count_words, rd_stats_decide, rd_build_matrix
+
+    t0 = time.perf_counter()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    N = count_words(m)
+    bounds = [panel_bounds(N, world, s) for s in range(world)]
+    r0, r1 = bounds[rank]
+    if A is None:
+        A = rd_build_matrix(m)
+    on_gpu = acc is None
+    device = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    A_rows = torch.from_numpy(np.ascontiguousarray(A[r0:r1])).to(device)
+    d = np.diag(A)[r0:r1] if r1 > r0 else np.array([], dtype=A.dtype)
+    fin = d[d < RD_INF]
+    d1 = int(fin.min()) if fin.size else 2**31 - 1
+    if world > 1:
+        tt = torch.tensor([d1], dtype=torch.int64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MIN, group=group)
+        d1 = int(tt.item())
+    if stats is None:
+        from . import rd_panel_stats, rd_stats_len
+        sbuf = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device=device)
+
+        def stats(cur, prevs):
+            return rd_panel_stats(cur, prevs, r0, alpha_max, sbuf)
+    ring = {1: A_rows.clone()}
+    if on_gpu:
+        torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    diag = [2**31 - 1] * (kmax + 1)
+    diag[1] = d1
+    found_k, n0, al, be, k = -1, 0, 0, 0, 1
+    for k in range(2, kmax + 1):
+        Xk = minplus_mul_allgather(A_rows, ring[k - 1], bounds, group, acc=acc)
+        ring[k] = Xk
+        prevs = [ring[k - a] for a in range(1, min(alpha_max, k - 1) + 1)]
+        s = stats(Xk, prevs)
+        if world > 1:
+            dist.all_reduce(s, op=dist.ReduceOp.MIN, group=group)
+        h = s.cpu().numpy()
+        ring.pop(k - alpha_max - 1, None)
+        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
+        if found_k < 0:
+            dec = rd_stats_decide(h, alpha_max, k)
+            if dec:
+                found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
+                if policy == 0:
+                    break
+        else:
+            aa = k - n0
+            if aa <= alpha_max:
+                dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
+                if dec:
+                    al, be = dec
+            if aa >= alpha_max:
+                break
+    t2 = time.perf_counter()
+    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
+                t_build=t1 - t0, t_chain=t2 - t1)

@@ -129,3 +129,85 @@ def test_gloo_world3_paper_compat_table2(golden):
     want = tuple(golden("table2_periods.json")["table2"]["4"])
     for r in range(3):
         assert (out[r]["n0"], out[r]["alpha"], out[r]["beta"]) == want
+
+
+# ------------------------------------------------------------ all-gather form --
+def _acc_oracle(A_rows, k0, k1, chunk, C):
+    if k1 <= k0 or A_rows.shape[0] == 0:
+        return
+    a = A_rows[:, k0:k1].numpy().astype(np.int32)
+    b = chunk.numpy().astype(np.int32)
+    a[a >= RINF] = OINF
+    b[b >= RINF] = OINF
+    P = O.minplus(a, b)
+    P[P == OINF] = RINF
+    C.copy_(torch.from_numpy(np.minimum(C.numpy(), P.astype(np.int16))))
+
+
+def _stats_oracle(r0, am):
+    def f(cur, prevs):
+        X = cur.numpy().astype(np.int64)
+        s = rdist.neutral_stats(am)
+        d = [X[i, r0 + i] for i in range(X.shape[0])]
+        s[0] = min(d) if d else 2**31 - 1
+        for a, P in enumerate(prevs, start=1):
+            P = P.numpy().astype(np.int64)
+            fx, fp = X < RINF, P < RINF
+            both = fx & fp
+            e = 1 + 4 * (a - 1)
+            if both.any():
+                diff = X[both] - P[both]
+                s[e], s[e + 1] = int(diff.min()), -int(diff.max())
+            s[e + 2] = -1 if (fx != fp).any() else 0
+            s[e + 3] = -1 if both.any() else 0
+        return torch.from_numpy(s)
+    return f
+
+
+def _ag_worker(rank, world, port, m, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = O.matrix(m)
+        A16 = np.where(A == OINF, RINF, A).astype(np.int16)
+        N = A.shape[0]
+        r0, _ = rdist.panel_bounds(N, world, rank)
+        # generic product first: C = X (x) A with X, A row/k-sharded
+        rng = np.random.default_rng(3)
+        X = rng.integers(0, 50, size=(N, N)).astype(np.int16)
+        bounds = [rdist.panel_bounds(N, world, s) for s in range(world)]
+        a, b = bounds[rank]
+        C = rdist.minplus_mul_allgather(torch.from_numpy(X[a:b].copy()), torch.from_numpy(A16[a:b].copy()),
+                                        bounds, acc=_acc_oracle)
+        res = rdist.power_sequence_allgather(m, 50, 10, 0, acc=_acc_oracle, stats=_stats_oracle(r0, 10), A=A16)
+        q.put((rank, (res, (a, b), C.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m", [(2, 5), (3, 5)])
+def test_gloo_allgather_product_and_chain(world, m):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ag_worker, args=(r, world, port, m, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = O.matrix(m)
+    N = A.shape[0]
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 50, size=(N, N)).astype(np.int32)
+    want = O.minplus(X, A)
+    want[want == OINF] = RINF
+    ref = O.power_chain(m, 50, 10, 0)
+    for r in range(world):
+        res, (a, b), C = out[r]
+        assert (C == want[a:b]).all()
+        assert (res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                         ref["k_stop"])
+        assert res["diag"][1:res["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]

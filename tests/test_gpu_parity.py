@@ -254,3 +254,62 @@ def test_alu_probe_reports_rates():
     assert 100 < r["dpx_minplus_per_clk_sm"] < 140     # VIADDMNMX.S16x2 at half rate: 128
     assert 100 < r["mixed_minplus_per_clk_sm"] < 200   # the DPX/IMAD mix: ~142 measured
     assert r["sm_mhz"] > 500
+
+
+# ------------------------------------------------ all-gather form building blocks
+def test_minplus_mul_acc_equals_min_of_chunk_products():
+    M, N, K = 300, 257, 1000
+    A = operand(M, K, 71, inf_frac=0.05)
+    B = operand(K, N, 72, inf_frac=0.05)
+    dA, dB = _gpu(A), _gpu(B)
+    C = torch.full((M, N), RINF, dtype=torch.int16, device="cuda")
+    cuts = [0, 130, 131, 600, K]
+    for k0, k1 in zip(cuts[:-1], cuts[1:]):
+        rd.rd_minplus_mul_acc(dA, K, dB[k0:k1].contiguous(), N, C, N, M, N, k1 - k0, a_offset=k0)
+    assert (C.cpu().numpy() == _oracle_mul(A, B)).all()
+    # accumulating into a non-INF C keeps the elementwise min
+    C0 = operand(M, N, 73, inf_frac=0.0, hi=200)
+    dC = _gpu(C0)
+    rd.rd_minplus_mul_acc(dA, K, dB, N, dC, N, M, N, K)
+    assert (dC.cpu().numpy() == np.minimum(C0, _oracle_mul(A, B))).all()
+
+
+def test_panel_stats_against_oracle_shift():
+    m, K = 5, 14
+    P = _oracle_powers(m, K)
+    am = 10
+    cur = _gpu(P[K])
+    prevs = [_gpu(P[K - a]) for a in range(1, am + 1)]
+    s = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device="cuda")
+    rd.rd_panel_stats(cur, prevs, 0, am, s)
+    st = s.cpu().numpy()
+    assert st[0] == int(np.diag(P[K]).min())
+    for a in range(1, am + 1):
+        b = O.shift(to_inf(P[K], RINF, OINF, np.int32), to_inf(P[K - a], RINF, OINF, np.int32))
+        dec = rd.rd_stats_decide(st, am, K, only_alpha=a)
+        assert (dec[1] if dec else None) == b, a
+    # a row panel with a diagonal offset, and one entry flipped to INF
+    X = P[K].copy()
+    X[40, 7] = RINF
+    s2 = rd.rd_panel_stats(_gpu(X[30:90]), [_gpu(P[K - 1][30:90])], 30, am, s).cpu().numpy()
+    assert s2[0] == int(np.diag(X)[30:90].min())
+    assert s2[3] == -1 and s2[4] == -1          # mismatch seen, finite pairs seen
+
+
+@pytest.mark.parametrize("m", [3, 5, 7])
+def test_power_sequence_allgather_single_rank(m):
+    from paper_2409_17658_b200 import dist as rdist
+    ref = O.power_chain(m, 50, 10, 0)
+    got = rdist.power_sequence_allgather(m, 50, 10)
+    assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                      ref["k_stop"])
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+def test_power_sequence_replicated_single_rank_driver():
+    from paper_2409_17658_b200 import dist as rdist
+    for m in (2, 6):
+        ref = O.power_chain(m, 50, 10, 0)
+        got = rdist.power_sequence(m, 50, 10)
+        assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                          ref["k_stop"])
