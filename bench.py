@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8, 9])
+    p.add_argument("--form", default="replicated", choices=["replicated", "allgather"],
+                   help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
+                        "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step")
     return p.parse_args()
 
 
@@ -192,8 +195,41 @@ def run_ours(args, rank, world, local_rank):
     launches_per_step = 2 if chain is not None else 0   # stats init + GEMM (librd kernels)
 
     k_state = {"k": 1, "found": None}
+    if args.form == "allgather":
+        bounds = [rdist.panel_bounds(N, world, s) for s in range(world)]
+        A_rows = torch.from_numpy(np.ascontiguousarray(rd.rd_build_matrix(m)[r0:r1])).to(dev)
+        ag = {"ring": {1: A_rows.clone()}}
+        if chain is not None:
+            chain.close()
+            chain = None
+        launches_per_step = 3 * world + 3   # per ring chunk: pack_left, pack_right, GEMM; stats init + 2 stats passes
+
+    def step_allgather(ev=None):
+        k = k_state["k"] + 1
+        with torch.cuda.stream(stream):
+            if ev is not None:
+                ev[0].record(stream)
+            X = rdist.minplus_mul_allgather(A_rows, ag["ring"][k - 1], bounds)
+            ag["ring"][k] = X
+            prevs = [ag["ring"][k - a] for a in range(1, min(am, k - 1) + 1)]
+            rd.rd_panel_stats(X, prevs, r0, am, stats, stream=stream)
+            ag["ring"].pop(k - am - 1, None)
+            if ev is not None:
+                ev[1].record(stream)
+            if world > 1:
+                dist.all_reduce(stats, op=dist.ReduceOp.MIN)
+            hstats.copy_(stats, non_blocking=True)
+        stream.synchronize()
+        k_state["k"] = k
+        h = hstats.numpy()
+        if k_state["found"] is None:
+            dec = rd.rd_stats_decide(h, am, k)
+            if dec:
+                k_state["found"] = (k - dec[0], dec[0], dec[1])
 
     def step(ev=None):
+        if args.form == "allgather":
+            return step_allgather(ev)
         with torch.cuda.stream(stream):
             if ev is not None:
                 ev[0].record(stream)
@@ -230,7 +266,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
     elapsed = t_start.elapsed_time(t_end) * 1e-3
-    gemm_s = statistics.mean(a.elapsed_time(b) for a, b in evs) * 1e-3 if chain is not None else 0.0
+    gemm_s = statistics.mean(a.elapsed_time(b) for a, b in evs) * 1e-3 if (chain is not None or args.form == "allgather") else 0.0
     t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -306,7 +342,7 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "i16",
             "data": "deterministic A(G) of P_m (no dataset); powers computed in the timed steps",
             "config": {"workload": f"P_{m} box C_n: power step A^k = A^(k-1) (x) A(G), N = C_{m} = {N}",
-                       "m": m, "N": N, "alpha_max": am, "parallelism": f"row panels x{world}",
+                       "m": m, "N": N, "alpha_max": am, "parallelism": f"row panels x{world}", "form": args.form,
                        "l2": "operands (2N^2 B = %.0f MB each) exceed L2; no flush" % (2 * N * N / 1e6),
                        "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",

@@ -443,6 +443,21 @@ extern "C" int rd_set_device(int device) {
 }
 
 // =========================================================== generic product ==
+// Keep stream-ordered workspace in the device's default pool across stream syncs (the
+// default release threshold of 0 would return ~2 GB to the driver after every call).
+static int retain_default_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && done[dev]) return RD_OK;
+  cudaMemPool_t pool;
+  RD_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  RD_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (dev >= 0 && dev < 64) done[dev] = true;
+  return RD_OK;
+}
+
 static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, int accumulate,
                             const char *who) {
@@ -454,6 +469,7 @@ static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int
   const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, 2 * kBK2);
   const int64_t kpairs = Kp / 2;
   uint32_t *XT = nullptr, *BP = nullptr;
+  if (int rc0 = retain_default_pool()) return rc0;
   RD_CUDA_CHECK(cudaMallocAsync((void **)&XT, (size_t)(kpairs * Mp * 4), st));
   cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(kpairs * Np * 4), st);
   if (e != cudaSuccess) {
@@ -490,33 +506,72 @@ struct PanelStatsArgs {
 };
 
 // One pass handles alphas [a0, a0 + 8) so the per-alpha state stays in registers.
+// blockIdx.y walks rows; each thread takes 8 consecutive columns (one 16-byte load per
+// array when aligned) and works on s16x2 pairs like the fused epilogue.
+__device__ __forceinline__ void stats_pair(uint32_t o, uint32_t w, uint32_t &lo2, uint32_t &hi2, uint32_t &mis,
+                                           uint32_t &fin) {
+  const uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
+  mis |= eo ^ ew;
+  const uint32_t fm = ~(eo | ew);
+  fin |= fm;
+  const uint32_t d = __vsub2(o, w);
+  lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
+  hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
+}
+
 __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
                                                           int64_t cols, int64_t ld, int64_t diag_row0,
                                                           PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
   __shared__ int32_t red[8][1 + 4 * 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t total = rows * cols;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int na = min(8, pa.nprev - a0);
   int32_t dmin = INT_MAX;
-  int32_t lo[8], nhi[8], nmis[8], nfin[8];
+  uint32_t lo2[8], hi2[8], mis[8], fin[8];
 #pragma unroll
-  for (int a = 0; a < 8; ++a) { lo[a] = INT_MAX; nhi[a] = INT_MAX; nmis[a] = 0; nfin[a] = 0; }
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int64_t i = e / cols, j = e - i * cols;
-    const int64_t off = i * ld + j;
-    const int v = min((int)cur[off], (int)RD_INF);
-    if (a0 == 0 && diag_row0 + i == j) dmin = min(dmin, v);
+  for (int a = 0; a < 8; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  const bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const int64_t gi = diag_row0 + i;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x * 8) {
+      const int64_t off = i * ld + j;
+      uint32_t o[4];
+      const bool full = vec && j + 8 <= cols;
+      if (full) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(cur + off);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+      } else {
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      if (a < na) {
-        const int w = min((int)pa.prev[a0 + a][off], (int)RD_INF);
-        const bool iv = v == RD_INF, iw = w == RD_INF;
-        if (iv != iw) nmis[a] = -1;
-        if (!iv && !iw) {
-          nfin[a] = -1;
-          lo[a] = min(lo[a], v - w);
-          nhi[a] = min(nhi[a], w - v);
+        for (int q = 0; q < 4; ++q) {
+          uint32_t lo = (j + 2 * q < cols) ? (uint16_t)cur[off + 2 * q] : (uint16_t)RD_INF;
+          uint32_t hi = (j + 2 * q + 1 < cols) ? (uint16_t)cur[off + 2 * q + 1] : (uint16_t)RD_INF;
+          o[q] = lo | (hi << 16);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q], kInf2);
+      if (a0 == 0 && gi >= j && gi < j + 8) {
+        const int t = (int)(gi - j);
+        dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
+      }
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        if (a < na) {
+          const int16_t *P = pa.prev[a0 + a];
+          uint32_t w[4];
+          if (full) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(P + off);
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t lo = (j + 2 * q < cols) ? (uint16_t)P[off + 2 * q] : (uint16_t)RD_INF;
+              uint32_t hi = (j + 2 * q + 1 < cols) ? (uint16_t)P[off + 2 * q + 1] : (uint16_t)RD_INF;
+              w[q] = lo | (hi << 16);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q], kInf2), lo2[a], hi2[a], mis[a], fin[a]);
         }
       }
     }
@@ -525,10 +580,13 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
   if (lane == 0) red[warp][0] = dmin;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
-    int32_t v0 = __reduce_min_sync(0xffffffffu, lo[a]);
-    int32_t v1 = __reduce_min_sync(0xffffffffu, nhi[a]);
-    int32_t v2 = __reduce_min_sync(0xffffffffu, nmis[a]);
-    int32_t v3 = __reduce_min_sync(0xffffffffu, nfin[a]);
+    int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
+    if (!fin[a]) { lo = INT_MAX; hi = INT_MIN + 1; }
+    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    int32_t v2 = __reduce_min_sync(0xffffffffu, mis[a] ? -1 : 0);
+    int32_t v3 = __reduce_min_sync(0xffffffffu, fin[a] ? -1 : 0);
     if (lane == 0) {
       red[warp][1 + 4 * a] = v0; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
     }
@@ -566,10 +624,11 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t want = (rows * cols + 255) / 256;
-  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+  // x covers a row (8 columns per thread); y walks rows, ~8 blocks per SM in total
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cols + 2047) / 2048, 64));
+  const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sms * 8 / gx + 1));
   for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 8) {
-    panel_stats_kernel<<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    panel_stats_kernel<<<dim3(gx, gy), 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
     RD_CUDA_CHECK(cudaGetLastError());
   }
   return RD_OK;
