@@ -155,6 +155,15 @@ int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, vo
                     rd_chain **out);
 int rd_chain_destroy(rd_chain *c);
 
+/* As rd_chain_create with the step method (0 dense GEMM, 1 structured, see
+ * rd_power_sequence_ex2).  rd_chain_step / read_rows / destroy work with either. */
+int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
+                       void *cuda_stream, rd_chain **out);
+
+/* (min,+) terms one rd_chain_step evaluates (the algorithmic count of its method):
+ * rows * N * N for method 0, rows * nnz(A) for method 1. */
+double rd_chain_terms_per_step(const rd_chain *c);
+
 /* Order N = C_m of the chain's matrices; current power k (1 after create). */
 int64_t rd_chain_order(const rd_chain *c);
 int rd_chain_current_k(const rd_chain *c);

@@ -55,6 +55,9 @@ def lib():
         L.rd_power_sequence_ex.argtypes = [ci, ci, ci, ci, p, p]
         L.rd_roman_cylinder.argtypes = [ci, i64, p]
         L.rd_chain_create.argtypes = [ci, ci, i64, i64, p, p]
+        L.rd_chain_create_ex.argtypes = [ci, ci, i64, i64, ci, p, p]
+        L.rd_chain_terms_per_step.argtypes = [p]; L.rd_chain_terms_per_step.restype = ctypes.c_double
+        L.rd_power_sequence_ex2.argtypes = [ci, ci, ci, ci, ci, p, p]
         L.rd_chain_destroy.argtypes = [p]
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
@@ -69,7 +72,7 @@ def lib():
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
                   "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
-                  "rd_minplus_mul_acc", "rd_panel_stats"):
+                  "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -179,13 +182,14 @@ def rd_panel_stats(cur, prevs, diag_row0: int, alpha_max: int, stats, stream=Non
     return stats
 
 
-def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0):
-    """Algorithm 2 on the GPU: dict(found, n0, alpha, beta, k_stop, diag)."""
+def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0, method: int = 0):
+    """Algorithm 2 on the GPU: dict(found, n0, alpha, beta, k_stop, diag).
+    method 0: dense (min,+) GEMM steps; 1: structured steps (finite terms only, NEXT-3)."""
     _sync_device()
     out = _Period()
     diag = np.zeros(kmax + 1, dtype=np.int32)
-    rc = _check(lib().rd_power_sequence_ex(m, kmax, alpha_max, policy, ctypes.byref(out), _np_ptr(diag)),
-                allow=(RD_OK, RD_NOTFOUND))
+    rc = _check(lib().rd_power_sequence_ex2(m, kmax, alpha_max, policy, method, ctypes.byref(out),
+                                            _np_ptr(diag)), allow=(RD_OK, RD_NOTFOUND))
     return dict(found=bool(out.found), n0=out.n0, alpha=out.alpha, beta=out.beta, k_stop=out.k_stop,
                 diag=[int(x) for x in diag], status=rc)
 
@@ -217,7 +221,7 @@ class Chain:
     (rd_chain_*).  step() enqueues A^{k+1} = A^k (x) A with the fused stats."""
 
     def __init__(self, m: int, alpha_max: int = 10, row_begin: int = 0, row_end: int | None = None,
-                 stream=None):
+                 stream=None, method: int = 0):
         import torch
         _sync_device()
         self.m, self.alpha_max = m, alpha_max
@@ -226,11 +230,17 @@ class Chain:
             row_end = count_words(m)
         self.row_begin, self.row_end = row_begin, row_end
         h = ctypes.c_void_p()
-        _check(lib().rd_chain_create(m, alpha_max, row_begin, row_end, _stream_ptr(self.stream),
-                                     ctypes.byref(h)))
+        _check(lib().rd_chain_create_ex(m, alpha_max, row_begin, row_end, method, _stream_ptr(self.stream),
+                                        ctypes.byref(h)))
+        self.method = method
         self._h = h
         self.N = lib().rd_chain_order(h)
         self.stats = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device="cuda")
+
+    @property
+    def terms_per_step(self) -> float:
+        """(min,+) terms one step evaluates (rows*N*N dense, rows*nnz(A) structured)."""
+        return lib().rd_chain_terms_per_step(self._h)
 
     @property
     def diag1(self) -> int:

@@ -112,6 +112,17 @@ __global__ void stats_init_kernel(int32_t *s, int alpha_max) {
   s[i] = (i == 0 || q == 0 || q == 1) ? INT_MAX : 0;
 }
 
+__device__ __forceinline__ void stats_pair(uint32_t o, uint32_t w, uint32_t &lo2, uint32_t &hi2, uint32_t &mis,
+                                           uint32_t &fin) {
+  const uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
+  mis |= eo ^ ew;
+  const uint32_t fm = ~(eo | ew);
+  fin |= fm;
+  const uint32_t d = __vsub2(o, w);
+  lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
+  hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
+}
+
 // --------------------------------------------------------------------- GEMM --
 struct EpiArgs {
   const uint32_t *prev[kMaxAlpha];  // PM slots of A^{k+1-a}, a = 1..nprev, same ld as C
@@ -508,16 +519,6 @@ struct PanelStatsArgs {
 // One pass handles alphas [a0, a0 + 8) so the per-alpha state stays in registers.
 // blockIdx.y walks rows; each thread takes 8 consecutive columns (one 16-byte load per
 // array when aligned) and works on s16x2 pairs like the fused epilogue.
-__device__ __forceinline__ void stats_pair(uint32_t o, uint32_t w, uint32_t &lo2, uint32_t &hi2, uint32_t &mis,
-                                           uint32_t &fin) {
-  const uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
-  mis |= eo ^ ew;
-  const uint32_t fm = ~(eo | ew);
-  fin |= fm;
-  const uint32_t d = __vsub2(o, w);
-  lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
-  hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
-}
 
 __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
                                                           int64_t cols, int64_t ld, int64_t diag_row0,
@@ -641,21 +642,235 @@ extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, in
   return rd_minplus_mul_ex(A, N, B, N, C, N, N, N, N, nullptr);
 }
 
+namespace {
+// ======================================================= structured step ==
+// NEXT-3: the right operand of every power step is the fixed, sparse A(G)
+// (0.55% dense at m = 9), so C[i][j] = min_{q : A[q][j] finite} (X[i][q] + A[q][j]) — the
+// same (min,+) product with the infinite terms skipped, N * nnz(A) terms per
+// step instead of N^3.  Layout "RP" (row pairs): RP[p][j] = X[2p][j] | X[2p+1][j] << 16.
+// One CTA owns 4 rows (2 row pairs); the q-range of those rows is staged in shared memory
+// as uint2 (both pairs of one q), chunked when N * 8 B exceeds shared memory.  A warp
+// takes one output column at a time: its lanes split the column's CSC entries
+// (q, w), each lane gathers xs[q] and applies two VIADDMNMX.S16x2 (4 rows), and a
+// butterfly of VIMNMX folds the lanes.  The diagonal min and the per-alpha periodicity
+// stats are fused (lane a owns alpha a+1), as in the dense epilogue.
+struct SpArgs {
+  const int32_t *colptr;  // nchunks x (N + 1) absolute offsets into ent
+  const uint32_t *ent;    // (q - chunk start) | w << 17
+  int nchunks, Qc;
+  int64_t N;              // columns
+};
+
+constexpr int kSpThreads = 512;        // 16 warps; 1 CTA per SM (shared memory)
+constexpr int kSpMaxAlpha = 16;        // lanes own alphas l+1 and l+9 of their 8-lane group
+constexpr int kSpGroup = 8;            // lanes per output column
+
+template <bool STATS>
+__global__ void __launch_bounds__(kSpThreads, 1)
+minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uint32_t *__restrict__ C,
+                      EpiArgs epi) {
+  extern __shared__ __align__(16) uint2 xs[];
+  __shared__ int32_t red[kSpThreads / 32][1 + 4 * kSpMaxAlpha];
+  __shared__ int next_col;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 3, sl = lane & 7;        // column group in the warp, lane in the group
+  const int64_t p0 = 2 * (int64_t)blockIdx.x;
+  const uint32_t *x0 = X + p0 * ld, *x1 = x0 + ld;
+  uint32_t *c0 = C + p0 * ld, *c1 = c0 + ld;
+  const int64_t N = sa.N;
+  constexpr int kWarps = kSpThreads / 32;
+  const int64_t gi0 = epi.diag_row0 + 2 * p0;
+  uint32_t lo2[2] = {0x7FFF7FFFu, 0x7FFF7FFFu}, hi2[2] = {0x80008000u, 0x80008000u}, mis[2] = {0, 0},
+           fin[2] = {0, 0};
+  int32_t dmin = INT_MAX;
+  for (int ch = 0; ch < sa.nchunks; ++ch) {
+    const int64_t q0 = (int64_t)ch * sa.Qc;
+    const int qn = (int)min((int64_t)sa.Qc, N - q0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < qn; q += kSpThreads) xs[q] = make_uint2(x0[q0 + q], x1[q0 + q]);
+    __syncthreads();
+    const int32_t *cp = sa.colptr + (int64_t)ch * (N + 1);
+    const bool last = ch == sa.nchunks - 1;
+    if (threadIdx.x == 0) next_col = 0;
+    __syncthreads();
+    // dynamic distribution: a warp grabs 4 consecutive columns (one per 8-lane group) at a
+    // time, so warps stay balanced although column in-degrees vary by two orders
+    for (;;) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&next_col, 4);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= N) break;
+      const int64_t j = base + g;
+      const bool valid = j < N;
+      int s = 0, e = 0;
+      if (valid) { s = __ldg(cp + j); e = __ldg(cp + j + 1); }
+      uint32_t a0 = kInf2, a1 = kInf2;
+      if (valid) {
+        for (int t = s + sl; t < e; t += kSpGroup) {
+          const uint32_t en = __ldg(sa.ent + t);
+          const uint32_t w = en >> 17;
+          const uint2 xv = xs[en & 0x1FFFFu];
+          const uint32_t w2 = w | (w << 16);
+          a0 = __viaddmin_s16x2(xv.x, w2, a0);
+          a1 = __viaddmin_s16x2(xv.y, w2, a1);
+        }
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        a0 = __vmins2(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+        a1 = __vmins2(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+      }
+      if (!valid) continue;
+      if (ch > 0) {
+        a0 = __vmins2(a0, c0[j]);
+        a1 = __vmins2(a1, c1[j]);
+      }
+      if (sl == 0) c0[j] = a0;
+      if (sl == 1) c1[j] = a1;
+      if (STATS && last) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = sl + 8 * h;
+          if (a < epi.nprev) {
+            const uint32_t *P = epi.prev[a];
+            stats_pair(a0, P[p0 * ld + j], lo2[h], hi2[h], mis[h], fin[h]);
+            stats_pair(a1, P[(p0 + 1) * ld + j], lo2[h], hi2[h], mis[h], fin[h]);
+          }
+        }
+        if (sl == 0 && j >= gi0 && j < gi0 + 4) {
+          const int t = (int)(j - gi0);
+          const uint32_t w = t < 2 ? a0 : a1;
+          dmin = min(dmin, (int)((w >> (16 * (t & 1))) & 0xFFFF));
+        }
+      }
+    }
+  }
+  if (!STATS) return;
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int32_t lo = min((int32_t)(int16_t)(lo2[h] & 0xFFFF), (int32_t)(int16_t)(lo2[h] >> 16));
+    int32_t nhi = -max((int32_t)(int16_t)(hi2[h] & 0xFFFF), (int32_t)(int16_t)(hi2[h] >> 16));
+    int32_t nm = mis[h] ? -1 : 0, nf = fin[h] ? -1 : 0;
+    if (!fin[h]) { lo = INT_MAX; nhi = INT_MAX; }
+    // combine the 4 column groups (lanes sl, sl+8, sl+16, sl+24 own the same alpha)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      nhi = min(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+      nm = min(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+      nf = min(nf, __shfl_xor_sync(0xffffffffu, nf, o));
+    }
+    const int a = sl + 8 * h;
+    if (g == 0 && a < epi.nprev) {
+      red[warp][1 + 4 * a + 0] = lo;
+      red[warp][1 + 4 * a + 1] = nhi;
+      red[warp][1 + 4 * a + 2] = nm;
+      red[warp][1 + 4 * a + 3] = nf;
+    }
+  }
+  if (lane == 0) red[warp][0] = dmin;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1 + 4 * epi.nprev; e += kSpThreads) {
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) v = min(v, red[w][e]);
+    atomicMin(epi.stats + e, v);
+  }
+}
+
+// Row-major int16 rows [row0, row0+rows) of X (ld) -> RP u32 [pairs][ldr], INF padded.
+__global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+                               int64_t row0, uint32_t *__restrict__ RP, int64_t ldr, int64_t pairs) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, p = blockIdx.y;
+  if (j >= ldr || p >= pairs) return;
+  uint32_t lo = RD_INF, hi = RD_INF;
+  if (j < cols) {
+    if (2 * p < rows) lo = (uint32_t)min((int)X[(row0 + 2 * p) * ld + j], (int)RD_INF);
+    if (2 * p + 1 < rows) hi = (uint32_t)min((int)X[(row0 + 2 * p + 1) * ld + j], (int)RD_INF);
+  }
+  RP[p * ldr + j] = lo | (hi << 16);
+}
+
+// RP -> row-major int16 rows x cols
+__global__ void unpack_rp_kernel(const uint32_t *__restrict__ RP, int64_t ldr, int64_t rows, int64_t cols,
+                                 int16_t *__restrict__ X) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (i >= rows || j >= cols) return;
+  const uint32_t w = RP[(i >> 1) * ldr + j];
+  X[i * cols + j] = (int16_t)((i & 1) ? (w >> 16) : (w & 0xFFFF));
+}
+
+}  // namespace
+
+namespace {
+constexpr int kSpSmemMax = 227 * 1024 - 8 * 1024;  // dynamic smem for xs (static red[] aside: 4.2 KB)
+
+// CSC of the right operand per q-chunk, from the row-major host matrix (OpenMP over
+// column blocks).  Entries (q - q0) | w << 17, q ascending within a column.
+void build_csc(const int16_t *A, int64_t N, int nchunks, int Qc, std::vector<int32_t> &colptr,
+               std::vector<uint32_t> &ent) {
+  colptr.assign((size_t)nchunks * (N + 1), 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int64_t q0 = (int64_t)ch * Qc, q1 = std::min(N, q0 + Qc);
+    int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t jb = 0; jb < N; jb += 256) {
+      const int64_t je = std::min(N, jb + 256);
+      for (int64_t q = q0; q < q1; ++q) {
+        const int16_t *row = A + q * N;
+        for (int64_t j = jb; j < je; ++j)
+          if (row[j] < RD_INF) cp[j + 1]++;
+      }
+    }
+  }
+  int64_t total = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    cp[0] = (int32_t)total;
+    for (int64_t j = 0; j < N; ++j) { total += cp[j + 1]; cp[j + 1] = (int32_t)total; }
+  }
+  ent.assign((size_t)std::max<int64_t>(total, 1), 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int64_t q0 = (int64_t)ch * Qc, q1 = std::min(N, q0 + Qc);
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t jb = 0; jb < N; jb += 256) {
+      const int64_t je = std::min(N, jb + 256);
+      std::vector<int32_t> pos(cp + jb, cp + je);
+      for (int64_t q = q0; q < q1; ++q) {
+        const int16_t *row = A + q * N;
+        for (int64_t j = jb; j < je; ++j)
+          if (row[j] < RD_INF) ent[pos[j - jb]++] = (uint32_t)(q - q0) | ((uint32_t)row[j] << 17);
+      }
+    }
+  }
+}
+}  // namespace
+
 // ================================================================ power chain ==
 struct rd_chain {
-  int m = 0, alpha_max = 0, k = 0, device = 0;
+  int m = 0, alpha_max = 0, k = 0, device = 0, method = 0;
   int64_t N = 0, P = 0, r0 = 0, r1 = 0, Mr = 0, Mp = 0;
   cudaStream_t st = nullptr;
-  uint32_t *BP = nullptr;    // packed A, [P/2][P]
-  uint32_t *ring = nullptr;  // (alpha_max+1) PM slots, each [P/2][Mp]
+  uint32_t *BP = nullptr;    // method 0: packed A, [P/2][P]
+  uint32_t *ring = nullptr;  // method 0: (alpha_max+1) PM slots [P/2][Mp]; method 1: RP slots [Mp/2][P]
   int64_t slot_words = 0;
   int32_t diag1 = INT32_MAX;  // min_p A_pp (self-loop labels), for diag[1]
+  // method 1 (structured step): CSC of A per q-chunk
+  int32_t *colptr = nullptr;
+  uint32_t *ent = nullptr;
+  int nchunks = 0, Qc = 0;
+  int64_t nnz = 0;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
 };
 
-extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
-                               rd_chain **out) {
+extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
+                                  void *cuda_stream, rd_chain **out) {
   clear_error();
+  if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_chain_create: method must be 0 (dense) or 1 (structured)");
+  if (method == 1 && alpha_max > kSpMaxAlpha)
+    return fail(RD_EINVAL, "rd_chain_create: the structured step supports alpha_max <= %d", kSpMaxAlpha);
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
@@ -666,16 +881,23 @@ extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t 
                 (long long)row_end, (long long)N);
   rd_chain *c = new rd_chain;
   c->m = m;
+  c->method = method;
   c->alpha_max = alpha_max;
   c->N = N;
-  c->P = round_up(N, kTile);
   c->r0 = row_begin;
   c->r1 = row_end;
   c->Mr = row_end - row_begin;
-  c->Mp = round_up(c->Mr, kTile);
   c->st = (cudaStream_t)cuda_stream;
   cudaGetDevice(&c->device);
-  c->slot_words = (c->P / 2) * c->Mp;
+  if (method == 0) {
+    c->P = round_up(N, kTile);
+    c->Mp = round_up(c->Mr, kTile);
+    c->slot_words = (c->P / 2) * c->Mp;
+  } else {
+    c->P = round_up(N, 4);          // RP pitch (u32 per row pair)
+    c->Mp = round_up(c->Mr, 4);     // whole CTAs of 4 rows
+    c->slot_words = (c->Mp / 2) * c->P;
+  }
 
   std::vector<int16_t> A((size_t)(N * N));
   int rc = build_matrix(m, A.data(), N);
@@ -688,10 +910,41 @@ extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t 
     if (dA) cudaFree(dA);
     if (c->BP) cudaFree(c->BP);
     if (c->ring) cudaFree(c->ring);
+    if (c->colptr) cudaFree(c->colptr);
+    if (c->ent) cudaFree(c->ent);
     delete c;
     return code;
   };
   cudaError_t e;
+  if (method == 1) {
+    c->nchunks = (int)((N * 8 + kSpSmemMax - 1) / kSpSmemMax);
+    c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);
+    std::vector<int32_t> colptr;
+    std::vector<uint32_t> ent;
+    build_csc(A.data(), N, c->nchunks, c->Qc, colptr, ent);
+    c->nnz = colptr.back();
+    if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
+      return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
+    if ((e = cudaMemcpyAsync(c->colptr, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(c->ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dA, A.data(), (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+      return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
+    int64_t n = (alpha_max + 1) * c->slot_words;
+    fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
+    dim3 grid((unsigned)((c->P + 255) / 256), (unsigned)(c->Mp / 2));
+    pack_rp_kernel<<<grid, 256, 0, c->st>>>(dA, N, c->Mr, N, c->r0, c->slot(1), c->P, c->Mp / 2);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
+      return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
+    cudaFree(dA);
+    dA = nullptr;
+    c->k = 1;
+    *out = c;
+    return RD_OK;
+  }
   if ((e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
       (e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
       (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
@@ -715,10 +968,17 @@ extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t 
   return RD_OK;
 }
 
+extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
+                               rd_chain **out) {
+  return rd_chain_create_ex(m, alpha_max, row_begin, row_end, 0, cuda_stream, out);
+}
+
 extern "C" int rd_chain_destroy(rd_chain *c) {
   if (!c) return RD_OK;
   if (c->BP) cudaFree(c->BP);
   if (c->ring) cudaFree(c->ring);
+  if (c->colptr) cudaFree(c->colptr);
+  if (c->ent) cudaFree(c->ent);
   delete c;
   return RD_OK;
 }
@@ -726,6 +986,10 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
 extern "C" int64_t rd_chain_order(const rd_chain *c) { return c ? c->N : -1; }
 extern "C" int rd_chain_current_k(const rd_chain *c) { return c ? c->k : -1; }
 extern "C" int32_t rd_chain_diag1(const rd_chain *c) { return c ? c->diag1 : INT32_MAX; }
+extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
+  if (!c) return -1.0;
+  return c->method == 0 ? (double)c->Mr * (double)c->N * (double)c->N : (double)c->Mr * (double)c->nnz;
+}
 
 extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   clear_error();
@@ -738,6 +1002,20 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   epi.diag_row0 = c->r0;
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
+  if (c->method == 1) {
+    static bool attr_set[64] = {};
+    if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
+      RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSpSmemMax));
+      attr_set[c->device] = true;
+    }
+    SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N};
+    minplus_sparse_kernel<true><<<(unsigned)(c->Mp / 4), kSpThreads, (size_t)c->Qc * 8, c->st>>>(
+        c->slot(c->k), c->P, sa, c->slot(knew), epi);
+    RD_CUDA_CHECK(cudaGetLastError());
+    c->k = knew;
+    return RD_OK;
+  }
   int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
                                    c->N, c->Mp, c->P, epi, c->st);
   if (rc != RD_OK) return rc;
@@ -753,7 +1031,10 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
   int16_t *d = nullptr;
   RD_CUDA_CHECK(cudaMallocAsync((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
   dim3 grid((unsigned)((c->N + 255) / 256), (unsigned)c->Mr);
-  unpack_pm_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->Mp, c->Mr, c->N, d);
+  if (c->method == 0)
+    unpack_pm_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->Mp, c->Mr, c->N, d);
+  else
+    unpack_rp_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->P, c->Mr, c->N, d);
   cudaError_t e = cudaMemcpyAsync(host_out, d, (size_t)(c->Mr * c->N * 2), cudaMemcpyDeviceToHost, c->st);
   cudaFreeAsync(d, c->st);
   if (e != cudaSuccess) return fail(RD_ECUDA, "rd_chain_read_rows: %s", cudaGetErrorString(e));
@@ -762,8 +1043,8 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
 }
 
 // ============================================================ power sequence ==
-extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out,
-                                    int32_t *diag) {
+extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                                     int32_t *diag) {
   clear_error();
   if (!out) return fail(RD_EINVAL, "rd_power_sequence: out is NULL");
   *out = rd_period_t{0, 0, 0, 0, 0};
@@ -780,14 +1061,14 @@ extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, 
   cudaStream_t st;
   RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   rd_chain *c = nullptr;
-  int rc = rd_chain_create(m, alpha_max, 0, N, st, &c);
+  int rc = rd_chain_create_ex(m, alpha_max, 0, N, method, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
 
   // Speculative depth: up to `depth` power steps are enqueued ahead of the host decision,
   // each with its own stats slot and async D2H copy, so launch and sync latency overlap the
   // GEMMs of small orders.  Steps issued past the detecting power are discarded (their
   // results are never read).  Large orders use depth 1: a step there is 10-300 ms.
-  const int depth = N >= 7000 ? 1 : (N >= 2000 ? 2 : 8);
+  const int depth = method == 1 ? 4 : (N >= 7000 ? 1 : (N >= 2000 ? 2 : 8));
   const int slen = rd_stats_len(alpha_max);
   int32_t *dstats = nullptr, *hstats = nullptr;
   std::vector<cudaEvent_t> ev(depth, nullptr);
@@ -849,6 +1130,11 @@ extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, 
     return RD_OK;
   }
   return RD_NOTFOUND;
+}
+
+extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out,
+                                    int32_t *diag) {
+  return rd_power_sequence_ex2(m, kmax, alpha_max, policy, 0, out, diag);
 }
 
 extern "C" int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag) {

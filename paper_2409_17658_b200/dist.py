@@ -61,7 +61,7 @@ class _EmptyPanel:
 
 
 def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0, group=None,
-                   chain_factory=None, diag1=None):
+                   chain_factory=None, diag1=None, method: int = 0):
     """Algorithm 2 over all ranks of `group`; every rank returns the same
     dict(found, n0, alpha, beta, k_stop, diag) as rd_power_sequence.
 
@@ -85,7 +85,7 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
         from . import Chain
 
         def chain_factory(m_, am_, a_, b_):
-            return Chain(m_, alpha_max=am_, row_begin=a_, row_end=b_)
+            return Chain(m_, alpha_max=am_, row_begin=a_, row_end=b_, method=method)
     device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
     chain = chain_factory(m, alpha_max, r0, r1) if r1 > r0 else _EmptyPanel(alpha_max, device)
     if diag1 is None:

@@ -313,3 +313,58 @@ def test_power_sequence_replicated_single_rank_driver():
         got = rdist.power_sequence(m, 50, 10)
         assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
                                                                           ref["k_stop"])
+
+
+# ----------------------------------------------------- structured step (NEXT-3)
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7])
+def test_structured_chain_every_power_bit_exact(m):
+    ref = O.power_chain(m, 50, 10, 0)
+    kstop = ref["k_stop"]
+    P = _oracle_powers(m, kstop)
+    ch = rd.Chain(m, alpha_max=10, method=1)
+    assert (ch.read_rows(1) == P[1]).all()
+    nnz = int((P[1] < RINF).sum())
+    assert ch.terms_per_step == float(P[1].shape[0]) * nnz
+    for k in range(2, kstop + 1):
+        st = ch.step().cpu().numpy()
+        assert (ch.read_rows(k) == P[k]).all(), (m, k)
+        assert st[0] == int(np.diag(P[k]).min()), (m, k)
+        for a in range(1, min(10, k - 1) + 1):
+            b = O.shift(to_inf(P[k], RINF, OINF, np.int32), to_inf(P[k - a], RINF, OINF, np.int32))
+            dec = rd.rd_stats_decide(st, 10, k, only_alpha=a)
+            assert (dec[1] if dec else None) == b, (m, k, a)
+    ch.close()
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 9])
+def test_structured_power_sequence_matches(m, golden):
+    got = rd.rd_power_sequence(m, 50, method=1)
+    if m <= 8:
+        ref = O.power_chain(m, 50, 10, 0)
+        assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                          ref["k_stop"])
+        assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+    else:
+        dense = rd.rd_power_sequence(9, 50, method=0)
+        assert got["diag"] == dense["diag"]
+        assert (got["n0"], got["alpha"], got["beta"]) == (22, 5, 20)
+
+
+def test_structured_panels_and_sampled_rows_m9():
+    m, K = 9, 5
+    A = O.matrix(m)
+    N = A.shape[0]
+    rows = sample_rows(N, 5, seed=19)
+    R = A[rows].copy()
+    for _ in range(2, K + 1):
+        R = O.minplus(R, A, skip=True)
+    R16 = to_inf(R, OINF, RINF, np.int16)
+    cuts = [0, 7001, 14002, N]     # ragged panels (not multiples of 4)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        ch = rd.Chain(m, alpha_max=3, row_begin=a, row_end=b, method=1)
+        for _ in range(K - 1):
+            ch.step()
+        got = ch.read_rows(K)
+        sel = [r for r in rows if a <= r < b]
+        assert (got[[r - a for r in sel]] == R16[[list(rows).index(r) for r in sel]]).all()
+        ch.close()
