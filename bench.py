@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 PAPER_K80_GOPS = {6: 99.6, 7: 156.9, 8: 143.1, 9: 166.2}   # BASELINE.md §1.1 (derived from Table 3)
 SM_COUNT = 148
+NNZ = {1: 7, 2: 33, 3: 167, 4: 836, 5: 4195, 6: 21043, 7: 105566, 8: 529584, 9: 2656733, 10: 13327868}  # nnz A(G)
 DPX_MINPLUS_PER_CLK_SM = 128      # VIADDMNMX.S16x2 at half rate: 64 lanes x 2 (measured)
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
@@ -323,6 +324,20 @@ def run_ours(args, rank, world, local_rank):
                             "total_s": round(float(tt[0] + tt[1]), 4), "k_stop": res["k_stop"],
                             "triple": [res["n0"], res["alpha"], res["beta"]],
                             "chain_gops": round((res["k_stop"] - 1) * float(nn) ** 3 / float(tt[1]) / 1e9, 1)}
+            # the structured step (NEXT-3: finite terms of the sparse right operand only),
+            # same results; its Gop/s counts its own terms (rows x nnz(A) per step)
+            if world > 1:
+                dist.barrier()
+            rs = rdist.power_sequence(mm, 50, am, method=1)
+            ts = torch.tensor([rs["t_build"], rs["t_chain"]], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+            assert (rs["n0"], rs["alpha"], rs["beta"]) == (res["n0"], res["alpha"], res["beta"])
+            ttp[str(mm)]["structured"] = {"build_s": round(float(ts[0]), 4), "chain_s": round(float(ts[1]), 4),
+                                          "total_s": round(float(ts[0] + ts[1]), 4),
+                                          "terms_per_step": NNZ.get(mm, 0) * nn,
+                                          "chain_gterms": round((rs["k_stop"] - 1) * NNZ.get(mm, 0) * nn
+                                                                / float(ts[1]) / 1e9, 1)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

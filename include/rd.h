@@ -136,8 +136,9 @@ int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t
 /* rd_roman_cylinder — gamma_R(P_m [] C_n) (Alg 1 P:257-268 via Cor 7 for n <= k_stop;
  * for larger n, Prop 8 + the finite-difference solution P:248:
  * n' = n0 + ((n - n0) mod alpha), gamma = diag[n'] + beta (n - n') / alpha).
- *   m >= 1, n >= 3.  The chain of m (kmax = 50) is computed on first use and
- *   cached per process.  Errors: RD_EINVAL, RD_NOTFOUND (no recurrence and n > 50). */
+ *   m >= 1, n >= 3.  The chain of m (kmax = 50, structured step method 1 — the
+ *   same powers as the dense GEMM, see rd_power_sequence_ex2) is computed on first use
+ *   and cached per process.  Errors: RD_EINVAL, RD_NOTFOUND (no recurrence and n > 50). */
 int rd_roman_cylinder(int m, int64_t n, int64_t *gamma);
 
 /* ---------------------------------------------------------------------------
@@ -207,6 +208,11 @@ int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, 
  * use two IMAD packed adds (fma pipe) + one VIMNMX3.S16x2 (alu) per two k-pairs
  * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
+
+/* rd_set_sparse_variant — tuning knob of the structured step (process-wide): 0: 512
+ * threads per CTA; 1: 512 threads, 2 entry loads in flight per lane; 2: 1024 threads;
+ * 3: 1024 threads, 2 in flight.  Identical results.  Errors: RD_EINVAL. */
+int rd_set_sparse_variant(int v);
 
 /* ---------------------------------------------------------------------------
  * rd_alu_probe — measures, on the current device, the issue rate of the integer

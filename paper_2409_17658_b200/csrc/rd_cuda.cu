@@ -661,11 +661,11 @@ struct SpArgs {
   int64_t N;              // columns
 };
 
-constexpr int kSpThreads = 512;        // 16 warps; 1 CTA per SM (shared memory)
+constexpr int kSpThreadsMax = 1024;    // 1 CTA per SM (shared memory); 16 or 32 warps
 constexpr int kSpMaxAlpha = 16;        // lanes own alphas l+1 and l+9 of their 8-lane group
 constexpr int kSpGroup = 8;            // lanes per output column
 
-template <bool STATS>
+template <bool STATS, int kSpThreads, int UNROLL>
 __global__ void __launch_bounds__(kSpThreads, 1)
 minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uint32_t *__restrict__ C,
                       EpiArgs epi) {
@@ -706,13 +706,20 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
       if (valid) { s = __ldg(cp + j); e = __ldg(cp + j + 1); }
       uint32_t a0 = kInf2, a1 = kInf2;
       if (valid) {
-        for (int t = s + sl; t < e; t += kSpGroup) {
-          const uint32_t en = __ldg(sa.ent + t);
-          const uint32_t w = en >> 17;
-          const uint2 xv = xs[en & 0x1FFFFu];
-          const uint32_t w2 = w | (w << 16);
-          a0 = __viaddmin_s16x2(xv.x, w2, a0);
-          a1 = __viaddmin_s16x2(xv.y, w2, a1);
+        constexpr uint32_t kSent = (uint32_t)RD_INF << 17;   // q = 0, w = RD_INF: never wins
+        for (int t = s + sl; t < e; t += UNROLL * kSpGroup) {
+          uint32_t en[UNROLL];
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u)
+            en[u] = (u == 0 || t + u * kSpGroup < e) ? __ldg(sa.ent + t + u * kSpGroup) : kSent;
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            const uint32_t w = en[u] >> 17;
+            const uint2 xv = xs[en[u] & 0x1FFFFu];
+            const uint32_t w2 = w | (w << 16);
+            a0 = __viaddmin_s16x2(xv.x, w2, a0);
+            a1 = __viaddmin_s16x2(xv.y, w2, a1);
+          }
         }
       }
 #pragma unroll
@@ -804,7 +811,7 @@ __global__ void unpack_rp_kernel(const uint32_t *__restrict__ RP, int64_t ldr, i
 }  // namespace
 
 namespace {
-constexpr int kSpSmemMax = 227 * 1024 - 8 * 1024;  // dynamic smem for xs (static red[] aside: 4.2 KB)
+constexpr int kSpSmemMax = 216 * 1024;  // dynamic smem for xs (static red[] + counter aside: <= 8.2 KB)
 
 // CSC of the right operand per q-chunk, from the row-major host matrix (OpenMP over
 // column blocks).  Entries (q - q0) | w << 17, q ascending within a column.
@@ -968,6 +975,29 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   return RD_OK;
 }
 
+static int g_sparse_variant = 3;   // rd_set_sparse_variant (default: measured best, 1024 threads)
+
+template <int THREADS, int UNROLL>
+static int launch_sparse(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
+  static bool attr_set[64] = {};
+  if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true, THREADS, UNROLL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemMax));
+    attr_set[c->device] = true;
+  }
+  minplus_sparse_kernel<true, THREADS, UNROLL><<<(unsigned)(c->Mp / 4), THREADS, (size_t)c->Qc * 8, c->st>>>(
+      c->slot(c->k), c->P, sa, c->slot(knew), epi);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+extern "C" int rd_set_sparse_variant(int v) {
+  clear_error();
+  if (v < 0 || v > 3) return fail(RD_EINVAL, "rd_set_sparse_variant: 0..3");
+  g_sparse_variant = v;
+  return RD_OK;
+}
+
 extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
                                rd_chain **out) {
   return rd_chain_create_ex(m, alpha_max, row_begin, row_end, 0, cuda_stream, out);
@@ -1003,16 +1033,15 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
   if (c->method == 1) {
-    static bool attr_set[64] = {};
-    if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
-      RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSpSmemMax));
-      attr_set[c->device] = true;
-    }
     SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N};
-    minplus_sparse_kernel<true><<<(unsigned)(c->Mp / 4), kSpThreads, (size_t)c->Qc * 8, c->st>>>(
-        c->slot(c->k), c->P, sa, c->slot(knew), epi);
-    RD_CUDA_CHECK(cudaGetLastError());
+    int rc1 = RD_OK;
+    switch (g_sparse_variant) {
+      case 1: rc1 = launch_sparse<512, 2>(c, sa, knew, epi); break;
+      case 2: rc1 = launch_sparse<1024, 1>(c, sa, knew, epi); break;
+      case 3: rc1 = launch_sparse<1024, 2>(c, sa, knew, epi); break;
+      default: rc1 = launch_sparse<512, 1>(c, sa, knew, epi); break;
+    }
+    if (rc1 != RD_OK) return rc1;
     c->k = knew;
     return RD_OK;
   }

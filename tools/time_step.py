@@ -11,6 +11,7 @@ import os
 ms = [int(x) for x in sys.argv[1:]] or [7, 8, 9]
 variants = [int(v) for v in os.environ.get("VARIANTS", "3").split(",")]
 method = int(os.environ.get("METHOD", "0"))
+rd.rd_set_sparse_variant(int(os.environ.get("SPV", "3")))
 for v, m in [(v, m) for v in variants for m in ms]:
     rd.rd_set_gemm_variant(v)
     t0 = time.time()
