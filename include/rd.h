@@ -133,6 +133,16 @@ int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag);
  *     alpha_max with A^{n0+alpha} = beta (x) A^{n0} (computes powers up to n0+alpha_max). */
 int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out, int32_t *diag);
 
+/* As rd_power_sequence_ex with the product method of every power step:
+ *   method 0: the dense (min,+) GEMM (N^3 terms per step; the north-star path);
+ *   method 1: the structured step: the right operand A(G) is fixed and
+ *             sparse, so each step evaluates only its finite terms — C[i][j] =
+ *             min_{q: A[q][j] finite} (A^k[i][q] + A[q][j]), N * nnz(A) terms.  Same
+ *             definition (an infinite term never attains a min), same results.
+ *             alpha_max <= 16 for method 1. */
+int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                          int32_t *diag);
+
 /* rd_roman_cylinder — gamma_R(P_m [] C_n) (Alg 1 P:257-268 via Cor 7 for n <= k_stop;
  * for larger n, Prop 8 + the finite-difference solution P:248:
  * n' = n0 + ((n - n0) mod alpha), gamma = diag[n'] + beta (n - n') / alpha).
