@@ -368,3 +368,41 @@ def test_structured_panels_and_sampled_rows_m9():
         sel = [r for r in rows if a <= r < b]
         assert (got[[r - a for r in sel]] == R16[[list(rows).index(r) for r in sel]]).all()
         ch.close()
+
+
+# ---------------------------------------------------------------- m = 10 (NEXT-2)
+def test_m10_structured_chain_pins():
+    # beyond the paper ("too big"): pinned by Cor 12 (P:501-507, 5 | n, m >= 10),
+    # and by the independent row DP X3 for n = 3..8
+    got = rd.rd_power_sequence(10, 50, alpha_max=10, method=1)
+    assert got["found"]
+    d = got["diag"]
+    for n in range(5, got["k_stop"] + 1, 5):
+        assert d[n] == 22 * n // 5, n
+    for n in range(3, 9):
+        assert d[n] == O.gamma_rowdp(10, n), n
+    g = O.gamma_from_chain(got, 200)
+    assert g == 22 * 200 // 5                      # Cor 12 through the recurrence
+    for n in range(10, 201, 5):
+        assert O.gamma_from_chain(got, n) == 22 * n // 5
+    for n in range(10, 201):
+        assert O.gamma_from_chain(got, n) >= -(-22 * n // 5)   # Thm 11 lower bound ceil(2(m+1)n/5)
+
+
+def test_m10_dense_equals_structured_first_powers():
+    m, K = 10, 4
+    N = rd.count_words(m)
+    rows = sample_rows(N, 8, seed=23)
+    outs = []
+    for method in (0, 1):
+        ch = rd.Chain(m, alpha_max=3, method=method)
+        for _ in range(K - 1):
+            ch.step()
+        outs.append(ch.read_rows(K)[rows])
+        ch.close()
+    assert (outs[0] == outs[1]).all()
+    A = O.matrix(m)
+    R = A[rows].copy()
+    for _ in range(K - 1):
+        R = O.minplus(R, A, skip=True)
+    assert (outs[1] == to_inf(R, OINF, RINF, np.int16)).all()
