@@ -55,6 +55,13 @@ def lib():
             getattr(L, f).argtypes = [ctypes.c_int, ctypes.c_int]
             getattr(L, f).restype = i32
         L.or_rdf_weight.argtypes = [ctypes.c_int, ctypes.c_int, p]; L.or_rdf_weight.restype = i32
+        L.or_power_chain_matrix.argtypes = [p, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, p, p, p]
+        L.or_power_chain_matrix.restype = ctypes.c_int
+        L.or_can_follow_border.argtypes = [ctypes.c_char_p, ctypes.c_char_p]; L.or_can_follow_border.restype = ctypes.c_int
+        L.or_nd.argtypes = [ctypes.c_char_p, ctypes.c_char_p]; L.or_nd.restype = ctypes.c_int
+        L.or_border_matrix.argtypes = [p]; L.or_border_matrix.restype = i64
+        L.or_border_bruteforce.argtypes = [ctypes.c_int]; L.or_border_bruteforce.restype = i32
+        L.or_border_rowdp.argtypes = [ctypes.c_int]; L.or_border_rowdp.restype = i32
         _lib = L
     return _lib
 
@@ -206,3 +213,43 @@ def rdf_weight(f) -> int:
     f = np.ascontiguousarray(f, dtype=np.int32)
     m, n = f.shape
     return int(lib().or_rdf_weight(m, n, _ptr(f)))
+
+
+# ------------------------------------------------ border / loss variant (App. A)
+def border_matrix() -> np.ndarray:
+    """The App. A matrix: 97 x 97 int32, labels 10p(a)+5p(b)-2nd (Alg 3)."""
+    n = int(lib().or_border_matrix(None))
+    A = np.empty((n, n), dtype=np.int32)
+    lib().or_border_matrix(_ptr(A))
+    return A
+
+
+def nd(q: str, p: str) -> int:
+    """Algorithm 3: newly dominated vertices nd(q, p)."""
+    return int(lib().or_nd(q.encode(), p.encode()))
+
+
+def can_follow_border(q: str, p: str) -> bool:
+    return bool(lib().or_can_follow_border(q.encode(), p.encode()))
+
+
+def power_chain_matrix(A: np.ndarray, kmax: int = 50, alpha_max: int = 10, policy: int = 0):
+    """Algorithm 2 on a given int32 matrix (INF = 2**31-1)."""
+    A = np.ascontiguousarray(A, dtype=np.int32)
+    diag = np.zeros(kmax + 1, dtype=np.int32)
+    out = np.zeros(5, dtype=np.int32)
+    rc = lib().or_power_chain_matrix(_ptr(A), A.shape[0], kmax, alpha_max, policy, _ptr(diag), _ptr(out), None)
+    if rc != 0:
+        raise ValueError("or_power_chain_matrix failed")
+    return dict(found=bool(out[0]), n0=int(out[1]), alpha=int(out[2]), beta=int(out[3]),
+                k_stop=int(out[4]), diag=[int(x) for x in diag], final=None)
+
+
+def border_bruteforce(n: int) -> int:
+    """(X6) 2 L_a(n) = min_g 5 g - 2|D(g)| over almost-RDFs of P_4 [] C_n."""
+    return int(lib().or_border_bruteforce(n))
+
+
+def border_rowdp(n: int) -> int:
+    """(X7) 2 L_a(n) by a DP over the 4 rows; n <= 10."""
+    return int(lib().or_border_rowdp(n))

@@ -234,10 +234,25 @@ int or_shift(const int32_t *P, const int32_t *Q, int64_t count, int32_t *beta) {
  * Powers are kept in a ring of alpha_max + 1 matrices.  The product used per step is
  * or_minplus_skip (identical to or_minplus).  diag must hold kmax+1 ints (diag[0] = INF).
  * out[0..4] = found, n0, alpha, beta, k_stop.  Returns 0, or -1 on bad arguments. */
+int or_power_chain_matrix(const int32_t *Ain, int64_t N, int kmax, int alpha_max, int policy, int32_t *diag,
+                          int32_t *out, int32_t *final_power);
+
 int or_power_chain(int m, int kmax, int alpha_max, int policy, int32_t *diag, int32_t *out,
                    int32_t *final_power /* nullable N*N: A^{k_stop} */) {
   if (m < 1 || kmax < 1 || alpha_max < 1) return -1;
   int64_t N = or_words(m, NULL);
+  int32_t *A = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N * N));
+  if (!A) return -1;
+  or_matrix(m, A);
+  int rc = or_power_chain_matrix(A, N, kmax, alpha_max, policy, diag, out, final_power);
+  free(A);
+  return rc;
+}
+
+/* Algorithm 2 on a given matrix (N x N int32, OR_INF = infinity): see or_power_chain. */
+int or_power_chain_matrix(const int32_t *Ain, int64_t N, int kmax, int alpha_max, int policy, int32_t *diag,
+                          int32_t *out, int32_t *final_power) {
+  if (N < 1 || kmax < 1 || alpha_max < 1) return -1;
   int64_t NN = N * N;
   int R = alpha_max + 1;
   int32_t **ring = (int32_t **)calloc((size_t)R, sizeof(int32_t *));
@@ -246,7 +261,7 @@ int or_power_chain(int m, int kmax, int alpha_max, int policy, int32_t *diag, in
     if (!ring[r]) return -1;
   }
   int32_t *A = ring[1 % R];
-  or_matrix(m, A);                      /* A^1 lives in slot 1 */
+  memcpy(A, Ain, sizeof(int32_t) * (size_t)NN);   /* A^1 lives in slot 1 */
   int32_t *A1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)NN);
   memcpy(A1, A, sizeof(int32_t) * (size_t)NN);
   for (int k = 0; k <= kmax; ++k) diag[k] = OR_INF;
@@ -455,4 +470,160 @@ int32_t or_rdf_weight(int m, int n, const int32_t *f) {
       if (!dom) return -1;
     }
   return w;
+}
+
+/* ------------------------------------------- border / loss variant (App. A) ---- */
+/* P:575-662.  The cylinder's top four rows P_4 [] C_n of P_m [] C_n (m >= 10); an almost
+ * Roman dominating function leaves row-4 zeros undominated (Def).  Words: the Def 4
+ * set (the appendix prints "ac, ca": read ad, da, R15).  Can-follow: rows 1-3 as
+ * before, row 4 as printed at P:594-599 with "p_3 = d" read p_4 = d (R15). */
+int or_can_follow_border(const char *q, const char *p) {
+  const int m = 4;
+  for (int i = 1; i <= 3; ++i) {
+    char qi = q[i - 1], pi = p[i - 1];
+    int up_a = (i >= 2) && p[i - 2] == 'a';
+    int dn_a = p[i] == 'a';
+    int ok;
+    if (i == 1) {
+      if (qi == 'a') ok = (pi == 'a') || (pi == 'c');
+      else if (qi == 'b') ok = (pi == 'c' && dn_a) || (pi == 'd');
+      else if (qi == 'c') ok = (pi == 'a') || (pi == 'b') || (pi == 'c' && dn_a) || (pi == 'd');
+      else ok = (pi == 'a');
+    } else {
+      if (qi == 'a') ok = (pi == 'a') || (pi == 'c');
+      else if (qi == 'b') ok = (pi == 'c' && up_a) || (pi == 'c' && dn_a) || (pi == 'd');
+      else if (qi == 'c') ok = (pi == 'a') || (pi == 'b') || (pi == 'c' && up_a) || (pi == 'c' && dn_a) || (pi == 'd');
+      else ok = (pi == 'a');
+    }
+    if (!ok) return 0;
+  }
+  {
+    char q4 = q[3], p4 = p[3];
+    int p3a = p[2] == 'a';
+    int ok;
+    if (q4 == 'a') ok = (p4 == 'a') || (p4 == 'c');
+    else if (q4 == 'b') ok = (p4 == 'c' && p3a) || (p4 == 'd');
+    else if (q4 == 'c') ok = (p4 == 'a') || (p4 == 'b') || (p4 == 'c' && p3a) || (p4 == 'd');
+    else ok = (p4 == 'a') || (p4 == 'b') || (p4 == 'c' && p3a) || (p4 == 'd');
+    (void)m;
+    if (!ok) return 0;
+  }
+  return 1;
+}
+
+/* Algorithm 3: newly dominated vertices nd(q, p), the switch taken in the
+ * printed order (first matching case), the case "q_i = c,d and p_i = b,c" read as the
+ * cross product (R15); +1 when p_4 = a (the row-5 cell below it). */
+int or_nd(const char *q, const char *p) {
+  int nd = 0;
+  for (int i = 0; i < 4; ++i) {
+    char qi = q[i], pi = p[i];
+    if (qi == 'a' && pi == 'a') nd += 1;
+    else if (qi == 'b' && pi == 'c') nd += 1;
+    else if (qi == 'c' && pi == 'a') nd += 2;
+    else if ((qi == 'c' || qi == 'd') && (pi == 'b' || pi == 'c')) nd += 1;
+    else if (qi == 'd' && pi == 'a') nd += 3;
+  }
+  if (p[3] == 'a') nd += 1;
+  return nd;
+}
+
+/* Border matrix: A_qp = 10 p(a) + 5 p(b) - 2 nd(q, p) on arcs, INF elsewhere. */
+int64_t or_border_matrix(int32_t *A) {
+  int64_t N = or_words(4, NULL);
+  if (!A) return N;
+  char *w = (char *)malloc((size_t)(N * 4));
+  or_words(4, w);
+  for (int64_t q = 0; q < N; ++q)
+    for (int64_t p = 0; p < N; ++p) {
+      const char *qq = w + q * 4, *pp = w + p * 4;
+      if (!or_can_follow_border(qq, pp)) { A[q * N + p] = OR_INF; continue; }
+      int na = 0, nb = 0;
+      for (int i = 0; i < 4; ++i) { na += pp[i] == 'a'; nb += pp[i] == 'b'; }
+      A[q * N + p] = 10 * na + 5 * nb - 2 * or_nd(qq, pp);
+    }
+  free(w);
+  return N;
+}
+
+/* (X6) 2 L_a(n) = min_g 5 g(P_4 [] C_n) - 2 |D(g)| by brute force over the
+ * 2-set R2 of g: with R2 fixed, a row 1-3 vertex outside N[R2] must get 1 (cost 5 - 2 = 3),
+ * a row-4 vertex outside N[R2] is best left 0 (a 1 would cost 3 > 0), every other vertex 0.
+ * N[R2] is taken in P_m [] C_n, so a 2 in row 4 also dominates the row-5 cell below it.
+ * Value = 10 |R2| - 2 |N[R2]| + 3 #(rows 1-3 outside N[R2]).  4n <= 28. */
+int32_t or_border_bruteforce(int n) {
+  int V = 4 * n;
+  if (n < 3 || V > 28) return -1;
+  uint64_t nb[32];
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < n; ++c) {
+      uint64_t s = 1ull << (r * n + c);
+      s |= 1ull << (r * n + (c + 1) % n);
+      s |= 1ull << (r * n + (c + n - 1) % n);
+      if (r > 0) s |= 1ull << ((r - 1) * n + c);
+      if (r < 3) s |= 1ull << ((r + 1) * n + c);
+      nb[r * n + c] = s;
+    }
+  uint64_t rows13 = (1ull << (3 * n)) - 1, row4 = ((1ull << n) - 1) << (3 * n);
+  int32_t best = OR_INF;
+  uint64_t full = (1ull << V) - 1;
+  for (uint64_t S = 0; S <= full; ++S) {
+    uint64_t dom = 0;
+    int k = 0;
+    for (uint64_t t = S; t; t &= t - 1) { dom |= nb[__builtin_ctzll(t)]; ++k; }
+    int row5 = __builtin_popcountll(S & row4);   /* row-5 cells below row-4 twos */
+    int nbsz = __builtin_popcountll(dom) + row5;
+    int und13 = __builtin_popcountll(rows13 & ~dom);
+    int32_t v = 10 * k - 2 * nbsz + 3 * und13;
+    if (v < best) best = v;
+    if (S == full) break;
+  }
+  return best;
+}
+
+/* (X7) the same quantity by a DP over the 4 rows (each a C_n ring, state = 2-sets of two
+ * consecutive rows).  Row r's dominated set: its own 2s and their ring neighbours plus the
+ * 2s directly above and below.  Cost of row r <= 3: 10|s_r| - 2|dom_r| + 3(n - |dom_r|);
+ * row 4: 10|s_4| - 2|dom_4| - 2|s_4| (the row-5 cells under row-4 twos).  4 * 2^{3n};
+ * n <= 11 (n = 11 takes minutes). */
+static int32_t or_bd_rowcost(uint32_t prev, uint32_t cur, uint32_t next, int n, int r) {
+  uint32_t full = (1u << n) - 1;
+  uint32_t rotl = ((cur << 1) | (cur >> (n - 1))) & full;
+  uint32_t rotr = ((cur >> 1) | (cur << (n - 1))) & full;
+  uint32_t dom = (cur | rotl | rotr | prev | next) & full;
+  int d = __builtin_popcount(dom), k = __builtin_popcount(cur);
+  if (r < 4) return 10 * k - 2 * d + 3 * (n - d);
+  return 10 * k - 2 * d - 2 * k;
+}
+int32_t or_border_rowdp(int n) {
+  if (n < 3 || n > 11) return -1;
+  int64_t S = 1ll << n;
+  int32_t *dp = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S * S));
+  int32_t *nx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S * S));
+  for (int64_t e = 0; e < S * S; ++e) dp[e] = OR_INF;
+  for (int64_t cur = 0; cur < S; ++cur) dp[cur] = 0;       /* (prev = row 0 = none, row 1 = cur) */
+  for (int r = 1; r <= 3; ++r) {                           /* charge row r, choose row r+1 */
+    for (int64_t e = 0; e < S * S; ++e) nx[e] = OR_INF;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t cur = 0; cur < S; ++cur)
+      for (int64_t prev = 0; prev < S; ++prev) {
+        int32_t base = dp[prev * S + cur];
+        if (base == OR_INF) continue;
+        for (int64_t next = 0; next < S; ++next) {
+          int32_t v = base + or_bd_rowcost((uint32_t)prev, (uint32_t)cur, (uint32_t)next, n, r);
+          if (v < nx[cur * S + next]) nx[cur * S + next] = v;
+        }
+      }
+    int32_t *t = dp; dp = nx; nx = t;
+  }
+  int32_t best = OR_INF;
+  for (int64_t prev = 0; prev < S; ++prev)
+    for (int64_t cur = 0; cur < S; ++cur) {
+      int32_t base = dp[prev * S + cur];
+      if (base == OR_INF) continue;
+      int32_t v = base + or_bd_rowcost((uint32_t)prev, (uint32_t)cur, 0u, n, 4);
+      if (v < best) best = v;
+    }
+  free(dp); free(nx);
+  return best;
 }
