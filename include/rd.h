@@ -143,6 +143,23 @@ int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t
 int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
                           int32_t *diag);
 
+/* ---------------------------------------------------------------------------
+ * Any matrix: Algorithm 2 / chains over a caller-supplied HOST matrix A (N x N int16
+ * row-major, entries in [0, RD_INF]; > RD_INF reads as +inf; negative entries are
+ * RD_EINVAL).  Used for the App. A border variant below and for general (min,+) powers.
+ * rd_power_sequence_matrix: RD_ERANGE if max finite entry * kmax >= RD_INF. */
+int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, int alpha_max, int policy, int method,
+                             rd_period_t *out, int32_t *diag);
+
+/* rd_build_matrix_border — the border / loss matrix of Appendix A for the
+ * top four rows of P_m [] C_n, m >= 10: the Def 4 words of length 4 (N = 97), the
+ * first/intermediate-row rules of P:165-183 and the fourth-row rules of P:594-599
+ * (reading "p_3 = d" as p_4 = d, R15), labels l(q,p) = 10 p(a) + 5 p(b) -
+ * 2 nd(q,p) with nd of Algorithm 3 (the case "q_i = c,d and p_i = b,c" read as
+ * the cross product, R15).  Labels lie in [0, 30].  Its diagonal gives 2 L_a(n) and its
+ * Algorithm 2 gives (30, 1, 1).  A nullable host N*N; N_out required.  Host only. */
+int rd_build_matrix_border(int16_t *A, int64_t *N_out);
+
 /* rd_roman_cylinder — gamma_R(P_m [] C_n) (Alg 1 P:257-268 via Cor 7 for n <= k_stop;
  * for larger n, Prop 8 + the finite-difference solution P:248:
  * n' = n0 + ((n - n0) mod alpha), gamma = diag[n'] + beta (n - n') / alpha).
@@ -170,6 +187,10 @@ int rd_chain_destroy(rd_chain *c);
  * rd_power_sequence_ex2).  rd_chain_step / read_rows / destroy work with either. */
 int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
                        void *cuda_stream, rd_chain **out);
+
+/* As rd_chain_create over a caller-supplied HOST matrix (see rd_power_sequence_matrix). */
+int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max, int64_t row_begin, int64_t row_end,
+                           int method, void *cuda_stream, rd_chain **out);
 
 /* (min,+) terms one rd_chain_step evaluates (the algorithmic count of its method):
  * rows * N * N for method 0, rows * nnz(A) for method 1. */

@@ -58,6 +58,9 @@ def lib():
         L.rd_chain_create_ex.argtypes = [ci, ci, i64, i64, ci, p, p]
         L.rd_chain_terms_per_step.argtypes = [p]; L.rd_chain_terms_per_step.restype = ctypes.c_double
         L.rd_power_sequence_ex2.argtypes = [ci, ci, ci, ci, ci, p, p]
+        L.rd_power_sequence_matrix.argtypes = [p, i64, ci, ci, ci, ci, p, p]
+        L.rd_build_matrix_border.argtypes = [p, p]
+        L.rd_chain_create_matrix.argtypes = [p, i64, ci, i64, i64, ci, p, p]
         L.rd_chain_destroy.argtypes = [p]
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
@@ -73,7 +76,8 @@ def lib():
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
                   "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
-                  "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant"):
+                  "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant",
+                  "rd_power_sequence_matrix", "rd_build_matrix_border", "rd_chain_create_matrix"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -119,6 +123,15 @@ def rd_build_matrix(m: int) -> np.ndarray:
     _check(lib().rd_build_matrix(m, None, ctypes.byref(n)))
     A = np.empty((n.value, n.value), dtype=np.int16)
     _check(lib().rd_build_matrix(m, _np_ptr(A), ctypes.byref(n)))
+    return A
+
+
+def rd_build_matrix_border() -> np.ndarray:
+    """The App. A border / loss matrix (97 x 97 int16, RD_INF off the arcs)."""
+    n = ctypes.c_int64()
+    _check(lib().rd_build_matrix_border(None, ctypes.byref(n)))
+    A = np.empty((n.value, n.value), dtype=np.int16)
+    _check(lib().rd_build_matrix_border(_np_ptr(A), ctypes.byref(n)))
     return A
 
 
@@ -195,6 +208,19 @@ def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int =
                 diag=[int(x) for x in diag], status=rc)
 
 
+def rd_power_sequence_matrix(A: np.ndarray, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
+                             method: int = 0):
+    """Algorithm 2 on a caller-supplied host int16 matrix (RD_INF = inf)."""
+    _sync_device()
+    A = np.ascontiguousarray(A, dtype=np.int16)
+    out = _Period()
+    diag = np.zeros(kmax + 1, dtype=np.int32)
+    rc = _check(lib().rd_power_sequence_matrix(_np_ptr(A), A.shape[0], kmax, alpha_max, policy, method,
+                                               ctypes.byref(out), _np_ptr(diag)), allow=(RD_OK, RD_NOTFOUND))
+    return dict(found=bool(out.found), n0=out.n0, alpha=out.alpha, beta=out.beta, k_stop=out.k_stop,
+                diag=[int(x) for x in diag], status=rc)
+
+
 def rd_roman_cylinder(m: int, n: int) -> int:
     """gamma_R(P_m [] C_n)."""
     _sync_device()
@@ -227,17 +253,22 @@ class Chain:
     (rd_chain_*).  step() enqueues A^{k+1} = A^k (x) A with the fused stats."""
 
     def __init__(self, m: int, alpha_max: int = 10, row_begin: int = 0, row_end: int | None = None,
-                 stream=None, method: int = 0):
+                 stream=None, method: int = 0, matrix: np.ndarray | None = None):
         import torch
         _sync_device()
         self.m, self.alpha_max = m, alpha_max
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         if row_end is None:
-            row_end = count_words(m)
+            row_end = count_words(m) if matrix is None else matrix.shape[0]
         self.row_begin, self.row_end = row_begin, row_end
         h = ctypes.c_void_p()
-        _check(lib().rd_chain_create_ex(m, alpha_max, row_begin, row_end, method, _stream_ptr(self.stream),
-                                        ctypes.byref(h)))
+        if matrix is None:
+            _check(lib().rd_chain_create_ex(m, alpha_max, row_begin, row_end, method, _stream_ptr(self.stream),
+                                            ctypes.byref(h)))
+        else:
+            Am = np.ascontiguousarray(matrix, dtype=np.int16)
+            _check(lib().rd_chain_create_matrix(_np_ptr(Am), Am.shape[0], alpha_max, row_begin, row_end, method,
+                                                _stream_ptr(self.stream), ctypes.byref(h)))
         self.method = method
         self._h = h
         self.N = lib().rd_chain_order(h)

@@ -872,20 +872,19 @@ struct rd_chain {
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
 };
 
-extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
-                                  void *cuda_stream, rd_chain **out) {
-  clear_error();
+// Creates a chain over the host matrix A (N x N int16 row-major, entries in [0, RD_INF]).
+static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_max, int64_t row_begin,
+                             int64_t row_end, int method, void *cuda_stream, rd_chain **out) {
+  if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
+  *out = nullptr;
   if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_chain_create: method must be 0 (dense) or 1 (structured)");
   if (method == 1 && alpha_max > kSpMaxAlpha)
     return fail(RD_EINVAL, "rd_chain_create: the structured step supports alpha_max <= %d", kSpMaxAlpha);
-  if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
-  *out = nullptr;
-  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
   if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_chain_create: alpha_max out of 1..32");
-  const int64_t N = count_words(m);
   if (row_begin < 0 || row_end > N || row_begin >= row_end)
     return fail(RD_EINVAL, "rd_chain_create: bad row range [%lld, %lld) for N=%lld", (long long)row_begin,
                 (long long)row_end, (long long)N);
+  if (method == 1 && N >= (1 << 17)) return fail(RD_EINVAL, "rd_chain_create: structured step needs N < 131072");
   rd_chain *c = new rd_chain;
   c->m = m;
   c->method = method;
@@ -905,10 +904,7 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
     c->Mp = round_up(c->Mr, 4);     // whole CTAs of 4 rows
     c->slot_words = (c->Mp / 2) * c->P;
   }
-
-  std::vector<int16_t> A((size_t)(N * N));
-  int rc = build_matrix(m, A.data(), N);
-  if (rc != RD_OK) { delete c; return rc; }
+  const int16_t *A = Ahost;
   for (int64_t p = c->r0; p < c->r1; ++p)
     if (A[p * N + p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, A[p * N + p]);
 
@@ -928,7 +924,7 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
     c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);
     std::vector<int32_t> colptr;
     std::vector<uint32_t> ent;
-    build_csc(A.data(), N, c->nchunks, c->Qc, colptr, ent);
+    build_csc(A, N, c->nchunks, c->Qc, colptr, ent);
     c->nnz = colptr.back();
     if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
         (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
@@ -938,7 +934,7 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
     if ((e = cudaMemcpyAsync(c->colptr, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st)) !=
             cudaSuccess ||
         (e = cudaMemcpyAsync(c->ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dA, A.data(), (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+        (e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
       return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
     int64_t n = (alpha_max + 1) * c->slot_words;
     fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
@@ -956,14 +952,14 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
       (e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
       (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
     return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
-  if ((e = cudaMemcpyAsync(dA, A.data(), (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+  if ((e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
     return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
   // every ring slot starts all-INF (slots are compared before they are first written)
   {
     int64_t n = (alpha_max + 1) * c->slot_words;
     fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
   }
-  rc = pack_right(dA, N, N, N, c->BP, c->P, c->P / 2, c->st);
+  int rc = pack_right(dA, N, N, N, c->BP, c->P, c->P / 2, c->st);
   if (rc == RD_OK) rc = pack_left(dA, N, c->Mr, N, c->r0, c->slot(1), c->Mp, c->P / 2, c->st);
   if (rc == RD_OK && (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
     rc = fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e));
@@ -973,6 +969,43 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   c->k = 1;
   *out = c;
   return RD_OK;
+}
+
+extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
+                                  void *cuda_stream, rd_chain **out) {
+  clear_error();
+  if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
+  *out = nullptr;
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
+  const int64_t N = count_words(m);
+  std::vector<int16_t> A((size_t)(N * N));
+  int rc = build_matrix(m, A.data(), N);
+  if (rc != RD_OK) return rc;
+  return chain_create_impl(A.data(), N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
+}
+
+// Validates a caller's matrix: entries in [0, RD_INF] (> RD_INF is read as +inf);
+// returns the largest finite entry in *maxlab.
+static int check_matrix(const int16_t *A, int64_t N, int32_t *maxlab, const char *who) {
+  if (!A || N < 1) return fail(RD_EINVAL, "%s: NULL matrix or N < 1", who);
+  int32_t mx = 0;
+  for (int64_t e = 0; e < N * N; ++e) {
+    if (A[e] < 0) return fail(RD_EINVAL, "%s: negative entry at %lld (entries must be >= 0)", who, (long long)e);
+    if (A[e] < RD_INF) mx = std::max<int32_t>(mx, A[e]);
+  }
+  *maxlab = mx;
+  return RD_OK;
+}
+
+extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max, int64_t row_begin,
+                                      int64_t row_end, int method, void *cuda_stream, rd_chain **out) {
+  clear_error();
+  int32_t mx = 0;
+  if (int rc = check_matrix(A, N, &mx, "rd_chain_create_matrix")) return rc;
+  // entries above RD_INF are +inf: clamp a copy so every path sees RD_INF exactly
+  std::vector<int16_t> Ac(A, A + N * N);
+  for (auto &x : Ac) x = std::min<int16_t>(x, RD_INF);
+  return chain_create_impl(Ac.data(), N, 0, alpha_max, row_begin, row_end, method, cuda_stream, out);
 }
 
 static int g_sparse_variant = 3;   // rd_set_sparse_variant (default: measured best, 1024 threads)
@@ -1072,26 +1105,59 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
 }
 
 // ============================================================ power sequence ==
-extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
-                                     int32_t *diag) {
-  clear_error();
+// Argument checks shared by the power-sequence entries; maxlab = the largest label (entries
+// of A^k are <= k * maxlab, R5).
+static int power_sequence_check(int kmax, int alpha_max, int policy, int method, int32_t maxlab,
+                                rd_period_t *out, int32_t *diag) {
   if (!out) return fail(RD_EINVAL, "rd_power_sequence: out is NULL");
   *out = rd_period_t{0, 0, 0, 0, 0};
-  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
   if (kmax < 2) return fail(RD_EINVAL, "rd_power_sequence: kmax=%d < 2", kmax);
   if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_power_sequence: alpha_max out of range");
   if (policy != 0 && policy != 1) return fail(RD_EINVAL, "rd_power_sequence: policy must be 0 or 1");
-  if ((int64_t)2 * m * kmax >= RD_INF)
-    return fail(RD_ERANGE, "rd_power_sequence: 2*m*kmax = %d exceeds the int16 headroom", 2 * m * kmax);
+  if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_power_sequence: method must be 0 or 1");
+  if ((int64_t)maxlab * kmax >= RD_INF)
+    return fail(RD_ERANGE, "rd_power_sequence: max label %d x kmax %d exceeds the int16 headroom", maxlab, kmax);
   if (diag)
     for (int k = 0; k <= kmax; ++k) diag[k] = INT32_MAX;
+  return RD_OK;
+}
 
+static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
+                              rd_period_t *out, int32_t *diag);
+
+extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                                     int32_t *diag) {
+  clear_error();
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
+  if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, 2 * m, out, diag)) return rc0;
   const int64_t N = count_words(m);
   cudaStream_t st;
   RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   rd_chain *c = nullptr;
   int rc = rd_chain_create_ex(m, alpha_max, 0, N, method, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
+  return power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
+}
+
+extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, int alpha_max, int policy,
+                                        int method, rd_period_t *out, int32_t *diag) {
+  clear_error();
+  int32_t mx = 0;
+  if (int rc0 = check_matrix(A, N, &mx, "rd_power_sequence_matrix")) return rc0;
+  if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, mx, out, diag)) return rc0;
+  cudaStream_t st;
+  RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  rd_chain *c = nullptr;
+  int rc = rd_chain_create_matrix(A, N, alpha_max, 0, N, method, st, &c);
+  if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
+  return power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
+}
+
+// Algorithm 2's loop over a created chain (consumes c and st).
+static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
+                              rd_period_t *out, int32_t *diag) {
+  const int64_t N = c->N;
+  int rc = RD_OK;
 
   // Speculative depth: up to `depth` power steps are enqueued ahead of the host decision,
   // each with its own stats slot and async D2H copy, so launch and sync latency overlap the

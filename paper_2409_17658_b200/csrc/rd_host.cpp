@@ -78,18 +78,23 @@ struct SuccGen {
   const int *q;  // digits of q
   const int32_t *index_of_code;
   int16_t *row;  // A[q][*]
+  bool border;   // App. A rules on the last row and loss labels
   int p[16];
   void go(int i, uint32_t code, int na, int nb) {
     if (i == m) {
       // last row's pending vertical condition: p_{m-1} (row m-1, 0-based m-2) must be a
       if (needs_vertical(m - 1) && !(m >= 2 && p[m - 2] == 0)) return;
       int32_t idx = index_of_code[code];
-      row[idx] = (int16_t)(2 * na + nb);
+      row[idx] = (int16_t)(border ? 10 * na + 5 * nb - 2 * newly_dominated() : 2 * na + nb);
       return;
     }
     static const int cand[4][4] = {{0, 2, -1, -1}, {2, 3, -1, -1}, {0, 1, 2, 3}, {0, -1, -1, -1}};
+    // App. A, fourth (last) row: a zero there needs no domination, so after q_4 = d every
+    // letter may follow (c only with an `a` above it, as after q_4 = c)
+    static const int cand_d_border[4] = {0, 1, 2, 3};
+    const int *cs = (border && i == m - 1 && q[i] == 3) ? cand_d_border : cand[q[i]];
     for (int t = 0; t < 4; ++t) {
-      int x = cand[q[i]][t];
+      int x = cs[t];
       if (x < 0) break;
       if (i > 0 && !adjacent_ok(p[i - 1], x)) continue;  // p must be a correct word
       p[i] = x;
@@ -102,11 +107,27 @@ struct SuccGen {
       go(i + 1, code * 4 + x, na + (x == 0), nb + (x == 1));
     }
   }
-  // row r's p_r = c with q_r in {b, c} needs an `a` above or below in p
-  bool needs_vertical(int r) const { return p[r] == 2 && (q[r] == 1 || q[r] == 2); }
+  // row r's p_r = c after q_r in {b, c} (or q_r = d on the border's last row) needs an `a`
+  // above or below it in p
+  bool needs_vertical(int r) const {
+    return p[r] == 2 && (q[r] == 1 || q[r] == 2 || (border && r == m - 1 && q[r] == 3));
+  }
+  // Algorithm 3 as a table over (q_i, p_i), plus the row-5 cell under p_4 = a
+  int newly_dominated() const {
+    static const int nd_tab[4][4] = {  // [q_i][p_i], letters a b c d
+        {1, 0, 0, 0},   // q = a: (a,a) +1
+        {0, 0, 1, 0},   // q = b: (b,c) +1
+        {2, 1, 1, 0},   // q = c: (c,a) +2, (c,b) +1, (c,c) +1
+        {3, 1, 1, 0}};  // q = d: (d,a) +3, (d,b) +1, (d,c) +1
+    int nd = 0;
+    for (int i = 0; i < m; ++i) nd += nd_tab[q[i]][p[i]];
+    return nd + (p[m - 1] == 0 ? 1 : 0);
+  }
 };
 
-int build_matrix(int m, int16_t *A, int64_t N) {
+int build_matrix(int m, int16_t *A, int64_t N) { return build_matrix_variant(m, A, N, false); }
+
+int build_matrix_variant(int m, int16_t *A, int64_t N, bool border) {
   std::vector<uint32_t> codes = word_codes(m);
   if ((int64_t)codes.size() != N) return fail(RD_EINVAL, "word count mismatch");
   std::vector<int32_t> index_of_code((size_t)1 << (2 * m), -1);
@@ -117,7 +138,7 @@ int build_matrix(int m, int16_t *A, int64_t N) {
     std::fill(row, row + N, RD_INF);
     int qd[16];
     for (int i = 0; i < m; ++i) qd[i] = (codes[q] >> (2 * (m - 1 - i))) & 3;
-    SuccGen g{m, qd, index_of_code.data(), row, {}};
+    SuccGen g{m, qd, index_of_code.data(), row, border, {}};
     g.go(0, 0, 0, 0);
   }
   return RD_OK;
@@ -149,6 +170,15 @@ extern "C" int rd_build_matrix(int m, int16_t *A, int64_t *N_out) {
   *N_out = N;
   if (!A) return RD_OK;
   return build_matrix(m, A, N);
+}
+
+extern "C" int rd_build_matrix_border(int16_t *A, int64_t *N_out) {
+  clear_error();
+  if (!N_out) return fail(RD_EINVAL, "rd_build_matrix_border: N_out is NULL");
+  const int64_t N = count_words(4);
+  *N_out = N;
+  if (!A) return RD_OK;
+  return build_matrix_variant(4, A, N, true);
 }
 
 extern "C" int rd_stats_len(int alpha_max) { return 1 + 4 * alpha_max; }

@@ -19,6 +19,8 @@ int64_t count_words(int m);
 std::vector<uint32_t> word_codes(int m);
 // A(G) into A (N*N int16 row-major, RD_INF off the arcs).  OpenMP over rows.
 int build_matrix(int m, int16_t *A, int64_t N);
+// border = the App. A variant (m = 4): last-row rules of P:594-599, labels 10p(a)+5p(b)-2nd
+int build_matrix_variant(int m, int16_t *A, int64_t N, bool border);
 
 // Packed right operand / pair-major layouts, see DESIGN.md "Data layout".
 constexpr int kTile = 128;          // CTA tile (rows and columns of C)

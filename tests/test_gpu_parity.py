@@ -406,3 +406,44 @@ def test_m10_dense_equals_structured_first_powers():
     for _ in range(K - 1):
         R = O.minplus(R, A, skip=True)
     assert (outs[1] == to_inf(R, OINF, RINF, np.int16)).all()
+
+
+
+# ------------------------------------------------------ App. A border (NEXT-1)
+@pytest.mark.parametrize("method", [0, 1])
+def test_border_chain_matches_oracle(method, golden):
+    A = rd.rd_build_matrix_border()
+    ref = O.power_chain_matrix(O.border_matrix(), 50, 10, 0)
+    got = rd.rd_power_sequence_matrix(A, 50, 10, 0, method)
+    assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                      ref["k_stop"])
+    assert (got["n0"], got["alpha"], got["beta"]) == tuple(golden("border_appendix_a.json")["triple"])
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+    P = {k: to_inf(X, OINF, RINF, np.int16) for k, X in
+         ((k, X) for k, X in _border_powers(8))}
+    ch = rd.Chain(4, alpha_max=4, method=method, matrix=A)
+    for k in range(2, 9):
+        ch.step()
+        assert (ch.read_rows(k) == P[k]).all(), k
+    ch.close()
+
+
+def _border_powers(kmax):
+    A = O.border_matrix()
+    X = A.copy()
+    yield 1, X
+    for k in range(2, kmax + 1):
+        X = O.minplus(X, A)
+        yield k, X
+
+
+def test_power_sequence_matrix_random_generic():
+    # a generic sparse matrix through the same pipeline (dense and structured) vs the oracle
+    A16 = sparse_like(300, 6, seed=31)
+    A32 = to_inf(A16, RINF, OINF, np.int32)
+    ref = O.power_chain_matrix(A32, 40, 10, 0)
+    for method in (0, 1):
+        got = rd.rd_power_sequence_matrix(A16, 40, 10, 0, method)
+        assert (got["found"], got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (
+            ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"])
+        assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]

@@ -96,3 +96,21 @@ def test_argument_validation_host_paths():
     assert L.rd_roman_cylinder(0, 5, ctypes.byref(g)) == rd.RD_EINVAL
     assert L.rd_minplus_mul(None, None, None, 4) == rd.RD_EINVAL
     assert L.rd_stats_len(10) == 41
+
+
+def test_build_matrix_border_bit_exact():
+    A = rd.rd_build_matrix_border()
+    B = to_inf(O.border_matrix(), int(O.INF), rd.RD_INF, np.int16)
+    assert A.shape == (97, 97)
+    assert (A == B).all()
+
+
+def test_power_sequence_matrix_argument_checks():
+    L = rd.lib()
+    per = rd._Period()
+    A = np.full((5, 5), rd.RD_INF, dtype=np.int16)
+    A[0, 1] = -3
+    assert L.rd_power_sequence_matrix(rd._np_ptr(A), 5, 50, 10, 0, 0, ctypes.byref(per), None) == rd.RD_EINVAL
+    A[0, 1] = 400                                   # 400 * 50 >= RD_INF: headroom
+    assert L.rd_power_sequence_matrix(rd._np_ptr(A), 5, 50, 10, 0, 0, ctypes.byref(per), None) == rd.RD_ERANGE
+    assert L.rd_power_sequence_matrix(None, 5, 50, 10, 0, 0, ctypes.byref(per), None) == rd.RD_EINVAL
