@@ -799,6 +799,24 @@ __global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_
   RP[p * ldr + j] = lo | (hi << 16);
 }
 
+// A^1 rows [r0, r1) into an all-INF RP slot straight from the CSC (thread per column).
+__global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent, int64_t N,
+                                  int nchunks, int Qc, int64_t r0, int64_t r1, uint32_t *__restrict__ RP,
+                                  int64_t ldr) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  uint16_t *h = reinterpret_cast<uint16_t *>(RP);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr + (int64_t)ch * (N + 1);
+    for (int t = cp[j]; t < cp[j + 1]; ++t) {
+      const int64_t q = (int64_t)ch * Qc + (ent[t] & 0x1FFFFu);
+      if (q < r0 || q >= r1) continue;
+      const int64_t i = q - r0;
+      h[((i >> 1) * ldr + j) * 2 + (i & 1)] = (uint16_t)(ent[t] >> 17);
+    }
+  }
+}
+
 // RP -> row-major int16 rows x cols
 __global__ void unpack_rp_kernel(const uint32_t *__restrict__ RP, int64_t ldr, int64_t rows, int64_t cols,
                                  int16_t *__restrict__ X) {
@@ -873,8 +891,10 @@ struct rd_chain {
 };
 
 // Creates a chain over the host matrix A (N x N int16 row-major, entries in [0, RD_INF]).
+// Ahost == nullptr (method 1 only): the CSC comes straight from the successor generator of
+// words of length m (border = App. A rules), with no dense matrix on the host or device.
 static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_max, int64_t row_begin,
-                             int64_t row_end, int method, void *cuda_stream, rd_chain **out) {
+                             int64_t row_end, int method, void *cuda_stream, rd_chain **out, bool border = false) {
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
   if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_chain_create: method must be 0 (dense) or 1 (structured)");
@@ -905,8 +925,9 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     c->slot_words = (c->Mp / 2) * c->P;
   }
   const int16_t *A = Ahost;
-  for (int64_t p = c->r0; p < c->r1; ++p)
-    if (A[p * N + p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, A[p * N + p]);
+  if (A)
+    for (int64_t p = c->r0; p < c->r1; ++p)
+      if (A[p * N + p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, A[p * N + p]);
 
   int16_t *dA = nullptr;
   auto cleanup = [&](int code) {
@@ -924,22 +945,34 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);
     std::vector<int32_t> colptr;
     std::vector<uint32_t> ent;
-    build_csc(A, N, c->nchunks, c->Qc, colptr, ent);
+    if (A) {
+      build_csc(A, N, c->nchunks, c->Qc, colptr, ent);
+    } else {
+      std::vector<int16_t> dg;
+      build_csc_direct(m, border, c->nchunks, c->Qc, colptr, ent, dg);
+      for (int64_t p = c->r0; p < c->r1; ++p)
+        if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
+    }
     c->nnz = colptr.back();
     if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
         (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
+        (A && (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess) ||
         (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
       return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
     if ((e = cudaMemcpyAsync(c->colptr, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st)) !=
             cudaSuccess ||
         (e = cudaMemcpyAsync(c->ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+        (A && (e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess))
       return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
     int64_t n = (alpha_max + 1) * c->slot_words;
     fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
-    dim3 grid((unsigned)((c->P + 255) / 256), (unsigned)(c->Mp / 2));
-    pack_rp_kernel<<<grid, 256, 0, c->st>>>(dA, N, c->Mr, N, c->r0, c->slot(1), c->P, c->Mp / 2);
+    if (A) {
+      dim3 grid((unsigned)((c->P + 255) / 256), (unsigned)(c->Mp / 2));
+      pack_rp_kernel<<<grid, 256, 0, c->st>>>(dA, N, c->Mr, N, c->r0, c->slot(1), c->P, c->Mp / 2);
+    } else {
+      scatter_rp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(c->colptr, c->ent, N, c->nchunks, c->Qc,
+                                                                          c->r0, c->r1, c->slot(1), c->P);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
       return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
     cudaFree(dA);
@@ -978,6 +1011,8 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   *out = nullptr;
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
   const int64_t N = count_words(m);
+  if (method == 1)   // structured: CSC from the successor generator, no dense matrix
+    return chain_create_impl(nullptr, N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
   std::vector<int16_t> A((size_t)(N * N));
   int rc = build_matrix(m, A.data(), N);
   if (rc != RD_OK) return rc;

@@ -77,15 +77,18 @@ struct SuccGen {
   int m;
   const int *q;  // digits of q
   const int32_t *index_of_code;
-  int16_t *row;  // A[q][*]
+  int16_t *row;  // A[q][*] (nullable when `edges` collects the successors)
   bool border;   // App. A rules on the last row and loss labels
   int p[16];
+  std::vector<std::pair<int32_t, int16_t>> *edges = nullptr;  // (successor index, label)
   void go(int i, uint32_t code, int na, int nb) {
     if (i == m) {
       // last row's pending vertical condition: p_{m-1} (row m-1, 0-based m-2) must be a
       if (needs_vertical(m - 1) && !(m >= 2 && p[m - 2] == 0)) return;
       int32_t idx = index_of_code[code];
-      row[idx] = (int16_t)(border ? 10 * na + 5 * nb - 2 * newly_dominated() : 2 * na + nb);
+      const int16_t lab = (int16_t)(border ? 10 * na + 5 * nb - 2 * newly_dominated() : 2 * na + nb);
+      if (edges) edges->emplace_back(idx, lab);
+      else row[idx] = lab;
       return;
     }
     static const int cand[4][4] = {{0, 2, -1, -1}, {2, 3, -1, -1}, {0, 1, 2, 3}, {0, -1, -1, -1}};
@@ -140,6 +143,50 @@ int build_matrix_variant(int m, int16_t *A, int64_t N, bool border) {
     for (int i = 0; i < m; ++i) qd[i] = (codes[q] >> (2 * (m - 1 - i))) & 3;
     SuccGen g{m, qd, index_of_code.data(), row, border, {}};
     g.go(0, 0, 0, 0);
+  }
+  return RD_OK;
+}
+
+// The arcs of A(G) as a CSC per q-chunk, straight from the successor generator (no dense
+// matrix): colptr[ch*(N+1) + j] absolute offsets, entries (q - ch*Qc) | label << 17 with q
+// ascending in each column; diag[q] = A[q][q] (RD_INF if no self-loop).
+int build_csc_direct(int m, bool border, int nchunks, int Qc, std::vector<int32_t> &colptr,
+                     std::vector<uint32_t> &ent, std::vector<int16_t> &diag) {
+  std::vector<uint32_t> codes = word_codes(m);
+  const int64_t N = (int64_t)codes.size();
+  std::vector<int32_t> index_of_code((size_t)1 << (2 * m), -1);
+  for (int64_t w = 0; w < N; ++w) index_of_code[codes[w]] = (int32_t)w;
+  // successors of every q (parallel), kept per q so the fill below is in q order
+  std::vector<std::vector<std::pair<int32_t, int16_t>>> succ((size_t)N);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t q = 0; q < N; ++q) {
+    int qd[16];
+    for (int i = 0; i < m; ++i) qd[i] = (codes[q] >> (2 * (m - 1 - i))) & 3;
+    SuccGen g{m, qd, index_of_code.data(), nullptr, border, {}};
+    g.edges = &succ[q];
+    g.go(0, 0, 0, 0);
+  }
+  diag.assign((size_t)N, RD_INF);
+  colptr.assign((size_t)nchunks * (N + 1), 0);
+  for (int64_t q = 0; q < N; ++q) {
+    int32_t *cp = colptr.data() + (size_t)(q / Qc) * (N + 1);
+    for (auto &e : succ[q]) {
+      cp[e.first + 1]++;
+      if (e.first == q) diag[q] = e.second;
+    }
+  }
+  int64_t total = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    cp[0] = (int32_t)total;
+    for (int64_t j = 0; j < N; ++j) { total += cp[j + 1]; cp[j + 1] = (int32_t)total; }
+  }
+  ent.assign((size_t)std::max<int64_t>(total, 1), 0);
+  std::vector<int32_t> pos(colptr.begin(), colptr.end());
+  for (int64_t q = 0; q < N; ++q) {
+    const int ch = (int)(q / Qc);
+    int32_t *ps = pos.data() + (size_t)ch * (N + 1);
+    for (auto &e : succ[q]) ent[ps[e.first]++] = (uint32_t)(q - (int64_t)ch * Qc) | ((uint32_t)e.second << 17);
   }
   return RD_OK;
 }

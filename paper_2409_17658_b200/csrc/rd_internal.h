@@ -21,6 +21,9 @@ std::vector<uint32_t> word_codes(int m);
 int build_matrix(int m, int16_t *A, int64_t N);
 // border = the App. A variant (m = 4): last-row rules of P:594-599, labels 10p(a)+5p(b)-2nd
 int build_matrix_variant(int m, int16_t *A, int64_t N, bool border);
+// The same arcs as a CSC per q-chunk straight from the successor generator (see rd_host.cpp).
+int build_csc_direct(int m, bool border, int nchunks, int Qc, std::vector<int32_t> &colptr,
+                     std::vector<uint32_t> &ent, std::vector<int16_t> &diag);
 
 // Packed right operand / pair-major layouts, see DESIGN.md "Data layout".
 constexpr int kTile = 128;          // CTA tile (rows and columns of C)
