@@ -40,11 +40,11 @@ namespace {
 
 constexpr uint32_t kInf2 = 0x3FFF3FFFu;
 constexpr int kThreads = 256;
-constexpr int kBK2 = 16;      // k-pairs per pipeline stage (32 k)
-constexpr int kStages = 4;
+constexpr int kBK2 = 32;      // k-pairs per pipeline stage (64 k)
+constexpr int kStages = 3;
 constexpr int kGroup = 8;     // row-tiles per rasterisation group
 constexpr int kStageWords = 2 * kBK2 * kTile;   // u32 per stage (left + right tile)
-constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4;   // 64 KB
+constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4;   // 96 KB (2 CTAs/SM)
 
 // ------------------------------------------------------------------ packing --
 // Row-major int16 X (rows x cols, ld) -> PM u32 XT[cols_p/2][rows_p] (ld = rows_p).
@@ -190,10 +190,11 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     uint32_t *sx = smem + stage * kStageWords;
     uint32_t *sb = sx + kBK2 * kTile;
     const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
-    cp_async16(sx + ld_row * kTile + ld_col, gx + ox);
-    cp_async16(sx + (ld_row + 8) * kTile + ld_col, gx + ox + gx_step8);
-    cp_async16(sb + ld_row * kTile + ld_col, gb + ob);
-    cp_async16(sb + (ld_row + 8) * kTile + ld_col, gb + ob + gb_step8);
+#pragma unroll
+    for (int r = 0; r < kBK2; r += 8) {
+      cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
+      cp_async16(sb + (ld_row + r) * kTile + ld_col, gb + ob + (r / 8) * gb_step8);
+    }
   };
 
   uint32_t acc[8][8];
