@@ -169,6 +169,27 @@ int rd_build_matrix_border(int16_t *A, int64_t *N_out);
 int rd_roman_cylinder(int m, int64_t n, int64_t *gamma);
 
 /* ---------------------------------------------------------------------------
+ * Closed form (NEXT-4): the unique solution of gamma(n + alpha) - gamma(n) = beta for
+ * n >= n0 (Prop 8) with the boundary values diag[n0..n0+alpha-1]:
+ *   gamma(n) = (beta * n + C[n mod alpha]) / alpha           for every n >= n_valid,
+ *            = ceil(beta * n / alpha) + d[n mod alpha]          (the paper's form).
+ * n_valid <= n0 is the smallest n >= 3 from which the formula matches every computed
+ * diag[n] (it holds for all n >= n0 by Lemma 2); the values for 3 <= n < n_valid are the
+ * exceptions, returned in `small` (small[n - 3], n_valid - 3 entries, nullable, <= 64). */
+typedef struct {
+  int32_t n0, alpha, beta, n_valid;
+  int32_t C[32];
+  int32_t d[32];
+} rd_formula_t;
+
+/* From a computed chain: per = (found, n0, alpha, beta, k_stop), diag[k] for k <= k_stop.
+ * Host only.  Errors: RD_EINVAL (not found, alpha > 32, n0 + alpha - 1 > k_stop). */
+int rd_closed_form_from(const rd_period_t *per, const int32_t *diag, rd_formula_t *f, int32_t *small);
+
+/* For P_m [] C_n: runs (or reuses) the chain of rd_roman_cylinder, then rd_closed_form_from. */
+int rd_closed_form(int m, rd_formula_t *f, int32_t *small);
+
+/* ---------------------------------------------------------------------------
  * Power-chain context: one row panel [row_begin, row_end) of every power A^k on the
  * current device.  Rows of A^{k+1} depend only on the same rows of A^k and on A
  * (A^{k+1} = A^k (x) A, P:83 + Thm 1), so ranks that own disjoint panels never

@@ -27,6 +27,11 @@ class RDError(RuntimeError):
         self.status = status
 
 
+class _Formula(ctypes.Structure):
+    _fields_ = [("n0", ctypes.c_int32), ("alpha", ctypes.c_int32), ("beta", ctypes.c_int32),
+                ("n_valid", ctypes.c_int32), ("C", ctypes.c_int32 * 32), ("d", ctypes.c_int32 * 32)]
+
+
 class _Period(ctypes.Structure):
     _fields_ = [("found", ctypes.c_int32), ("n0", ctypes.c_int32), ("alpha", ctypes.c_int32),
                 ("beta", ctypes.c_int32), ("k_stop", ctypes.c_int32)]
@@ -61,6 +66,8 @@ def lib():
         L.rd_power_sequence_matrix.argtypes = [p, i64, ci, ci, ci, ci, p, p]
         L.rd_build_matrix_border.argtypes = [p, p]
         L.rd_chain_create_matrix.argtypes = [p, i64, ci, i64, i64, ci, p, p]
+        L.rd_closed_form_from.argtypes = [p, p, p, p]
+        L.rd_closed_form.argtypes = [ci, p, p]
         L.rd_chain_destroy.argtypes = [p]
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
@@ -77,7 +84,8 @@ def lib():
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
                   "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
                   "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant",
-                  "rd_power_sequence_matrix", "rd_build_matrix_border", "rd_chain_create_matrix"):
+                  "rd_power_sequence_matrix", "rd_build_matrix_border", "rd_chain_create_matrix",
+                  "rd_closed_form_from", "rd_closed_form"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -141,6 +149,38 @@ def rd_stats_decide(stats, alpha_max: int, k: int, only_alpha: int = 0):
     a, b = ctypes.c_int32(), ctypes.c_int32()
     ok = lib().rd_stats_decide(_np_ptr(s), alpha_max, k, only_alpha, ctypes.byref(a), ctypes.byref(b))
     return (a.value, b.value) if ok else None
+
+
+def _formula_dict(f, small):
+    a = f.alpha
+    out = dict(n0=f.n0, alpha=a, beta=f.beta, n_valid=f.n_valid, C=[f.C[r] for r in range(a)],
+               d=[f.d[r] for r in range(a)], small={n: int(small[n - 3]) for n in range(3, f.n_valid)})
+    terms = []
+    for r in range(a):
+        terms.append(f"ceil({f.beta}n/{a}){'+' if f.d[r] >= 0 else '-'}{abs(f.d[r])} if n = {r} mod {a}")
+    out["text"] = "; ".join(terms) + f"  (n >= {f.n_valid})" + (
+        "; " + ", ".join(f"gamma({n}) = {v}" for n, v in out["small"].items()) if out["small"] else "")
+    return out
+
+
+def rd_closed_form_from(res: dict):
+    """NEXT-4 on a chain result dict (found, n0, alpha, beta, k_stop, diag): per-residue
+    formula gamma(n) = (beta n + C_r)/alpha = ceil(beta n/alpha) + d_r for n >= n_valid."""
+    per = _Period(int(res["found"]), res["n0"], res["alpha"], res["beta"], res["k_stop"])
+    diag = np.ascontiguousarray(np.asarray(res["diag"], dtype=np.int64).clip(max=2**31 - 1).astype(np.int32))
+    f = _Formula()
+    small = (ctypes.c_int32 * 64)()
+    _check(lib().rd_closed_form_from(ctypes.byref(per), _np_ptr(diag), ctypes.byref(f), small))
+    return _formula_dict(f, small)
+
+
+def rd_closed_form(m: int):
+    """NEXT-4 for P_m [] C_n (computes or reuses the chain on the GPU)."""
+    _sync_device()
+    f = _Formula()
+    small = (ctypes.c_int32 * 64)()
+    _check(lib().rd_closed_form(m, ctypes.byref(f), small))
+    return _formula_dict(f, small)
 
 
 def rd_stats_len(alpha_max: int) -> int:

@@ -293,3 +293,45 @@ extern "C" int rd_roman_cylinder(int m, int64_t n, int64_t *gamma) {
   *gamma = (int64_t)c.diag[np] + b * ((n - np) / a);
   return RD_OK;
 }
+
+// Closed form from the recurrence (Prop 8 + the finite-difference solution).
+extern "C" int rd_closed_form_from(const rd_period_t *per, const int32_t *diag, rd_formula_t *f, int32_t *small) {
+  clear_error();
+  if (!per || !diag || !f) return fail(RD_EINVAL, "rd_closed_form_from: NULL argument");
+  if (!per->found) return fail(RD_EINVAL, "rd_closed_form_from: no recurrence");
+  const int64_t n0 = per->n0, a = per->alpha, b = per->beta;
+  if (a < 1 || a > 32 || n0 < 1 || n0 + a - 1 > per->k_stop)
+    return fail(RD_EINVAL, "rd_closed_form_from: need 1 <= alpha <= 32 and n0 + alpha - 1 <= k_stop");
+  *f = rd_formula_t{};
+  f->n0 = (int32_t)n0;
+  f->alpha = (int32_t)a;
+  f->beta = (int32_t)b;
+  for (int64_t n = n0; n < n0 + a; ++n) {
+    const int64_t r = n % a;
+    f->C[r] = (int32_t)(a * diag[n] - b * n);             // gamma(n) = (b n + C_r) / a
+    f->d[r] = (int32_t)(diag[n] - (b * n + a - 1) / a);   // gamma(n) = ceil(b n / a) + d_r
+  }
+  auto formula = [&](int64_t n) { return (b * n + f->C[n % a]) / a; };
+  int64_t nv = n0;
+  while (nv - 1 >= 3 && diag[nv - 1] != INT32_MAX && formula(nv - 1) == diag[nv - 1]) --nv;
+  f->n_valid = (int32_t)nv;
+  for (int64_t n = n0; n <= per->k_stop; ++n)
+    if (formula(n) != diag[n]) return fail(RD_EINVAL, "rd_closed_form_from: diag[%lld] disagrees", (long long)n);
+  if (small)
+    for (int64_t n = 3; n < nv && n - 3 < 64; ++n) small[n - 3] = diag[n];
+  return RD_OK;
+}
+
+extern "C" int rd_closed_form(int m, rd_formula_t *f, int32_t *small) {
+  clear_error();
+  if (!f) return fail(RD_EINVAL, "rd_closed_form: f is NULL");
+  int64_t g = 0;
+  int rc = rd_roman_cylinder(m, 3, &g);   // fills the cache
+  if (rc < 0) return rc;
+  Cached c;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    c = g_cache[m];
+  }
+  return rd_closed_form_from(&c.per, c.diag.data(), f, small);
+}

@@ -447,3 +447,8 @@ def test_power_sequence_matrix_random_generic():
         assert (got["found"], got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (
             ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"])
         assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+def test_closed_form_gpu_m9_formula():
+    f = rd.rd_closed_form(9)
+    assert (f["alpha"], f["beta"], f["d"], f["n_valid"]) == (5, 20, [0, 2, 2, 2, 2], 3)   # 4n / 4n+2

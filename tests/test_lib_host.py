@@ -114,3 +114,36 @@ def test_power_sequence_matrix_argument_checks():
     A[0, 1] = 400                                   # 400 * 50 >= RD_INF: headroom
     assert L.rd_power_sequence_matrix(rd._np_ptr(A), 5, 50, 10, 0, 0, ctypes.byref(per), None) == rd.RD_ERANGE
     assert L.rd_power_sequence_matrix(None, 5, 50, 10, 0, 0, ctypes.byref(per), None) == rd.RD_EINVAL
+
+
+# --------------------------------------------------------- NEXT-4 closed form
+def _paper_d(m):
+    # the paper's per-residue offsets over ceil(beta n / 5)
+    return {7: [0, 1, 1, 1, 1], 8: [0, 2, 1, 1, 1], 9: [0, 2, 2, 2, 2]}[m]
+
+
+def test_closed_form_from_oracle_chains():
+    r1 = rd.rd_closed_form_from(O.power_chain(1, 50, 10, 0))
+    assert (r1["alpha"], r1["beta"], r1["d"], r1["n_valid"]) == (3, 2, [0, 0, 0], 3)   # ceil(2n/3)
+    r7 = rd.rd_closed_form_from(O.power_chain(7, 50, 10, 0))
+    assert (r7["alpha"], r7["beta"], r7["d"]) == (5, 16, _paper_d(7))
+    assert r7["n_valid"] == 7 and r7["small"][6] == 20          # erratum R10: formula gives 21
+    for n in range(7, 200):
+        g = (r7["beta"] * n + r7["C"][n % 5]) // 5
+        assert g == -(-16 * n // 5) + (0 if n % 5 == 0 else 1)
+
+
+@pytest.mark.slow
+def test_closed_form_m8_oracle():
+    r8 = rd.rd_closed_form_from(O.power_chain(8, 50, 10, 0))
+    assert (r8["alpha"], r8["beta"], r8["d"]) == (5, 18, _paper_d(8))
+    assert r8["small"] == {3: 13, 4: 16, 5: 18, 6: 23}          # n = 3 erratum, n = 6 special case
+
+
+def test_closed_form_rejects_bad_input():
+    with pytest.raises(rd.RDError):
+        rd.rd_closed_form_from(dict(found=False, n0=0, alpha=0, beta=0, k_stop=5, diag=[0] * 6))
+    bad = O.power_chain(3, 50, 10, 0)
+    bad["diag"][bad["k_stop"]] += 1
+    with pytest.raises(rd.RDError):
+        rd.rd_closed_form_from(bad)
