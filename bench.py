@@ -187,7 +187,11 @@ def run_ours(args, rank, world, local_rank):
     r0, r1 = rdist.panel_bounds(N, world, rank)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        chain = rd.Chain(m, alpha_max=am, row_begin=r0, row_end=r1, stream=stream) if r1 > r0 else None
+        if world > 1 and args.form == "replicated":
+            # A(G) built and packed once on rank 0, broadcast over NVLink (not rebuilt per rank)
+            chain = rdist.broadcast_chain(m, am, r0, r1)
+        else:
+            chain = rd.Chain(m, alpha_max=am, row_begin=r0, row_end=r1, stream=stream) if r1 > r0 else None
         stats = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device=dev)
         neutral = torch.from_numpy(rdist.neutral_stats(am)).to(dev)
         hstats = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, pin_memory=True)
@@ -293,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         t0 = time.perf_counter()
         if world > 1:
-            res = rdist.power_sequence(m, 50, am)
+            res = rdist.power_sequence(m, 50, am, broadcast=True)
         else:
             res = rd.rd_power_sequence(m, 50, am)
         torch.cuda.synchronize()
@@ -315,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
         for mm in args.ttp_m:
             if world > 1:
                 dist.barrier()
-            res = rdist.power_sequence(mm, 50, am)
+            res = rdist.power_sequence(mm, 50, am, broadcast=world > 1)
             tt = torch.tensor([res["t_build"], res["t_chain"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)

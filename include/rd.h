@@ -213,6 +213,16 @@ int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end,
 int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max, int64_t row_begin, int64_t row_end,
                            int method, void *cuda_stream, rd_chain **out);
 
+/* Broadcast support for the row-panel driver.  rd_chain_packed_operand exposes a dense
+ * chain's packed right operand (DEVICE u32 [P/2][P], P = N rounded up to 128; *words =
+ * its length) so it can be broadcast (NCCL over NVLink) instead of rebuilt on every rank;
+ * rd_chain_create_packed makes a dense chain over such a buffer (copied; the caller keeps
+ * ownership), deriving its A^1 panel on the device.  diag1 = min_p A_pp over the panel
+ * (rd_chain_diag1 of the exporting chain, all-reduced).  Errors: RD_EINVAL, RD_ENOMEM. */
+int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_dev, int64_t *words);
+int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, int64_t row_end, const uint32_t *bp_dev,
+                           int32_t diag1, void *cuda_stream, rd_chain **out);
+
 /* (min,+) terms one rd_chain_step evaluates (the algorithmic count of its method):
  * rows * N * N for method 0, rows * nnz(A) for method 1. */
 double rd_chain_terms_per_step(const rd_chain *c);

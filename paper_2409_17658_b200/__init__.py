@@ -68,6 +68,8 @@ def lib():
         L.rd_chain_create_matrix.argtypes = [p, i64, ci, i64, i64, ci, p, p]
         L.rd_closed_form_from.argtypes = [p, p, p, p]
         L.rd_closed_form.argtypes = [ci, p, p]
+        L.rd_chain_packed_operand.argtypes = [p, p, p]
+        L.rd_chain_create_packed.argtypes = [ci, ci, i64, i64, p, ctypes.c_int32, p, p]
         L.rd_chain_destroy.argtypes = [p]
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
@@ -85,7 +87,7 @@ def lib():
                   "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
                   "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant",
                   "rd_power_sequence_matrix", "rd_build_matrix_border", "rd_chain_create_matrix",
-                  "rd_closed_form_from", "rd_closed_form"):
+                  "rd_closed_form_from", "rd_closed_form", "rd_chain_packed_operand", "rd_chain_create_packed"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -293,7 +295,8 @@ class Chain:
     (rd_chain_*).  step() enqueues A^{k+1} = A^k (x) A with the fused stats."""
 
     def __init__(self, m: int, alpha_max: int = 10, row_begin: int = 0, row_end: int | None = None,
-                 stream=None, method: int = 0, matrix: np.ndarray | None = None):
+                 stream=None, method: int = 0, matrix: np.ndarray | None = None, packed=None,
+                 diag1: int | None = None):
         import torch
         _sync_device()
         self.m, self.alpha_max = m, alpha_max
@@ -302,7 +305,12 @@ class Chain:
             row_end = count_words(m) if matrix is None else matrix.shape[0]
         self.row_begin, self.row_end = row_begin, row_end
         h = ctypes.c_void_p()
-        if matrix is None:
+        if packed is not None:
+            # dense chain over a packed operand (a torch int32/uint32 device tensor), e.g. broadcast
+            _check(lib().rd_chain_create_packed(m, alpha_max, row_begin, row_end, packed.data_ptr(),
+                                                2**31 - 1 if diag1 is None else diag1,
+                                                _stream_ptr(self.stream), ctypes.byref(h)))
+        elif matrix is None:
             _check(lib().rd_chain_create_ex(m, alpha_max, row_begin, row_end, method, _stream_ptr(self.stream),
                                             ctypes.byref(h)))
         else:
@@ -313,6 +321,13 @@ class Chain:
         self._h = h
         self.N = lib().rd_chain_order(h)
         self.stats = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device="cuda")
+
+    def packed_operand(self):
+        """The packed right operand as a torch int32 CUDA tensor VIEW (no copy, owned by the chain)."""
+        import torch
+        ptr, words = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().rd_chain_packed_operand(self._h, ctypes.byref(ptr), ctypes.byref(words)))
+        return _wrap_device(ptr.value, words.value, torch.int32)
 
     @property
     def terms_per_step(self) -> float:
@@ -348,6 +363,16 @@ class Chain:
             self.close()
         except Exception:
             pass
+
+
+def _wrap_device(ptr: int, n: int, dtype):
+    """A torch view of library-owned device memory (via __cuda_array_interface__)."""
+    import torch
+
+    class _Buf:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Buf(), device="cuda")
 
 
 def count_words(m: int) -> int:

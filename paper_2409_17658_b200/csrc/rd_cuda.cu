@@ -88,6 +88,32 @@ __global__ void pack_right_kernel(const int16_t *__restrict__ B, int64_t ld, int
   BP[t * ldp + j] = lo | (hi << 16);
 }
 
+// PM panel of rows [row0, row0+rows) of A from the packed right operand BP[t][j] =
+// A[2t][j] | A[2t+1][j] << 16 (ld = ldp): XT[t][i] = A[row0+i][2t] | A[row0+i][2t+1] << 16.
+__global__ void pm_from_bp_kernel(const uint32_t *__restrict__ BP, int64_t ldp, int64_t rows, int64_t row0,
+                                  uint32_t *__restrict__ XT, int64_t ldt, int64_t tpairs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+  if (i >= ldt || t >= tpairs) return;
+  uint32_t v = 0x3FFF3FFFu;
+  if (i < rows) {
+    const int64_t r = row0 + i;
+    const uint32_t *src = BP + (r >> 1) * ldp;
+    const int sh = (int)(r & 1) * 16;
+    const uint32_t lo = (src[2 * t] >> sh) & 0xFFFF, hi = (src[2 * t + 1] >> sh) & 0xFFFF;
+    v = lo | (hi << 16);
+  }
+  XT[t * ldt + i] = v;
+}
+
+// min over rows r in [r0, r1) of A[r][r] = half of BP[r/2][r] (INT_MAX if no finite one)
+__global__ void diag_from_bp_kernel(const uint32_t *__restrict__ BP, int64_t ldp, int64_t r0, int64_t r1,
+                                    int32_t *out) {
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const int v = (int)((BP[(r >> 1) * ldp + r] >> ((r & 1) * 16)) & 0xFFFF);
+  if (v < RD_INF) atomicMin(out, v);
+}
+
 // PM u32 XT[t][i] (ld = ldt) -> row-major int16 rows x cols (host-bound readback path).
 __global__ void unpack_pm_kernel(const uint32_t *__restrict__ XT, int64_t ldt, int64_t rows, int64_t cols,
                                  int16_t *__restrict__ X) {
@@ -1042,6 +1068,70 @@ extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max
   std::vector<int16_t> Ac(A, A + N * N);
   for (auto &x : Ac) x = std::min<int16_t>(x, RD_INF);
   return chain_create_impl(Ac.data(), N, 0, alpha_max, row_begin, row_end, method, cuda_stream, out);
+}
+
+// Dense chain (method 0) over the packed operand of A(G) that another chain exported
+// (e.g. broadcast over NVLink from rank 0): no host build, the A^1 panel comes from BP.
+extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, int64_t row_end,
+                                      const uint32_t *bp_dev, int32_t diag1, void *cuda_stream, rd_chain **out) {
+  clear_error();
+  if (!out || !bp_dev) return fail(RD_EINVAL, "rd_chain_create_packed: NULL argument");
+  *out = nullptr;
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create_packed: m=%d out of range", m);
+  if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_chain_create_packed: alpha_max out of 1..32");
+  const int64_t N = count_words(m);
+  if (row_begin < 0 || row_end > N || row_begin >= row_end)
+    return fail(RD_EINVAL, "rd_chain_create_packed: bad row range");
+  rd_chain *c = new rd_chain;
+  c->m = m; c->method = 0; c->alpha_max = alpha_max; c->N = N;
+  c->r0 = row_begin; c->r1 = row_end; c->Mr = row_end - row_begin;
+  c->st = (cudaStream_t)cuda_stream;
+  cudaGetDevice(&c->device);
+  c->P = round_up(N, kTile);
+  c->Mp = round_up(c->Mr, kTile);
+  c->slot_words = (c->P / 2) * c->Mp;
+  c->diag1 = diag1;
+  cudaError_t e;
+  const size_t bp_bytes = (size_t)(c->P / 2 * c->P * 4);
+  if ((e = cudaMalloc((void **)&c->BP, bp_bytes)) != cudaSuccess ||
+      (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess) {
+    rd_chain_destroy(c);
+    return fail(RD_ENOMEM, "rd_chain_create_packed: %s", cudaGetErrorString(e));
+  }
+  if ((e = cudaMemcpyAsync(c->BP, bp_dev, bp_bytes, cudaMemcpyDeviceToDevice, c->st)) != cudaSuccess) {
+    rd_chain_destroy(c);
+    return fail(RD_ECUDA, "rd_chain_create_packed: %s", cudaGetErrorString(e));
+  }
+  const int64_t n = (alpha_max + 1) * c->slot_words;
+  fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
+  dim3 grid((unsigned)((c->Mp + 255) / 256), (unsigned)(c->P / 2));
+  pm_from_bp_kernel<<<grid, 256, 0, c->st>>>(c->BP, c->P, c->Mr, c->r0, c->slot(1), c->Mp, c->P / 2);
+  if (diag1 == INT32_MAX) {   // not supplied: the panel's self-loop labels from the packed operand
+    int32_t *dd = nullptr;
+    if ((e = cudaMallocAsync((void **)&dd, 4, c->st)) == cudaSuccess) {
+      int32_t init = INT32_MAX;
+      cudaMemcpyAsync(dd, &init, 4, cudaMemcpyHostToDevice, c->st);
+      diag_from_bp_kernel<<<(unsigned)((c->Mr + 255) / 256), 256, 0, c->st>>>(c->BP, c->P, c->r0, c->r1, dd);
+      cudaMemcpyAsync(&c->diag1, dd, 4, cudaMemcpyDeviceToHost, c->st);
+      cudaFreeAsync(dd, c->st);
+    }
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess) {
+    rd_chain_destroy(c);
+    return fail(RD_ECUDA, "rd_chain_create_packed: %s", cudaGetErrorString(e));
+  }
+  c->k = 1;
+  *out = c;
+  return RD_OK;
+}
+
+extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_dev, int64_t *words) {
+  clear_error();
+  if (!c || !bp_dev || !words) return fail(RD_EINVAL, "rd_chain_packed_operand: NULL argument");
+  if (c->method != 0 || !c->BP) return fail(RD_EINVAL, "rd_chain_packed_operand: not a dense chain");
+  *bp_dev = c->BP;
+  *words = c->P / 2 * c->P;
+  return RD_OK;
 }
 
 static int g_sparse_variant = 3;   // rd_set_sparse_variant (default: measured best, 1024 threads)

@@ -60,8 +60,46 @@ class _EmptyPanel:
         pass
 
 
+def broadcast_chain(m: int, alpha_max: int, r0: int, r1: int, group=None, src: int = 0):
+    """Dense panel chain whose packed operand is built once on rank `src` and broadcast
+    (NCCL over NVLink; 969 MB at m = 9) instead of being rebuilt from the host on every
+    rank.  Every rank must call it (also ranks with empty panels, which get None)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import Chain, count_words
+    rank = dist.get_rank(group)
+    N = count_words(m)
+    P = (N + TILE - 1) // TILE * TILE
+    words = P // 2 * P
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if rank == src:
+        # src builds a full chain over its own panel (or a 1-row one if its panel is empty)
+        a, b = (r0, r1) if r1 > r0 else (0, 1)
+        own = Chain(m, alpha_max=alpha_max, row_begin=a, row_end=b)
+        buf = own.packed_operand()
+        d1 = own.diag1 if r1 > r0 else 2**31 - 1
+    else:
+        own = None
+        buf = torch.empty(words, dtype=torch.int32, device=dev)
+        d1 = 2**31 - 1
+    torch.cuda.synchronize()
+    dist.broadcast(buf, src=src, group=group)
+    if rank == src:
+        chain = own if r1 > r0 else None
+        if chain is None:
+            own.close()
+        return chain
+    if r1 <= r0:
+        return None
+    # this rank's diag1 from its rows of A: the packed operand holds them
+    chain = Chain(m, alpha_max=alpha_max, row_begin=r0, row_end=r1, packed=buf, diag1=None)
+    del buf
+    return chain
+
+
 def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0, group=None,
-                   chain_factory=None, diag1=None, method: int = 0):
+                   chain_factory=None, diag1=None, method: int = 0, broadcast: bool = False):
     """Algorithm 2 over all ranks of `group`; every rank returns the same
     dict(found, n0, alpha, beta, k_stop, diag) as rd_power_sequence.
 
@@ -87,7 +125,11 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
         def chain_factory(m_, am_, a_, b_):
             return Chain(m_, alpha_max=am_, row_begin=a_, row_end=b_, method=method)
     device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
-    chain = chain_factory(m, alpha_max, r0, r1) if r1 > r0 else _EmptyPanel(alpha_max, device)
+    if broadcast and world > 1 and method == 0:
+        chain = broadcast_chain(m, alpha_max, r0, r1, group)
+        chain = chain if chain is not None else _EmptyPanel(alpha_max, device)
+    else:
+        chain = chain_factory(m, alpha_max, r0, r1) if r1 > r0 else _EmptyPanel(alpha_max, device)
     if diag1 is None:
         d1 = getattr(chain, "diag1", 2**31 - 1)
         if world > 1:

@@ -452,3 +452,23 @@ def test_power_sequence_matrix_random_generic():
 def test_closed_form_gpu_m9_formula():
     f = rd.rd_closed_form(9)
     assert (f["alpha"], f["beta"], f["d"], f["n_valid"]) == (5, 20, [0, 2, 2, 2, 2], 3)   # 4n / 4n+2
+
+
+def test_chain_from_packed_operand_equals_built_chain():
+    # the broadcast path of the row-panel driver, emulated in one process: rank 0's packed
+    # operand feeds a chain for another panel, which must equal a chain built from the host
+    m, K = 6, 8
+    src = rd.Chain(m, alpha_max=4, row_begin=0, row_end=128)
+    buf = src.packed_operand().clone()
+    N = src.N
+    for a, b in ((128, 700), (700, N)):
+        ref = rd.Chain(m, alpha_max=4, row_begin=a, row_end=b)
+        got = rd.Chain(m, alpha_max=4, row_begin=a, row_end=b, packed=buf)
+        assert got.diag1 == ref.diag1
+        for k in range(2, K + 1):
+            s1, s2 = ref.step().cpu().numpy(), got.step().cpu().numpy()
+            assert (s1 == s2).all(), k
+        assert (ref.read_rows(K) == got.read_rows(K)).all()
+        ref.close()
+        got.close()
+    src.close()
