@@ -88,6 +88,7 @@ def broadcast_chain(m: int, alpha_max: int, r0: int, r1: int, group=None, src: i
     if rank == src:
         chain = own if r1 > r0 else None
         if chain is None:
+            torch.cuda.synchronize()       # the broadcast has read the buffer
             own.close()
         return chain
     if r1 <= r0:
