@@ -683,16 +683,22 @@ namespace {
 // stats are fused (lane a owns alpha a+1), as in the dense epilogue.
 struct SpArgs {
   const int32_t *colptr;  // nchunks x (N + 1) absolute offsets into ent
-  const uint32_t *ent;    // (q - chunk start) | w << 17
+  const uint32_t *ent;    // general: (q - chunk start) | w << 17;  uniform: (q - chunk start) * 8
   int nchunks, Qc;
   int64_t N;              // columns
+  const int16_t *wcol;    // uniform format: the label of column j (RD_INF if the column is empty)
 };
 
 constexpr int kSpThreadsMax = 1024;    // 1 CTA per SM (shared memory); 16 or 32 warps
 constexpr int kSpMaxAlpha = 16;        // lanes own alphas l+1 and l+9 of their 8-lane group
 constexpr int kSpGroup = 8;            // lanes per output column
 
-template <bool STATS, int kSpThreads, int UNROLL>
+// UNIFORM: every finite entry of column j carries the same label w_j (A(G): l(q,p) depends
+// on p only), so the CSC holds bare shared-memory byte offsets, each column's list is
+// padded to a multiple of 16 with the offset of an all-INF slot xs[Qc], two entries fold
+// into one VIMNMX3 per row pair, and w_j is added once per column (min_q x_q + w = min_q
+// (x_q + w)).  Otherwise (general labels, e.g. App. A) each entry carries its label.
+template <bool STATS, int kSpThreads, int UNROLL, bool UNIFORM>
 __global__ void __launch_bounds__(kSpThreads, 1)
 minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uint32_t *__restrict__ C,
                       EpiArgs epi) {
@@ -715,6 +721,7 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
     const int qn = (int)min((int64_t)sa.Qc, N - q0);
     __syncthreads();
     for (int q = threadIdx.x; q < qn; q += kSpThreads) xs[q] = make_uint2(x0[q0 + q], x1[q0 + q]);
+    if (UNIFORM && threadIdx.x == 0) xs[sa.Qc] = make_uint2(kInf2, kInf2);   // padding target
     __syncthreads();
     const int32_t *cp = sa.colptr + (int64_t)ch * (N + 1);
     const bool last = ch == sa.nchunks - 1;
@@ -732,7 +739,19 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
       int s = 0, e = 0;
       if (valid) { s = __ldg(cp + j); e = __ldg(cp + j + 1); }
       uint32_t a0 = kInf2, a1 = kInf2;
-      if (valid) {
+      if (valid && UNIFORM) {
+        const uint32_t *ep = sa.ent + s + sl;
+        const int cnt = e - s;                       // a multiple of 16
+        const char *xb = reinterpret_cast<const char *>(xs);
+#pragma unroll 2
+        for (int t = 0; t < cnt; t += 2 * kSpGroup) {
+          const uint32_t o0 = __ldg(ep + t), o1 = __ldg(ep + t + kSpGroup);
+          const uint2 v0 = *reinterpret_cast<const uint2 *>(xb + o0);
+          const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + o1);
+          a0 = __vimin3_s16x2(a0, v0.x, v1.x);
+          a1 = __vimin3_s16x2(a1, v0.y, v1.y);
+        }
+      } else if (valid) {
         constexpr uint32_t kSent = (uint32_t)RD_INF << 17;   // q = 0, w = RD_INF: never wins
         for (int t = s + sl; t < e; t += UNROLL * kSpGroup) {
           uint32_t en[UNROLL];
@@ -758,6 +777,12 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
       if (ch > 0) {
         a0 = __vmins2(a0, c0[j]);
         a1 = __vmins2(a1, c1[j]);
+      }
+      if (UNIFORM && last) {   // + w_j, saturating at RD_INF: min(a + w, INF)
+        const uint32_t w = (uint16_t)__ldg(sa.wcol + j);
+        const uint32_t w2 = w | (w << 16);
+        a0 = __viaddmin_s16x2(a0, w2, kInf2);
+        a1 = __viaddmin_s16x2(a1, w2, kInf2);
       }
       if (sl == 0) c0[j] = a0;
       if (sl == 1) c1[j] = a1;
@@ -829,17 +854,27 @@ __global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_
 // A^1 rows [r0, r1) into an all-INF RP slot straight from the CSC (thread per column).
 __global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent, int64_t N,
                                   int nchunks, int Qc, int64_t r0, int64_t r1, uint32_t *__restrict__ RP,
-                                  int64_t ldr) {
+                                  int64_t ldr, const int16_t *__restrict__ wcol) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   uint16_t *h = reinterpret_cast<uint16_t *>(RP);
   for (int ch = 0; ch < nchunks; ++ch) {
     const int32_t *cp = colptr + (int64_t)ch * (N + 1);
     for (int t = cp[j]; t < cp[j + 1]; ++t) {
-      const int64_t q = (int64_t)ch * Qc + (ent[t] & 0x1FFFFu);
+      int64_t ql;
+      uint16_t w;
+      if (wcol) {                                   // uniform: byte offsets, padding = Qc * 8
+        ql = ent[t] >> 3;
+        if (ql >= Qc) continue;
+        w = (uint16_t)wcol[j];
+      } else {
+        ql = ent[t] & 0x1FFFFu;
+        w = (uint16_t)(ent[t] >> 17);
+      }
+      const int64_t q = (int64_t)ch * Qc + ql;
       if (q < r0 || q >= r1) continue;
       const int64_t i = q - r0;
-      h[((i >> 1) * ldr + j) * 2 + (i & 1)] = (uint16_t)(ent[t] >> 17);
+      h[((i >> 1) * ldr + j) * 2 + (i & 1)] = w;
     }
   }
 }
@@ -898,6 +933,47 @@ void build_csc(const int16_t *A, int64_t N, int nchunks, int Qc, std::vector<int
     }
   }
 }
+// Re-encodes a general CSC (entries (q - q0) | w << 17) in the uniform-label format if every
+// column's entries share one label: entries (q - q0) * 8 (shared-memory byte offsets), each
+// column's list per chunk padded to a multiple of 16 with Qc * 8, wcol[j] = the label
+// (RD_INF for an empty column).  Returns false (inputs untouched) if some column mixes labels.
+bool csc_to_uniform(int64_t N, int nchunks, int Qc, std::vector<int32_t> &colptr, std::vector<uint32_t> &ent,
+                    std::vector<int16_t> &wcol) {
+  std::vector<int32_t> w((size_t)N, -1);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    for (int64_t j = 0; j < N; ++j)
+      for (int32_t t = cp[j]; t < cp[j + 1]; ++t) {
+        const int32_t lab = (int32_t)(ent[t] >> 17);
+        if (w[j] < 0) w[j] = lab;
+        else if (w[j] != lab) return false;
+      }
+  }
+  std::vector<int32_t> ucp((size_t)nchunks * (N + 1), 0);
+  int64_t total = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    int32_t *up = ucp.data() + (size_t)ch * (N + 1);
+    up[0] = (int32_t)total;
+    for (int64_t j = 0; j < N; ++j) {
+      total += (cp[j + 1] - cp[j] + 15) / 16 * 16;
+      up[j + 1] = (int32_t)total;
+    }
+  }
+  std::vector<uint32_t> uent((size_t)std::max<int64_t>(total, 1), (uint32_t)Qc * 8u);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    const int32_t *up = ucp.data() + (size_t)ch * (N + 1);
+    for (int64_t j = 0; j < N; ++j)
+      for (int32_t t = cp[j]; t < cp[j + 1]; ++t) uent[up[j] + (t - cp[j])] = (ent[t] & 0x1FFFFu) * 8u;
+  }
+  wcol.assign((size_t)N, RD_INF);
+  for (int64_t j = 0; j < N; ++j)
+    if (w[j] >= 0) wcol[j] = (int16_t)w[j];
+  colptr.swap(ucp);
+  ent.swap(uent);
+  return true;
+}
 }  // namespace
 
 // ================================================================ power chain ==
@@ -912,6 +988,7 @@ struct rd_chain {
   // method 1 (structured step): CSC of A per q-chunk
   int32_t *colptr = nullptr;
   uint32_t *ent = nullptr;
+  int16_t *wcol = nullptr;   // uniform-label format (see minplus_sparse_kernel)
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
@@ -963,13 +1040,14 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     if (c->ring) cudaFree(c->ring);
     if (c->colptr) cudaFree(c->colptr);
     if (c->ent) cudaFree(c->ent);
+    if (c->wcol) cudaFree(c->wcol);
     delete c;
     return code;
   };
   cudaError_t e;
   if (method == 1) {
-    c->nchunks = (int)((N * 8 + kSpSmemMax - 1) / kSpSmemMax);
-    c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);
+    c->nchunks = (int)(((N + 1) * 8 + kSpSmemMax - 1) / kSpSmemMax);
+    c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);   // (Qc + 1) * 8 B of shared memory
     std::vector<int32_t> colptr;
     std::vector<uint32_t> ent;
     if (A) {
@@ -981,6 +1059,12 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
         if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
     }
     c->nnz = colptr.back();
+    std::vector<int16_t> wcol;
+    if (csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol)) {
+      if ((e = cudaMalloc((void **)&c->wcol, wcol.size() * 2)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(c->wcol, wcol.data(), wcol.size() * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+        return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
+    }
     if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
         (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
         (A && (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess) ||
@@ -998,7 +1082,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
       pack_rp_kernel<<<grid, 256, 0, c->st>>>(dA, N, c->Mr, N, c->r0, c->slot(1), c->P, c->Mp / 2);
     } else {
       scatter_rp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(c->colptr, c->ent, N, c->nchunks, c->Qc,
-                                                                          c->r0, c->r1, c->slot(1), c->P);
+                                                                          c->r0, c->r1, c->slot(1), c->P, c->wcol);
     }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
       return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
@@ -1136,18 +1220,25 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 
 static int g_sparse_variant = 3;   // rd_set_sparse_variant (default: measured best, 1024 threads)
 
-template <int THREADS, int UNROLL>
-static int launch_sparse(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
+template <int THREADS, int UNROLL, bool UNIFORM>
+static int launch_sparse_u(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
   static bool attr_set[64] = {};
   if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true, THREADS, UNROLL>,
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true, THREADS, UNROLL, UNIFORM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemMax));
     attr_set[c->device] = true;
   }
-  minplus_sparse_kernel<true, THREADS, UNROLL><<<(unsigned)(c->Mp / 4), THREADS, (size_t)c->Qc * 8, c->st>>>(
-      c->slot(c->k), c->P, sa, c->slot(knew), epi);
+  minplus_sparse_kernel<true, THREADS, UNROLL, UNIFORM>
+      <<<(unsigned)(c->Mp / 4), THREADS, (size_t)(c->Qc + 1) * 8, c->st>>>(c->slot(c->k), c->P, sa, c->slot(knew),
+                                                                        epi);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
+}
+
+template <int THREADS, int UNROLL>
+static int launch_sparse(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
+  return sa.wcol ? launch_sparse_u<THREADS, UNROLL, true>(c, sa, knew, epi)
+                 : launch_sparse_u<THREADS, UNROLL, false>(c, sa, knew, epi);
 }
 
 extern "C" int rd_set_sparse_variant(int v) {
@@ -1168,6 +1259,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
   if (c->ring) cudaFree(c->ring);
   if (c->colptr) cudaFree(c->colptr);
   if (c->ent) cudaFree(c->ent);
+  if (c->wcol) cudaFree(c->wcol);
   delete c;
   return RD_OK;
 }
@@ -1192,7 +1284,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
   if (c->method == 1) {
-    SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N};
+    SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N, c->wcol};
     int rc1 = RD_OK;
     switch (g_sparse_variant) {
       case 1: rc1 = launch_sparse<512, 2>(c, sa, knew, epi); break;
