@@ -7,7 +7,7 @@ periodicity stats (a2-a4), the stats all_reduce(MIN) across ranks, the device->h
 of the stats and the host decision (a5).  The right operand A is packed once before the
 timed region (a1).  One process per GPU; ranks own 128-row panels of the output.
 
-    python bench.py [--gpus N --steps K --warmup W] [--m 9] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--order-m 9] [--form replicated|allgather] [--impl reference]
 
 Prints ONE JSON line on rank 0 (contract in DESIGN.md §Measurement).
 """
@@ -39,7 +39,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--m", type=int, default=9)
+    p.add_argument("--order-m", dest="m", type=int, default=9,
+                   help="m of P_m (named to stay unambiguous next to torchrun's own options)")
     p.add_argument("--alpha-max", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
@@ -172,7 +173,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank, world, local_rank):
+def run_ours(args, rank, world, local_rank, backend="nccl"):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -362,6 +363,7 @@ def run_ours(args, rank, world, local_rank):
             "data": "deterministic A(G) of P_m (no dataset); powers computed in the timed steps",
             "config": {"workload": f"P_{m} box C_n: power step A^k = A^(k-1) (x) A(G), N = C_{m} = {N}",
                        "m": m, "N": N, "alpha_max": am, "parallelism": f"row panels x{world}", "form": args.form,
+                       "backend": backend if world > 1 else None,
                        "l2": "operands (2N^2 B = %.0f MB each) exceed L2; no flush" % (2 * N * N / 1e6),
                        "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
@@ -389,6 +391,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: several ranks on one GPU with host-side (gloo) collectives; never used for
+    # a reported number (the line then says so in config.backend)
+    if "RD_FORCE_DEVICE" in os.environ:
+        local_rank = int(os.environ["RD_FORCE_DEVICE"])
+    backend = os.environ.get("RD_DIST_BACKEND", "nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -396,9 +403,12 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, rank, world, local_rank, backend)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -202,17 +202,30 @@ def minplus_mul_allgather(A_rows, B_panel, k_bounds, group=None, acc=None):
     cur = torch.empty((kmax_rows, N), dtype=B_panel.dtype, device=B_panel.device)
     cur[:B_panel.shape[0]].copy_(B_panel)
     nxt = torch.empty_like(cur)
+    # gloo cannot send from device memory: stage the ring through host buffers then (tests
+    # run several ranks on one GPU that way); NCCL moves device buffers over NVLink directly
+    staged = world > 1 and cur.is_cuda and dist.get_backend(group) == "gloo"
+    if staged:
+        h_cur = torch.empty(cur.shape, dtype=cur.dtype, pin_memory=True)
+        h_nxt = torch.empty_like(h_cur)
     for t in range(world):
         src = (rank - t) % world
         reqs = []
         if t < world - 1:
-            ops = [dist.P2POp(dist.isend, cur, (rank + 1) % world, group),
-                   dist.P2POp(dist.irecv, nxt, (rank - 1) % world, group)]
+            if staged:
+                h_cur.copy_(cur)
+                s_buf, r_buf = h_cur, h_nxt
+            else:
+                s_buf, r_buf = cur, nxt
+            ops = [dist.P2POp(dist.isend, s_buf, (rank + 1) % world, group),
+                   dist.P2POp(dist.irecv, r_buf, (rank - 1) % world, group)]
             reqs = dist.batch_isend_irecv(ops)
         k0, k1 = k_bounds[src]
         acc(A_rows, k0, k1, cur[:k1 - k0], C)
         for q in reqs:
             q.wait()
+        if staged and t < world - 1:
+            nxt.copy_(h_nxt)
         cur, nxt = nxt, cur
     return C
 

@@ -1,0 +1,91 @@
+"""The multi-rank drivers on one GPU: 2 processes on cuda:0 with gloo (host-side) collectives.
+
+No kernel waits on another rank (the ranks only meet in the host collectives), so this runs
+the real row-panel, broadcast and all-gather drivers end to end on the single GPU the test
+box has; results must equal the oracle.  (NCCL needs distinct devices; bench.py uses NCCL.)"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch, torch.distributed as dist
+import paper_2409_17658_b200 as rd
+from paper_2409_17658_b200 import dist as D
+torch.cuda.set_device(0)
+dist.init_process_group("gloo")
+out = {}
+for m in (5, 6):
+    r = D.power_sequence(m, 50, 10)
+    out["rep%d" % m] = [r["n0"], r["alpha"], r["beta"], r["k_stop"], r["diag"][1:r["k_stop"] + 1]]
+    r = D.power_sequence(m, 50, 10, broadcast=True)
+    out["bc%d" % m] = [r["n0"], r["alpha"], r["beta"], r["k_stop"], r["diag"][1:r["k_stop"] + 1]]
+    r = D.power_sequence(m, 50, 10, method=1)
+    out["st%d" % m] = [r["n0"], r["alpha"], r["beta"], r["k_stop"], r["diag"][1:r["k_stop"] + 1]]
+r = D.power_sequence_allgather(5, 50, 10)
+out["ag5"] = [r["n0"], r["alpha"], r["beta"], r["k_stop"], r["diag"][1:r["k_stop"] + 1]]
+torch.cuda.synchronize()
+if dist.get_rank() == 0:
+    print("RESULT " + json.dumps(out), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_two_ranks_one_gpu_gloo_drivers(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(WORKER)
+    env = dict(os.environ, ROOT=ROOT, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), WORLD_SIZE="2")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    line = [l for l in outs[0].splitlines() if l.startswith("RESULT ")][0]
+    res = json.loads(line[7:])
+    for m in (5, 6):
+        ref = O.power_chain(m, 50, 10, 0)
+        want = [ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"], ref["diag"][1:ref["k_stop"] + 1]]
+        assert res["rep%d" % m] == want
+        assert res["bc%d" % m] == want
+        assert res["st%d" % m] == want
+    ref = O.power_chain(5, 50, 10, 0)
+    assert res["ag5"] == [ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"], ref["diag"][1:ref["k_stop"] + 1]]
+
+
+def test_bench_two_ranks_one_gpu_gloo():
+    # bench.py under torchrun with 2 ranks (gloo, one GPU): the line is well formed and the
+    # detected triple is right; not a performance number
+    env = dict(os.environ, RD_DIST_BACKEND="gloo", RD_FORCE_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--order-m", "7", "--steps", "3", "--warmup", "22", "--no-cpu-baseline", "--ttp-m", "5"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["backend"] == "gloo"
+    assert d["config"]["detected"] == [21, 5, 16]
+    assert d["e2e"]["triple"] == [21, 5, 16]
+    assert d["time_to_periodicity"]["5"]["triple"] == [16, 5, 12]
