@@ -141,14 +141,19 @@ __global__ void stats_init_kernel(int32_t *s, int alpha_max) {
 __device__ __forceinline__ void stats_pair(uint32_t o, uint32_t w, uint32_t &lo2, uint32_t &hi2, uint32_t &mis,
                                            uint32_t &fin) {
   const uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
+  const uint32_t d = __vsub2(o, w);
+  if (!(eo | ew)) {            // both lanes finite in both powers (every entry from k = 4 on)
+    fin = 0xFFFFFFFFu;
+    lo2 = __vmins2(lo2, d);
+    hi2 = __vmaxs2(hi2, d);
+    return;
+  }
   mis |= eo ^ ew;
   const uint32_t fm = ~(eo | ew);
   fin |= fm;
-  const uint32_t d = __vsub2(o, w);
   lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
   hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
 }
-
 // --------------------------------------------------------------------- GEMM --
 struct EpiArgs {
   const uint32_t *prev[kMaxAlpha];  // PM slots of A^{k+1-a}, a = 1..nprev, same ld as C
@@ -379,16 +384,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
         uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
         const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t o = out[g * 4 + q][p], w = pw[q];
-          uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
-          mis |= eo ^ ew;
-          uint32_t fm = ~(eo | ew);
-          fin |= fm;
-          uint32_t d = __vsub2(o, w);
-          lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
-          hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
-        }
+        for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
       }
     int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
     int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
@@ -851,6 +847,23 @@ __global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_
   RP[p * ldr + j] = lo | (hi << 16);
 }
 
+// Dense-chain operands straight from a (single-chunk, general-format) CSC of A, thread per
+// column, into all-INF buffers: the packed right operand BP[t][j] = A[2t][j] | A[2t+1][j] << 16
+// and the PM panel XT[t][i] = A[r0+i][2t] | A[r0+i][2t+1] << 16 of rows [r0, r1).
+__global__ void scatter_dense_operands_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent,
+                                              int64_t N, uint32_t *__restrict__ BP, int64_t ldp,
+                                              uint32_t *__restrict__ XT, int64_t ldt, int64_t r0, int64_t r1) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  uint16_t *hb = reinterpret_cast<uint16_t *>(BP), *hx = reinterpret_cast<uint16_t *>(XT);
+  for (int t = colptr[j]; t < colptr[j + 1]; ++t) {
+    const int64_t q = ent[t] & 0x1FFFFu;
+    const uint16_t w = (uint16_t)(ent[t] >> 17);
+    hb[((q >> 1) * ldp + j) * 2 + (q & 1)] = w;
+    if (q >= r0 && q < r1) hx[((j >> 1) * ldt + (q - r0)) * 2 + (j & 1)] = w;
+  }
+}
+
 // A^1 rows [r0, r1) into an all-INF RP slot straight from the CSC (thread per column).
 __global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent, int64_t N,
                                   int nchunks, int Qc, int64_t r0, int64_t r1, uint32_t *__restrict__ RP,
@@ -1094,6 +1107,41 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     *out = c;
     return RD_OK;
   }
+  if (!A) {
+    // dense chain without a dense host matrix: CSC from the successor generator, scattered
+    // into the INF-filled packed operand and A^1 panel on the device (10 MB H2D at m = 9
+    // instead of 960 MB, and no N^2 host fill)
+    std::vector<int32_t> colptr;
+    std::vector<uint32_t> ent;
+    std::vector<int16_t> dg;
+    build_csc_direct(m, border, 1, (int)N, colptr, ent, dg);
+    for (int64_t p = c->r0; p < c->r1; ++p)
+      if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
+    int32_t *dcp = nullptr;
+    uint32_t *dent = nullptr;
+    if ((e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess ||
+        (e = cudaMalloc((void **)&dcp, colptr.size() * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&dent, ent.size() * 4)) != cudaSuccess) {
+      if (dcp) cudaFree(dcp);
+      return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
+    }
+    cudaMemcpyAsync(dcp, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st);
+    cudaMemcpyAsync(dent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st);
+    const int64_t nbp = c->P / 2 * c->P, nring = (alpha_max + 1) * c->slot_words;
+    fill_u32_kernel<<<(unsigned)((nbp + 255) / 256), 256, 0, c->st>>>(c->BP, nbp, kInf2);
+    fill_u32_kernel<<<(unsigned)((nring + 255) / 256), 256, 0, c->st>>>(c->ring, nring, kInf2);
+    scatter_dense_operands_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(dcp, dent, N, c->BP, c->P,
+                                                                                  c->slot(1), c->Mp, c->r0, c->r1);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+    cudaFree(dcp);
+    cudaFree(dent);
+    if (e != cudaSuccess) return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
+    c->k = 1;
+    *out = c;
+    return RD_OK;
+  }
   if ((e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
       (e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
       (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
@@ -1124,7 +1172,9 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   *out = nullptr;
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
   const int64_t N = count_words(m);
-  if (method == 1)   // structured: CSC from the successor generator, no dense matrix
+  // both methods: CSC from the successor generator, operands built on the device (the CSC
+  // entry holds q in 17 bits: m = 11 dense chains take the dense host matrix instead)
+  if (method == 1 || N < (1 << 17))
     return chain_create_impl(nullptr, N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
   std::vector<int16_t> A((size_t)(N * N));
   int rc = build_matrix(m, A.data(), N);

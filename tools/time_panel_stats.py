@@ -1,0 +1,25 @@
+"""Times rd_panel_stats on m=9-sized panels (21909 x 21909 int16 against 10 earlier powers)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2409_17658_b200 as rd  # noqa: E402
+
+N = 21909
+g = torch.Generator(device="cuda").manual_seed(0)
+cur = torch.randint(100, 140, (N, N), dtype=torch.int16, device="cuda", generator=g)
+prevs = [torch.randint(60 + 4 * a, 100, (N, N), dtype=torch.int16, device="cuda", generator=g) for a in range(10)]
+s = torch.empty(rd.rd_stats_len(10), dtype=torch.int32, device="cuda")
+for _ in range(3):
+    rd.rd_panel_stats(cur, prevs, 0, 10, s)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    rd.rd_panel_stats(cur, prevs, 0, 10, s)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+by = 11 * 2 * N * N
+print(f"panel_stats N={N} alpha=10: {ms:.3f} ms per call (2 passes), {by / ms / 1e6:.1f} GB/s algorithmic")
