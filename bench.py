@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8, 9])
+    p.add_argument("--oracle-ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
+    p.add_argument("--gops-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--form", default="replicated", choices=["replicated", "allgather"],
                    help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
                         "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step")
@@ -313,6 +315,27 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                "seconds": round(te, 3), "k_stop": res["k_stop"],
                "triple": [res["n0"], res["alpha"], res["beta"]]}
 
+    # dense power-step Gop/s at every order N = C_m (SURVEY §8(d) shapes), one rank, CUDA events
+    gops_by_m = {}
+    if rank == 0 and not args.no_e2e:
+        for mm in args.gops_m:
+            chm = rd.Chain(mm, alpha_max=am, stream=stream)
+            nn = chm.N
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    chm.step()
+                reps = 20 if mm <= 8 else 3
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record(stream)
+                for _ in range(reps):
+                    chm.step()
+                eb.record(stream)
+            torch.cuda.synchronize()
+            dtm = ea.elapsed_time(eb) / reps * 1e-3
+            gops_by_m[str(mm)] = {"N": nn, "ms_per_step": round(dtm * 1e3, 4),
+                                  "gops": round(float(nn) ** 3 / dtm / 1e9, 1)}
+            chm.close()
+
     # time to periodicity per m (Alg 2 to first detection): build (words, A(G), upload,
     # packing) and chain (products + fused checks + per-step stats decision), max over ranks
     ttp = {}
@@ -351,6 +374,15 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         rate, dt = smp.run(rows)
         cpu = {"value": round(rate, 3), "unit": "Gop/s", "cores": cores_used(), "kind": "oracle",
                "sample": f"{rows} sampled output rows of A^(k-1) (x) A(G), m={m}, dense i-j-k oracle, {dt:.1f} s"}
+        # the oracle's own time to periodicity (Algorithm 2 with the INF-skipping product,
+        # all host cores) beside the GPU's time_to_periodicity
+        import oracle as O
+        ttp_o = {}
+        for mm in args.oracle_ttp_m:
+            t0 = time.perf_counter()
+            r = O.power_chain(mm, 50, am, 0)
+            ttp_o[str(mm)] = {"seconds": round(time.perf_counter() - t0, 4), "triple": [r["n0"], r["alpha"], r["beta"]]}
+        cpu["time_to_periodicity"] = ttp_o
 
     if rank == 0:
         line = {
@@ -378,6 +410,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_periodicity": ttp,
+            "gops_by_m": gops_by_m,
             "paper_context": {"k80_cumatrixtrop_gops_derived": PAPER_K80_GOPS.get(m),
                               "source": "BASELINE.md 1.1, 49 N^3 / Table 3 kernel time"},
         }
