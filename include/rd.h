@@ -271,6 +271,12 @@ int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, 
  * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 
+/* rd_set_split_k — process-wide switch (default on) of split-K in dense chain steps whose
+ * grid is under 3 waves (2 CTAs x the SM count): the k-range is split over 2 or 4 CTAs per
+ * tile and a combine kernel takes the min, stores the power and computes the stats.
+ * Identical results.  Always RD_OK. */
+int rd_set_split_k(int enable);
+
 /* rd_set_sparse_variant — tuning knob of the structured step (process-wide): 0: 512
  * threads per CTA; 1: 512 threads, 2 entry loads in flight per lane; 2: 1024 threads;
  * 3: 1024 threads, 2 in flight.  Identical results.  Errors: RD_EINVAL. */

@@ -161,6 +161,7 @@ struct EpiArgs {
   int32_t *stats;          // MIN-reducible stats vector (nullable: no stats)
   int64_t diag_row0;       // global row index of local row 0 (row panels)
   int accumulate;          // row-major output only: C = min(C, X (x) B)
+  int64_t split_stride;    // split-K (gridDim.y > 1, PM output): u32 between the splits' partial tiles
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -234,10 +235,13 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
 
-  const int KB = kpairs / kBK2;
+  // split-K (gridDim.y > 1): this CTA folds the k-stages [kb0, kb0 + KB) into a partial tile
+  const int KBt = kpairs / kBK2;
+  const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
+  const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
-    if (s < KB) load_stage(s, s);
+    if (s < KB) load_stage(s, kb0 + s);
     cp_async_commit();
   }
 
@@ -246,7 +250,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     __syncthreads();
     {
       int nk = kb + kStages - 1;
-      if (nk < KB) load_stage(nk % kStages, nk);
+      if (nk < KB) load_stage(nk % kStages, kb0 + nk);
       cp_async_commit();
     }
     const uint32_t *sx = smem + (kb % kStages) * kStageWords;
@@ -315,7 +319,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     }
 
   if (OUT_PM) {
-    uint32_t *C = reinterpret_cast<uint32_t *>(Cv);
+    uint32_t *C = reinterpret_cast<uint32_t *>(Cv) + (int64_t)blockIdx.y * epi.split_stride;
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -410,12 +414,86 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   }
 }
 
+// Split-K combine for small grids: C = min over the nsplit partial PM tiles in W (HBM-bound,
+// 16-byte accesses), written into the chain's ring slot, with the diagonal min and the
+// periodicity stats of alphas [a0, a0 + 8) fused (pass a0 > 0 re-reads C instead of W).
+// PM element e = t * ldc + i holds C[i][2t] | C[i][2t+1] << 16 (global row diag_row0 + i).
+__global__ void __launch_bounds__(256) combine_pm_kernel(const uint32_t *__restrict__ W, int64_t stride, int nsplit,
+                                                         uint32_t *__restrict__ C, int64_t nwords, int64_t ldc,
+                                                         EpiArgs epi, int a0) {
+  __shared__ int32_t red[8][1 + 4 * 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int na = max(0, min(8, epi.nprev - a0));
+  int32_t dmin = INT_MAX;
+  uint32_t lo2[8], hi2[8], mis[8], fin[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nwords / 4; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 4 * v;
+    uint4 o;
+    if (a0 == 0) {
+      o = *reinterpret_cast<const uint4 *>(W + e);
+      for (int sp = 1; sp < nsplit; ++sp) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(W + (int64_t)sp * stride + e);
+        o.x = __vmins2(o.x, w.x); o.y = __vmins2(o.y, w.y); o.z = __vmins2(o.z, w.z); o.w = __vmins2(o.w, w.w);
+      }
+      *reinterpret_cast<uint4 *>(C + e) = o;
+      // diagonal: row gi = diag_row0 + i meets column 2t or 2t + 1
+      const int64_t t = e / ldc, i0 = e - t * ldc;
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t gi = epi.diag_row0 + i0 + q;
+        if (gi == 2 * t) dmin = min(dmin, (int)(ow[q] & 0xFFFF));
+        if (gi == 2 * t + 1) dmin = min(dmin, (int)(ow[q] >> 16));
+      }
+    } else {
+      o = *reinterpret_cast<const uint4 *>(C + e);
+    }
+    const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      if (a < na) {
+        const uint4 pv = *reinterpret_cast<const uint4 *>(epi.prev[a0 + a] + e);
+        const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) stats_pair(ow[q], pw[q], lo2[a], hi2[a], mis[a], fin[a]);
+      }
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
+    if (!fin[a]) { lo = INT_MAX; hi = INT_MIN + 1; }
+    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    int32_t v2 = __reduce_min_sync(0xffffffffu, mis[a] ? -1 : 0);
+    int32_t v3 = __reduce_min_sync(0xffffffffu, fin[a] ? -1 : 0);
+    if (lane == 0) {
+      red[warp][1 + 4 * a] = v0; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1 + 4 * na; e += blockDim.x) {
+    int32_t v = red[0][e];
+    for (int w = 1; w < 8; ++w) v = min(v, red[w][e]);
+    if (e == 0) {
+      if (a0 == 0) atomicMin(epi.stats, v);
+    } else {
+      atomicMin(epi.stats + 4 * a0 + e, v);
+    }
+  }
+}
+
 int g_dpx_cols = 3;   // rd_set_gemm_variant (default: measured best)
 
 template <bool OUT_PM, bool STATS, int DPXC>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                  cudaStream_t st) {
+                  cudaStream_t st, int nsplit) {
   static bool attr_set[64] = {};
   int dev = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));
@@ -425,7 +503,7 @@ int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t l
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
-  minplus_gemm_kernel<OUT_PM, STATS, DPXC><<<(unsigned)(nti * ntj), kThreads, kSmemBytes, st>>>(
+  minplus_gemm_kernel<OUT_PM, STATS, DPXC><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads, kSmemBytes, st>>>(
       XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
@@ -434,14 +512,16 @@ int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t l
 template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                cudaStream_t st) {
+                cudaStream_t st, int nsplit = 1) {
+#define RD_LG(D) launch_gemm_v<OUT_PM, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit)
   switch (g_dpx_cols) {
-    case 0: return launch_gemm_v<OUT_PM, STATS, 0>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
-    case 2: return launch_gemm_v<OUT_PM, STATS, 2>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
-    case 3: return launch_gemm_v<OUT_PM, STATS, 3>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
-    case 4: return launch_gemm_v<OUT_PM, STATS, 4>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
-    default: return launch_gemm_v<OUT_PM, STATS, 8>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st);
+    case 0: return RD_LG(0);
+    case 2: return RD_LG(2);
+    case 3: return RD_LG(3);
+    case 4: return RD_LG(4);
+    default: return RD_LG(8);
   }
+#undef RD_LG
 }
 
 int pack_left(const int16_t *X, int64_t ld, int64_t rows, int64_t cols, int64_t row0, uint32_t *XT,
@@ -1002,6 +1082,8 @@ struct rd_chain {
   int32_t *colptr = nullptr;
   uint32_t *ent = nullptr;
   int16_t *wcol = nullptr;   // uniform-label format (see minplus_sparse_kernel)
+  uint32_t *ws = nullptr;    // method 0 split-K partial tiles (small grids), lazily allocated
+  int nsplit = 1;
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
@@ -1270,7 +1352,13 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
   return RD_OK;
 }
 
-static int g_sparse_variant = 3;   // rd_set_sparse_variant (default: measured best, 1024 threads)
+static int g_sparse_variant = 3;
+static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
+
+extern "C" int rd_set_split_k(int enable) {
+  g_split_k_off = enable ? 0 : 1;
+  return RD_OK;
+}   // rd_set_sparse_variant (default: measured best, 1024 threads)
 
 template <int THREADS, int UNROLL, bool UNIFORM>
 static int launch_sparse_u(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
@@ -1312,6 +1400,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
   if (c->colptr) cudaFree(c->colptr);
   if (c->ent) cudaFree(c->ent);
   if (c->wcol) cudaFree(c->wcol);
+  if (c->ws) cudaFree(c->ws);
   delete c;
   return RD_OK;
 }
@@ -1348,9 +1437,39 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
     c->k = knew;
     return RD_OK;
   }
-  int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                   c->N, c->Mp, c->P, epi, c->st);
-  if (rc != RD_OK) return rc;
+  // small grids (< 3 waves of 2 CTAs x 148 SMs) split K so the machine fills; the partial
+  // tiles are combined, stored and reduced by combine_pm_kernel
+  const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
+  const int64_t kstages = (c->P / 2) / kBK2;
+  int nsplit = ntiles >= 888 ? 1 : (ntiles >= 296 ? 2 : 4);
+  while (nsplit > 1 && kstages < 4 * nsplit) nsplit /= 2;
+  if (g_split_k_off) nsplit = 1;
+  if (nsplit == 1) {
+    int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
+                                     c->N, c->Mp, c->P, epi, c->st);
+    if (rc != RD_OK) return rc;
+  } else {
+    if (!c->ws || c->nsplit < nsplit) {
+      if (c->ws) cudaFree(c->ws);
+      c->ws = nullptr;
+      RD_CUDA_CHECK(cudaMalloc((void **)&c->ws, (size_t)nsplit * c->slot_words * 4));
+      c->nsplit = nsplit;
+    }
+    EpiArgs ge{};
+    ge.split_stride = c->slot_words;
+    int rc = launch_gemm<true, false>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->ws, c->Mp, c->Mr, c->N, c->Mp,
+                                      c->P, ge, c->st, nsplit);
+    if (rc != RD_OK) return rc;
+    int dev = c->device, sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nv = c->slot_words / 4;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, (int64_t)sms * 8));
+    for (int a0 = 0; a0 < std::max(epi.nprev, 1); a0 += 8) {
+      combine_pm_kernel<<<grid, 256, 0, c->st>>>(c->ws, c->slot_words, nsplit, c->slot(knew), c->slot_words, c->Mp,
+                                                 epi, a0);
+      RD_CUDA_CHECK(cudaGetLastError());
+    }
+  }
   c->k = knew;
   return RD_OK;
 }

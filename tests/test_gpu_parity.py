@@ -472,3 +472,20 @@ def test_chain_from_packed_operand_equals_built_chain():
         ref.close()
         got.close()
     src.close()
+
+
+@pytest.mark.parametrize("m,r0,r1", [(6, 0, 848), (7, 0, 2507), (8, 0, 1024), (8, 3712, 4736)])
+def test_split_k_equals_single_pass(m, r0, r1):
+    outs = []
+    for on in (True, False):
+        rd.rd_set_split_k(on)
+        try:
+            ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+            st = [ch.step().cpu().numpy() for _ in range(7)]
+            outs.append((st, ch.read_rows(8)))
+            ch.close()
+        finally:
+            rd.rd_set_split_k(True)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert (a == b).all()
+    assert (outs[0][1] == outs[1][1]).all()
