@@ -619,86 +619,81 @@ struct PanelStatsArgs {
   int nprev;
 };
 
-// One pass handles alphas [a0, a0 + 8) so the per-alpha state stays in registers.
-// blockIdx.y walks rows; each thread takes 8 consecutive columns (one 16-byte load per
-// array when aligned) and works on s16x2 pairs like the fused epilogue.
-
+// One pass handles alphas [a0, a0 + 8): warp w of a block owns alpha a0 + w (warps beyond
+// the pass's alphas only read), lane l a 16-byte column chunk; a block sweeps (row,
+// 256-column block) items, so the current power's segment is read once from HBM and
+// re-served from L1 to the block's eight warps.  Per lane the state is one alpha's packed
+// (lo, hi, mis, fin): few registers, many loads in flight.
 __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
                                                           int64_t cols, int64_t ld, int64_t diag_row0,
                                                           PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
   __shared__ int32_t red[8][1 + 4 * 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int na = min(8, pa.nprev - a0);
+  const bool mine = warp < na;
+  const int16_t *P = mine ? pa.prev[a0 + warp] : cur;
   int32_t dmin = INT_MAX;
-  uint32_t lo2[8], hi2[8], mis[8], fin[8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
-  const bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
-  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-    const int64_t gi = diag_row0 + i;
-    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; j < cols;
-         j += (int64_t)gridDim.x * blockDim.x * 8) {
-      const int64_t off = i * ld + j;
-      uint32_t o[4];
-      const bool full = vec && j + 8 <= cols;
-      if (full) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(cur + off);
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t lo = (j + 2 * q < cols) ? (uint16_t)cur[off + 2 * q] : (uint16_t)RD_INF;
-          uint32_t hi = (j + 2 * q + 1 < cols) ? (uint16_t)cur[off + 2 * q + 1] : (uint16_t)RD_INF;
-          o[q] = lo | (hi << 16);
-        }
+  uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+  const bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(P) & 15) == 0);
+  const int64_t nb = (cols + 255) / 256;
+  const int64_t items = rows * nb;
+  for (int64_t v = blockIdx.x; v < items; v += gridDim.x) {
+    const int64_t i = v / nb, j = (v - i * nb) * 256 + lane * 8;
+    if (j >= cols) continue;
+    const int64_t off = i * ld + j;
+    uint32_t o[4], w[4];
+    if (vec && j + 8 <= cols) {
+      const uint4 x = *reinterpret_cast<const uint4 *>(cur + off);
+      o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
+      if (mine) {
+        const uint4 y = *reinterpret_cast<const uint4 *>(P + off);
+        w[0] = y.x; w[1] = y.y; w[2] = y.z; w[3] = y.w;
       }
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q], kInf2);
-      if (a0 == 0 && gi >= j && gi < j + 8) {
+      for (int q = 0; q < 4; ++q) {
+        const bool in0 = j + 2 * q < cols, in1 = j + 2 * q + 1 < cols;
+        o[q] = (in0 ? (uint16_t)cur[off + 2 * q] : (uint16_t)RD_INF) |
+               ((uint32_t)(in1 ? (uint16_t)cur[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
+        if (mine)
+          w[q] = (in0 ? (uint16_t)P[off + 2 * q] : (uint16_t)RD_INF) |
+                 ((uint32_t)(in1 ? (uint16_t)P[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q], kInf2);
+    if (a0 == 0 && warp == 0) {
+      const int64_t gi = diag_row0 + i;
+      if (gi >= j && gi < j + 8) {
         const int t = (int)(gi - j);
         dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
       }
+    }
+    if (mine) {
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        if (a < na) {
-          const int16_t *P = pa.prev[a0 + a];
-          uint32_t w[4];
-          if (full) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(P + off);
-            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t lo = (j + 2 * q < cols) ? (uint16_t)P[off + 2 * q] : (uint16_t)RD_INF;
-              uint32_t hi = (j + 2 * q + 1 < cols) ? (uint16_t)P[off + 2 * q + 1] : (uint16_t)RD_INF;
-              w[q] = lo | (hi << 16);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q], kInf2), lo2[a], hi2[a], mis[a], fin[a]);
-        }
-      }
+      for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q], kInf2), lo2, hi2, mis, fin);
     }
   }
   dmin = __reduce_min_sync(0xffffffffu, dmin);
-  if (lane == 0) red[warp][0] = dmin;
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
-    int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
-    if (!fin[a]) { lo = INT_MAX; hi = INT_MIN + 1; }
-    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
-    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
-    int32_t v2 = __reduce_min_sync(0xffffffffu, mis[a] ? -1 : 0);
-    int32_t v3 = __reduce_min_sync(0xffffffffu, fin[a] ? -1 : 0);
+  {
+    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
+    if (!fin) { lo = INT_MAX; hi = INT_MIN + 1; }
+    const int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    const int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
+    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
     if (lane == 0) {
-      red[warp][1 + 4 * a] = v0; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
+      if (warp == 0) red[0][0] = dmin;
+      if (mine) {
+        red[0][1 + 4 * warp] = v0; red[0][2 + 4 * warp] = v1; red[0][3 + 4 * warp] = v2; red[0][4 + 4 * warp] = v3;
+      }
     }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 1 + 4 * na; e += blockDim.x) {
-    int32_t v = red[0][e];
-    for (int w = 1; w < 8; ++w) v = min(v, red[w][e]);
+    const int32_t v = red[0][e];
     if (e == 0) {
       if (a0 == 0) atomicMin(stats, v);
     } else {
@@ -728,11 +723,11 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // x covers a row (8 columns per thread); y walks rows, ~8 blocks per SM in total
-  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cols + 2047) / 2048, 64));
-  const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sms * 8 / gx + 1));
+  // blocks sweep (row, 256-column block) items; 8 resident blocks per SM
+  const int64_t items = rows * ((cols + 255) / 256);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * 8));
   for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 8) {
-    panel_stats_kernel<<<dim3(gx, gy), 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    panel_stats_kernel<<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
     RD_CUDA_CHECK(cudaGetLastError());
   }
   return RD_OK;
