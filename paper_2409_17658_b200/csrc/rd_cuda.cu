@@ -1098,7 +1098,6 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
   if (row_begin < 0 || row_end > N || row_begin >= row_end)
     return fail(RD_EINVAL, "rd_chain_create: bad row range [%lld, %lld) for N=%lld", (long long)row_begin,
                 (long long)row_end, (long long)N);
-  if (method == 1 && N >= (1 << 17)) return fail(RD_EINVAL, "rd_chain_create: structured step needs N < 131072");
   rd_chain *c = new rd_chain;
   c->m = m;
   c->method = method;

@@ -303,3 +303,67 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
     t2 = time.perf_counter()
     return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
                 t_build=t1 - t0, t_chain=t2 - t1)
+
+
+# ----------------------------------------------------- panel-sequential (one GPU) --
+def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int | None = None, method: int = 1,
+                          policy: int = 0, progress=None):
+    """Algorithm 2 for orders whose ring of powers does not fit one GPU (m = 11: 73 GB per
+    int16 power).  Rows of A^{k+1} depend only on the same rows of A^k, so the chain
+    runs panel by panel to a fixed kmax, each panel's per-power stats vector is kept, and the
+    decision (first k with a uniform alpha, Alg 2 step 4) is taken on the MIN-combined stats
+    afterwards — the same decision the row-panel driver takes across ranks.  Returns the
+    dict of power_sequence plus per-panel timings."""
+    import time
+
+    import torch
+
+    from . import Chain, RD_INF, count_words, rd_stats_decide
+    N = count_words(m)
+    if panel_rows is None:
+        panel_rows = N
+    panel_rows = max(TILE, (panel_rows + TILE - 1) // TILE * TILE)
+    combined = None
+    diag1 = 2**31 - 1
+    timings = []
+    for r0 in range(0, N, panel_rows):
+        r1 = min(N, r0 + panel_rows)
+        t0 = time.perf_counter()
+        ch = Chain(m, alpha_max=alpha_max, row_begin=r0, row_end=r1, method=method)
+        torch.cuda.synchronize()
+        tb = time.perf_counter() - t0
+        diag1 = min(diag1, ch.diag1)
+        rows = []
+        for k in range(2, kmax + 1):
+            rows.append(ch.step().clone())
+        st = torch.stack(rows).cpu().numpy()
+        ch.close()
+        combined = st if combined is None else np.minimum(combined, st)
+        timings.append({"rows": [r0, r1], "build_s": round(tb, 3), "chain_s": round(time.perf_counter() - t0 - tb, 3)})
+        if progress:
+            progress(timings[-1])
+    diag = [2**31 - 1] * (kmax + 1)
+    diag[1] = diag1
+    found_k, n0, al, be, k_stop = -1, 0, 0, 0, kmax
+    for k in range(2, kmax + 1):
+        h = combined[k - 2]
+        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
+        if found_k < 0:
+            dec = rd_stats_decide(h, alpha_max, k)
+            if dec:
+                found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
+                if policy == 0:
+                    k_stop = k
+                    break
+        else:
+            aa = k - n0
+            if aa <= alpha_max:
+                dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
+                if dec:
+                    al, be = dec
+            if aa >= alpha_max:
+                k_stop = k
+                break
+    for k in range(k_stop + 1, kmax + 1):       # powers computed past the decision are not reported
+        diag[k] = 2**31 - 1
+    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=k_stop, diag=diag, panels=timings)

@@ -489,3 +489,15 @@ def test_split_k_equals_single_pass(m, r0, r1):
     for a, b in zip(outs[0][0], outs[1][0]):
         assert (a == b).all()
     assert (outs[0][1] == outs[1][1]).all()
+
+
+
+@pytest.mark.parametrize("m,rows,method", [(6, 256, 1), (7, 640, 1), (7, 1024, 0)])
+def test_panel_sequential_driver_matches_oracle(m, rows, method):
+    from paper_2409_17658_b200 import dist as rdist
+    ref = O.power_chain(m, 50, 5, 0)
+    got = rdist.power_sequence_panels(m, ref["k_stop"] + 3, alpha_max=5, panel_rows=rows, method=method)
+    assert len(got["panels"]) > 1
+    assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                      ref["k_stop"])
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
