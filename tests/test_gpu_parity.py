@@ -379,7 +379,7 @@ def test_m10_structured_chain_pins():
     d = got["diag"]
     for n in range(5, got["k_stop"] + 1, 5):
         assert d[n] == 22 * n // 5, n
-    for n in range(3, 9):
+    for n in range(3, 11):
         assert d[n] == O.gamma_rowdp(10, n), n
     g = O.gamma_from_chain(got, 200)
     assert g == 22 * 200 // 5                      # Cor 12 through the recurrence
@@ -501,3 +501,18 @@ def test_panel_sequential_driver_matches_oracle(m, rows, method):
     assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
                                                                       ref["k_stop"])
     assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+
+@pytest.mark.skipif(__import__("os").environ.get("RD_LONG") != "1", reason="~15 min of GPU; RD_LONG=1")
+def test_m11_panel_sequential_pins():
+    # m = 11 (N = 191476) on one GPU, panel by panel: Cor 12 (24n/5 for 5 | n) and
+    # the independent row DP X3 for n = 3..10
+    from paper_2409_17658_b200 import dist as rdist
+    got = rdist.power_sequence_panels(11, 45, alpha_max=5, panel_rows=57344, method=1)
+    assert got["found"]
+    d = got["diag"]
+    for n in range(5, got["k_stop"] + 1, 5):
+        assert d[n] == 24 * n // 5, n
+    for n in range(3, 11):
+        assert d[n] == O.gamma_rowdp(11, n), n
