@@ -277,6 +277,12 @@ int rd_set_gemm_variant(int dpx_cols);
  * Identical results.  Always RD_OK. */
 int rd_set_split_k(int enable);
 
+/* rd_set_sparse_bytes — process-wide switch (default on) of the structured step's byte
+ * kernel: chains created afterwards over column-uniform labels keep 8 rows per CTA as byte
+ * offsets from each row's minimum (exact while every row's finite spread is <= 254, checked
+ * on every output; the 16-bit kernel takes over otherwise).  Identical results.  RD_OK. */
+int rd_set_sparse_bytes(int enable);
+
 /* rd_set_sparse_variant — tuning knob of the structured step (process-wide): 0: 512
  * threads per CTA; 1: 512 threads, 2 entry loads in flight per lane; 2: 1024 threads;
  * 3: 1024 threads, 2 in flight.  Identical results.  Errors: RD_EINVAL. */

@@ -82,6 +82,7 @@ def lib():
         L.rd_set_gemm_variant.argtypes = [ci]
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
+        L.rd_set_sparse_bytes.argtypes = [ci]
         for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
@@ -89,7 +90,7 @@ def lib():
                   "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant",
                   "rd_power_sequence_matrix", "rd_build_matrix_border", "rd_chain_create_matrix",
                   "rd_closed_form_from", "rd_closed_form", "rd_chain_packed_operand", "rd_chain_create_packed",
-                  "rd_set_split_k"):
+                  "rd_set_split_k", "rd_set_sparse_bytes"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -281,6 +282,11 @@ def rd_set_gemm_variant(dpx_cols: int):
 def rd_set_split_k(enable: bool):
     """Split-K for small dense chain grids (default on; identical results)."""
     _check(lib().rd_set_split_k(1 if enable else 0))
+
+
+def rd_set_sparse_bytes(enable: bool):
+    """Byte kernel of the structured step for later chains (default on; identical results)."""
+    _check(lib().rd_set_sparse_bytes(1 if enable else 0))
 
 
 def rd_set_sparse_variant(v: int):

@@ -162,6 +162,8 @@ struct EpiArgs {
   int64_t diag_row0;       // global row index of local row 0 (row panels)
   int accumulate;          // row-major output only: C = min(C, X (x) B)
   int64_t split_stride;    // split-K (gridDim.y > 1, PM output): u32 between the splits' partial tiles
+  const int *spread_in;    // structured step: 1 if some row of X has a finite spread > 254 (nullable)
+  int *spread_out;         // ... the same flag for the output, for the next step (nullable)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -488,7 +490,8 @@ __global__ void __launch_bounds__(256) combine_pm_kernel(const uint32_t *__restr
   }
 }
 
-int g_dpx_cols = 3;   // rd_set_gemm_variant (default: measured best)
+int g_dpx_cols = 3;
+int g_sparse_bytes = 1;  // rd_set_sparse_bytes(0) disables the structured step's byte kernel   // rd_set_gemm_variant (default: measured best)
 
 template <bool OUT_PM, bool STATS, int DPXC>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
@@ -764,6 +767,39 @@ constexpr int kSpThreadsMax = 1024;    // 1 CTA per SM (shared memory); 16 or 32
 constexpr int kSpMaxAlpha = 16;        // lanes own alphas l+1 and l+9 of their 8-lane group
 constexpr int kSpGroup = 8;            // lanes per output column
 
+// Per-row finite spread of the output (for the next step's byte path): lanes keep packed
+// running min (inf lanes are the largest value, so they never lower it) and max over finite
+// values (inf lanes masked to 0); a CTA folds them per row pair and raises the flag if some
+// row's max - min exceeds 254.
+__device__ __forceinline__ void spread_update(uint32_t v, uint32_t &mn, uint32_t &mx) {
+  mn = __vmins2(mn, v);
+  mx = __vmaxs2(mx, v & ~__vcmpeq2(v, kInf2));
+}
+
+template <int NP>   // NP row pairs per CTA
+__device__ __forceinline__ void spread_finish(uint32_t (&mn)[NP], uint32_t (&mx)[NP], int *flag,
+                                              uint32_t (*smn)[NP], uint32_t (*smx)[NP]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < NP; ++r)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn[r] = __vmins2(mn[r], __shfl_xor_sync(0xffffffffu, mn[r], o));
+      mx[r] = __vmaxs2(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], o));
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r < NP; ++r) { smn[warp][r] = mn[r]; smx[warp][r] = mx[r]; }
+  __syncthreads();
+  if (threadIdx.x < NP) {
+    const int r = threadIdx.x;
+    uint32_t a = smn[0][r], b = smx[0][r];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = __vmins2(a, smn[w][r]); b = __vmaxs2(b, smx[w][r]); }
+    const int lo0 = (int)(a & 0xFFFF), lo1 = (int)(a >> 16), hi0 = (int)(b & 0xFFFF), hi1 = (int)(b >> 16);
+    if ((lo0 < RD_INF && hi0 - lo0 > 254) || (lo1 < RD_INF && hi1 - lo1 > 254)) atomicOr(flag, 1);
+  }
+}
+
 // UNIFORM: every finite entry of column j carries the same label w_j (A(G): l(q,p) depends
 // on p only), so the CSC holds bare shared-memory byte offsets, each column's list is
 // padded to a multiple of 16 with the offset of an all-INF slot xs[Qc], two entries fold
@@ -775,9 +811,12 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
                       EpiArgs epi) {
   extern __shared__ __align__(16) uint2 xs[];
   __shared__ int32_t red[kSpThreads / 32][1 + 4 * kSpMaxAlpha];
+  __shared__ uint32_t smn[kSpThreads / 32][2], smx[kSpThreads / 32][2];
   __shared__ int next_col;
+  if (epi.spread_in && *epi.spread_in == 0) return;   // the byte kernel handles this step
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 3, sl = lane & 7;        // column group in the warp, lane in the group
+  uint32_t smin2[2] = {kInf2, kInf2}, smax2[2] = {0, 0};
   const int64_t p0 = 2 * (int64_t)blockIdx.x;
   const uint32_t *x0 = X + p0 * ld, *x1 = x0 + ld;
   uint32_t *c0 = C + p0 * ld, *c1 = c0 + ld;
@@ -857,6 +896,10 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
       }
       if (sl == 0) c0[j] = a0;
       if (sl == 1) c1[j] = a1;
+      if (last && sl == 0 && epi.spread_out) {
+        spread_update(a0, smin2[0], smax2[0]);
+        spread_update(a1, smin2[1], smax2[1]);
+      }
       if (STATS && last) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -875,6 +918,7 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
       }
     }
   }
+  if (epi.spread_out) spread_finish<2>(smin2, smax2, epi.spread_out, smn, smx);
   if (!STATS) return;
   dmin = __reduce_min_sync(0xffffffffu, dmin);
 #pragma unroll
@@ -905,6 +949,172 @@ minplus_sparse_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uin
     int32_t v = red[0][e];
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) v = min(v, red[w][e]);
+    atomicMin(epi.stats + e, v);
+  }
+}
+
+// The structured step with 8 rows per CTA stored as BYTES in shared memory (uniform labels
+// only): byte r of xs[q] = X[row r][q] - base_r (the row's minimum over the q-chunk), 255 =
+// inf; exact while every row's finite spread is <= 254 (flag spread_in == 0, computed by the
+// previous step; V12: the spread is <= 16 from k = 4 on), otherwise the 16-bit kernel runs.
+// Per gathered uint2 (8 rows) four PRMT expand the bytes into s16x2 pairs and two VIMNMX3 fold
+// two entries; the group's minimum r gives base_r + r + w_j (255 -> inf).  Twice the rows of
+// the 16-bit kernel for the same shared memory halves the per-column work per term.
+template <bool STATS>
+__global__ void __launch_bounds__(1024, 1)
+minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, uint32_t *__restrict__ C,
+                       EpiArgs epi) {
+  constexpr int kT = 1024, kW = kT / 32;
+  extern __shared__ __align__(16) uint2 xs[];
+  __shared__ int32_t red[kW][1 + 4 * kSpMaxAlpha];
+  __shared__ uint32_t smn[kW][4], smx[kW][4], sbase[4];
+  __shared__ int next_col;
+  if (*epi.spread_in != 0) return;                 // the 16-bit kernel handles this step
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 3, sl = lane & 7;
+  const int64_t p0 = 4 * (int64_t)blockIdx.x;     // row pairs p0 .. p0+3 = rows 8b .. 8b+7
+  const int64_t N = sa.N;
+  const int64_t gi0 = epi.diag_row0 + 2 * p0;
+  uint32_t lo2[2] = {0x7FFF7FFFu, 0x7FFF7FFFu}, hi2[2] = {0x80008000u, 0x80008000u}, mis[2] = {0, 0},
+           fin[2] = {0, 0};
+  uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, mx[4] = {0, 0, 0, 0};
+  int32_t dmin = INT_MAX;
+  const char *xb = reinterpret_cast<const char *>(xs);
+  for (int ch = 0; ch < sa.nchunks; ++ch) {
+    const int64_t q0 = (int64_t)ch * sa.Qc;
+    const int qn = (int)min((int64_t)sa.Qc, N - q0);
+    __syncthreads();
+    // per-row minimum over the chunk (inf is the largest value)
+    {
+      uint32_t m4[4] = {kInf2, kInf2, kInf2, kInf2};
+      for (int q = threadIdx.x; q < qn; q += kT)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) m4[r] = __vmins2(m4[r], X[(p0 + r) * ld + q0 + q]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m4[r] = __vmins2(m4[r], __shfl_xor_sync(0xffffffffu, m4[r], o));
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) smn[warp][r] = m4[r];
+      __syncthreads();
+      if (threadIdx.x < 4) {
+        uint32_t a = smn[0][threadIdx.x];
+        for (int w = 1; w < kW; ++w) a = __vmins2(a, smn[w][threadIdx.x]);
+        sbase[threadIdx.x] = a;
+      }
+      __syncthreads();
+    }
+    uint32_t base[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) base[r] = sbase[r];
+    // bytes: x - base (finite, <= 254) or 255 (inf)
+    for (int q = threadIdx.x; q < qn; q += kT) {
+      uint32_t d[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t x = X[(p0 + r) * ld + q0 + q];
+        const uint32_t im = __vcmpeq2(x, kInf2);
+        d[r] = (__vsub2(x, base[r]) & ~im) | (0x00FF00FFu & im);
+      }
+      xs[q] = make_uint2(__byte_perm(d[0], d[1], 0x6420), __byte_perm(d[2], d[3], 0x6420));
+    }
+    if (threadIdx.x == 0) xs[sa.Qc] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);   // padding target
+    if (threadIdx.x == 0) next_col = 0;
+    __syncthreads();
+    const int32_t *cp = sa.colptr + (int64_t)ch * (N + 1);
+    const bool last = ch == sa.nchunks - 1;
+    for (;;) {
+      int bcol = 0;
+      if (lane == 0) bcol = atomicAdd(&next_col, 4);
+      bcol = __shfl_sync(0xffffffffu, bcol, 0);
+      if (bcol >= N) break;
+      const int64_t j = bcol + g;
+      const bool valid = j < N;
+      uint32_t a[4] = {0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu};
+      if (valid) {
+        const int s = __ldg(cp + j), cnt = __ldg(cp + j + 1) - s;   // cnt: a multiple of 16
+        const uint32_t *ep = sa.ent + s + sl;
+#pragma unroll 2
+        for (int t = 0; t < cnt; t += 2 * kSpGroup) {
+          const uint32_t o0 = __ldg(ep + t), o1 = __ldg(ep + t + kSpGroup);
+          const uint2 v0 = *reinterpret_cast<const uint2 *>(xb + o0);
+          const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + o1);
+          a[0] = __vimin3_s16x2(a[0], __byte_perm(v0.x, 0, 0x4140), __byte_perm(v1.x, 0, 0x4140));
+          a[1] = __vimin3_s16x2(a[1], __byte_perm(v0.x, 0, 0x4342), __byte_perm(v1.x, 0, 0x4342));
+          a[2] = __vimin3_s16x2(a[2], __byte_perm(v0.y, 0, 0x4140), __byte_perm(v1.y, 0, 0x4140));
+          a[3] = __vimin3_s16x2(a[3], __byte_perm(v0.y, 0, 0x4342), __byte_perm(v1.y, 0, 0x4342));
+        }
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = __vmins2(a[r], __shfl_xor_sync(0xffffffffu, a[r], o));
+      if (!valid) continue;
+      const uint32_t w = (uint16_t)__ldg(sa.wcol + j);
+      const uint32_t w2 = w | (w << 16);
+      uint32_t v[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // back to absolute: base + r + w (255 -> inf), saturating
+        const uint32_t im = __vcmpeq2(a[r], 0x00FF00FFu);
+        const uint32_t val = __vmins2(__vadd2(__vadd2(a[r], base[r]), w2), kInf2);
+        v[r] = (val & ~im) | (kInf2 & im);
+        if (ch > 0) v[r] = __vmins2(v[r], C[(p0 + r) * ld + j]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (sl == r) C[(p0 + r) * ld + j] = v[r];
+      if (last) {
+        if (sl == 0)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) spread_update(v[r], mn[r], mx[r]);
+        if (STATS) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int al = sl + 8 * h;
+            if (al < epi.nprev) {
+              const uint32_t *P = epi.prev[al];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) stats_pair(v[r], P[(p0 + r) * ld + j], lo2[h], hi2[h], mis[h], fin[h]);
+            }
+          }
+          if (sl == 0 && j >= gi0 && j < gi0 + 8) {
+            const int t = (int)(j - gi0);
+            dmin = min(dmin, (int)((v[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
+          }
+        }
+      }
+    }
+  }
+  spread_finish<4>(mn, mx, epi.spread_out, smn, smx);
+  if (!STATS) return;
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int32_t lo = min((int32_t)(int16_t)(lo2[h] & 0xFFFF), (int32_t)(int16_t)(lo2[h] >> 16));
+    int32_t nhi = -max((int32_t)(int16_t)(hi2[h] & 0xFFFF), (int32_t)(int16_t)(hi2[h] >> 16));
+    int32_t nm = mis[h] ? -1 : 0, nf = fin[h] ? -1 : 0;
+    if (!fin[h]) { lo = INT_MAX; nhi = INT_MAX; }
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      nhi = min(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+      nm = min(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+      nf = min(nf, __shfl_xor_sync(0xffffffffu, nf, o));
+    }
+    const int al = sl + 8 * h;
+    if (g == 0 && al < epi.nprev) {
+      red[warp][1 + 4 * al + 0] = lo;
+      red[warp][1 + 4 * al + 1] = nhi;
+      red[warp][1 + 4 * al + 2] = nm;
+      red[warp][1 + 4 * al + 3] = nf;
+    }
+  }
+  if (lane == 0) red[warp][0] = dmin;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1 + 4 * epi.nprev; e += kT) {
+    int32_t v = red[0][e];
+    for (int w = 1; w < kW; ++w) v = min(v, red[w][e]);
     atomicMin(epi.stats + e, v);
   }
 }
@@ -1079,6 +1289,7 @@ struct rd_chain {
   int16_t *wcol = nullptr;   // uniform-label format (see minplus_sparse_kernel)
   uint32_t *ws = nullptr;    // method 0 split-K partial tiles (small grids), lazily allocated
   int nsplit = 1;
+  int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
@@ -1114,7 +1325,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     c->slot_words = (c->P / 2) * c->Mp;
   } else {
     c->P = round_up(N, 4);          // RP pitch (u32 per row pair)
-    c->Mp = round_up(c->Mr, 4);     // whole CTAs of 4 rows
+    c->Mp = round_up(c->Mr, 8);     // whole CTAs of 8 (byte kernel) or 4 rows
     c->slot_words = (c->Mp / 2) * c->P;
   }
   const int16_t *A = Ahost;
@@ -1130,6 +1341,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     if (c->colptr) cudaFree(c->colptr);
     if (c->ent) cudaFree(c->ent);
     if (c->wcol) cudaFree(c->wcol);
+    if (c->spread) cudaFree(c->spread);
     delete c;
     return code;
   };
@@ -1149,12 +1361,24 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     }
     c->nnz = colptr.back();
     std::vector<int16_t> wcol;
-    // measured: the uniform-label format wins when the q-range is chunked
-    // (m = 10: 510 vs 762 ms per step) and loses at m = 9 (30.0 vs 24.1 ms)
-    if (c->nchunks > 1 && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol)) {
+    // uniform labels (A(G): l(q,p) depends on p only) take the byte kernel (8 rows per CTA);
+    // without it, the 16-bit kernel measured faster on the general format at m = 9 (24.5 vs
+    // 30.0 ms) and slower at m = 10 (762 vs 521 ms), DESIGN.md §5
+    const bool want_uniform = g_sparse_bytes || c->nchunks > 1;
+    if (want_uniform && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol)) {
       if ((e = cudaMalloc((void **)&c->wcol, wcol.size() * 2)) != cudaSuccess ||
           (e = cudaMemcpyAsync(c->wcol, wcol.data(), wcol.size() * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
         return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
+      if (g_sparse_bytes) {
+        int16_t mxl = 0;
+        for (int16_t x : wcol)
+          if (x < RD_INF) mxl = std::max(mxl, x);
+        const int init[2] = {0, mxl > 254 ? 1 : 0};   // flags[1] describes A^1 (row spread <= max label)
+        if ((e = cudaMalloc((void **)&c->spread, 8)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(c->spread, init, 8, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
+          return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
+      }
     }
     if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
         (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
@@ -1349,6 +1573,11 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
 
+extern "C" int rd_set_sparse_bytes(int enable) {
+  g_sparse_bytes = enable ? 1 : 0;
+  return RD_OK;
+}
+
 extern "C" int rd_set_split_k(int enable) {
   g_split_k_off = enable ? 0 : 1;
   return RD_OK;
@@ -1395,6 +1624,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
   if (c->ent) cudaFree(c->ent);
   if (c->wcol) cudaFree(c->wcol);
   if (c->ws) cudaFree(c->ws);
+  if (c->spread) cudaFree(c->spread);
   delete c;
   return RD_OK;
 }
@@ -1418,6 +1648,27 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   epi.diag_row0 = c->r0;
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
+  if (c->method == 1 && c->spread) {
+    // byte kernel (8 rows / CTA) unless the current power's flag says some row spreads > 254,
+    // then the 16-bit kernel; both launched, the one not selected exits at once (no host sync)
+    SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N, c->wcol};
+    epi.spread_in = c->spread + (c->k & 1);
+    epi.spread_out = c->spread + (knew & 1);
+    RD_CUDA_CHECK(cudaMemsetAsync(c->spread + (knew & 1), 0, 4, c->st));
+    static bool attr8[64] = {};
+    if (c->device >= 0 && c->device < 64 && !attr8[c->device]) {
+      RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSpSmemMax));
+      attr8[c->device] = true;
+    }
+    minplus_sparse8_kernel<true><<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 1) * 8, c->st>>>(
+        c->slot(c->k), c->P, sa, c->slot(knew), epi);
+    RD_CUDA_CHECK(cudaGetLastError());
+    int rc1 = launch_sparse<1024, 2>(c, sa, knew, epi);
+    if (rc1 != RD_OK) return rc1;
+    c->k = knew;
+    return RD_OK;
+  }
   if (c->method == 1) {
     SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N, c->wcol};
     int rc1 = RD_OK;

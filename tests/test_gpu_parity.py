@@ -516,3 +516,45 @@ def test_m11_panel_sequential_pins():
         assert d[n] == 24 * n // 5, n
     for n in range(3, 11):
         assert d[n] == O.gamma_rowdp(11, n), n
+
+
+@pytest.mark.parametrize("wmax,kmax", [(20, 30), (100, 12), (300, 10)])
+def test_structured_byte_path_and_fallback(wmax, kmax):
+    # column-uniform labels select the byte kernel; wider labels make row spreads cross 254
+    # during the chain (wmax=100) or from the start (wmax=300), forcing the 16-bit kernel
+    rng = np.random.default_rng(wmax)
+    N = 700
+    pat = rng.random((N, N)) < 0.02
+    np.fill_diagonal(pat, True)
+    w = rng.integers(0, wmax + 1, size=N)
+    A16 = np.where(pat, w[None, :], RINF).astype(np.int16)
+    A32 = to_inf(A16, RINF, OINF, np.int32)
+    ch = rd.Chain(0, alpha_max=4, method=1, matrix=A16)
+    X = A32.copy()
+    for k in range(2, kmax + 1):
+        st = ch.step().cpu().numpy()
+        X = O.minplus(X, A32, skip=True)
+        got = ch.read_rows(k)
+        assert (got == to_inf(X, OINF, RINF, np.int16)).all(), (wmax, k)
+        assert st[0] == min(int(np.diag(X).min()), RINF)
+    ch.close()
+    for method in (0, 1):
+        got = rd.rd_power_sequence_matrix(A16, kmax, 4, 0, method)
+        ref = O.power_chain_matrix(A32, kmax, 4, 0)
+        assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+def test_structured_bytes_on_off_identical():
+    outs = []
+    for on in (True, False):
+        rd.rd_set_sparse_bytes(on)
+        try:
+            ch = rd.Chain(8, alpha_max=6, method=1, row_begin=1000, row_end=2999)
+            st = [ch.step().cpu().numpy() for _ in range(8)]
+            outs.append((st, ch.read_rows(9)))
+            ch.close()
+        finally:
+            rd.rd_set_sparse_bytes(True)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert (a == b).all()
+    assert (outs[0][1] == outs[1][1]).all()
