@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmds = [
         ["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-I", INCLUDE, "-c",
          os.path.join(CSRC, "rd_host.cpp"), "-o", host_o],
-        [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+        [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "-Xptxas", "-v",
          "-I", INCLUDE, "-c", os.path.join(CSRC, "rd_cuda.cu"), "-o", cuda_o],
         [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", host_o, cuda_o, "-o", LIB + ".tmp",
          "-lgomp", "-lpthread"],

@@ -763,7 +763,6 @@ struct SpArgs {
   const int16_t *wcol;    // uniform format: the label of column j (RD_INF if the column is empty)
 };
 
-constexpr int kSpThreadsMax = 1024;    // 1 CTA per SM (shared memory); 16 or 32 warps
 constexpr int kSpMaxAlpha = 16;        // lanes own alphas l+1 and l+9 of their 8-lane group
 constexpr int kSpGroup = 8;            // lanes per output column
 
