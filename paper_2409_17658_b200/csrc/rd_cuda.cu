@@ -29,6 +29,14 @@
 
 using namespace rd;
 
+// Entry of every C-ABI call of this file: clear this thread's message and drop a stale,
+// non-sticky CUDA error left by an earlier failed call (e.g. an out-of-memory cudaMalloc that
+// was reported as RD_ENOMEM), so a later launch check does not report it again.
+static inline void rd_enter() {
+  clear_error();
+  (void)cudaGetLastError();
+}
+
 #define RD_CUDA_CHECK(expr)                                                                     \
   do {                                                                                          \
     cudaError_t e_ = (expr);                                                                    \
@@ -546,7 +554,7 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 }  // namespace
 
 extern "C" int rd_set_gemm_variant(int dpx_cols) {
-  clear_error();
+  rd_enter();
   if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
     return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
   g_dpx_cols = dpx_cols;
@@ -554,7 +562,7 @@ extern "C" int rd_set_gemm_variant(int dpx_cols) {
 }
 
 extern "C" int rd_set_device(int device) {
-  clear_error();
+  rd_enter();
   RD_CUDA_CHECK(cudaSetDevice(device));
   return RD_OK;
 }
@@ -578,7 +586,7 @@ static int retain_default_pool() {
 static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, int accumulate,
                             const char *who) {
-  clear_error();
+  rd_enter();
   if (!A || !B || !C) return fail(RD_EINVAL, "%s: NULL pointer", who);
   if (M < 1 || N < 1 || K < 1) return fail(RD_EINVAL, "%s: M, N, K must be >= 1", who);
   if (lda < K || ldb < N || ldc < N) return fail(RD_EINVAL, "%s: leading dimension too small", who);
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
 extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, int nprev, int64_t rows,
                               int64_t cols, int64_t ld, int64_t diag_row0, int alpha_max, int32_t *stats_dev,
                               void *cuda_stream) {
-  clear_error();
+  rd_enter();
   if (!cur || !stats_dev || (nprev > 0 && !prev)) return fail(RD_EINVAL, "rd_panel_stats: NULL argument");
   if (alpha_max < 1 || alpha_max > kMaxAlpha || nprev < 0 || nprev > alpha_max)
     return fail(RD_EINVAL, "rd_panel_stats: need 0 <= nprev <= alpha_max <= 32");
@@ -737,9 +745,9 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
 }
 
 extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N) {
-  if (!A || !B || !C) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: NULL pointer"); }
-  if (N < 1) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: N must be >= 1"); }
-  if (C == A || C == B) { clear_error(); return fail(RD_EINVAL, "rd_minplus_mul: C aliases an input"); }
+  if (!A || !B || !C) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: NULL pointer"); }
+  if (N < 1) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: N must be >= 1"); }
+  if (C == A || C == B) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: C aliases an input"); }
   return rd_minplus_mul_ex(A, N, B, N, C, N, N, N, N, nullptr);
 }
 
@@ -1466,7 +1474,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
 
 extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
                                   void *cuda_stream, rd_chain **out) {
-  clear_error();
+  rd_enter();
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
@@ -1496,7 +1504,7 @@ static int check_matrix(const int16_t *A, int64_t N, int32_t *maxlab, const char
 
 extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max, int64_t row_begin,
                                       int64_t row_end, int method, void *cuda_stream, rd_chain **out) {
-  clear_error();
+  rd_enter();
   int32_t mx = 0;
   if (int rc = check_matrix(A, N, &mx, "rd_chain_create_matrix")) return rc;
   // entries above RD_INF are +inf: clamp a copy so every path sees RD_INF exactly
@@ -1509,7 +1517,7 @@ extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max
 // (e.g. broadcast over NVLink from rank 0): no host build, the A^1 panel comes from BP.
 extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, int64_t row_end,
                                       const uint32_t *bp_dev, int32_t diag1, void *cuda_stream, rd_chain **out) {
-  clear_error();
+  rd_enter();
   if (!out || !bp_dev) return fail(RD_EINVAL, "rd_chain_create_packed: NULL argument");
   *out = nullptr;
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create_packed: m=%d out of range", m);
@@ -1561,7 +1569,7 @@ extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, i
 }
 
 extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_dev, int64_t *words) {
-  clear_error();
+  rd_enter();
   if (!c || !bp_dev || !words) return fail(RD_EINVAL, "rd_chain_packed_operand: NULL argument");
   if (c->method != 0 || !c->BP) return fail(RD_EINVAL, "rd_chain_packed_operand: not a dense chain");
   *bp_dev = c->BP;
@@ -1604,7 +1612,7 @@ static int launch_sparse(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs 
 }
 
 extern "C" int rd_set_sparse_variant(int v) {
-  clear_error();
+  rd_enter();
   if (v < 0 || v > 3) return fail(RD_EINVAL, "rd_set_sparse_variant: 0..3");
   g_sparse_variant = v;
   return RD_OK;
@@ -1637,7 +1645,7 @@ extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
 }
 
 extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
-  clear_error();
+  rd_enter();
   if (!c || !stats_dev) return fail(RD_EINVAL, "rd_chain_step: NULL argument");
   const int knew = c->k + 1;
   EpiArgs epi{};
@@ -1719,7 +1727,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
 }
 
 extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
-  clear_error();
+  rd_enter();
   if (!c || !host_out) return fail(RD_EINVAL, "rd_chain_read_rows: NULL argument");
   if (k < 1 || k > c->k || k < c->k - c->alpha_max)
     return fail(RD_EINVAL, "rd_chain_read_rows: power %d not in the ring (current %d)", k, c->k);
@@ -1760,7 +1768,7 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
 
 extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
                                      int32_t *diag) {
-  clear_error();
+  rd_enter();
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
   if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, 2 * m, out, diag)) return rc0;
   const int64_t N = count_words(m);
@@ -1774,7 +1782,7 @@ extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy,
 
 extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, int alpha_max, int policy,
                                         int method, rd_period_t *out, int32_t *diag) {
-  clear_error();
+  rd_enter();
   int32_t mx = 0;
   if (int rc0 = check_matrix(A, N, &mx, "rd_power_sequence_matrix")) return rc0;
   if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, mx, out, diag)) return rc0;
@@ -1970,7 +1978,7 @@ int probe_one(int sms, double *minplus_per_clk_sm, double *mhz, double *instr_pe
 }  // namespace
 
 extern "C" int rd_alu_probe(double out[4]) {
-  clear_error();
+  rd_enter();
   if (!out) return fail(RD_EINVAL, "rd_alu_probe: NULL");
   int dev = 0, sms = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));

@@ -558,3 +558,34 @@ def test_structured_bytes_on_off_identical():
     for a, b in zip(outs[0][0], outs[1][0]):
         assert (a == b).all()
     assert (outs[0][1] == outs[1][1]).all()
+
+
+@pytest.mark.parametrize("m,method", [(8, 0), (9, 0), (9, 1)])
+def test_every_power_sampled_rows_full_size(m, method):
+    # rows of A^k for every k up to first detection, recomputed by the oracle's INF-skipping
+    # row recurrence (row_k = row_{k-1} (x) A)
+    A = O.matrix(m)
+    N = A.shape[0]
+    kstop = {8: 26, 9: 27}[m]
+    rows = sample_rows(N, 40, seed=100 + m)
+    R = A[rows].copy()
+    ch = rd.Chain(m, alpha_max=10, method=method)
+    for k in range(2, kstop + 1):
+        ch.step()
+        R = O.minplus(R, A, skip=True)
+        got = ch.read_rows(k)[rows]
+        assert (got == to_inf(R, OINF, RINF, np.int16)).all(), (m, k)
+    ch.close()
+
+
+def test_device_allocation_failure_is_reported():
+    # a dense m = 11 chain with a 33-power ring needs ~2.4 TB: RD_ENOMEM, no crash, and the
+    # device stays usable
+    with pytest.raises(rd.RDError) as e:
+        rd.Chain(11, alpha_max=32)
+    assert e.value.status in (rd.RD_ENOMEM, rd.RD_EINVAL)
+    with pytest.raises(rd.RDError) as e:
+        rd.Chain(3, alpha_max=17, method=1)          # structured step: alpha_max <= 16
+    assert e.value.status == rd.RD_EINVAL
+    C = rd.rd_minplus_mul(_gpu(operand(64, 64, 1)), _gpu(operand(64, 64, 2)))
+    assert C.shape == (64, 64)
