@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8, 9])
     p.add_argument("--oracle-ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--gops-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
+    p.add_argument("--ttp-structured-only-m", type=int, nargs="*", default=[10])
     p.add_argument("--form", default="replicated", choices=["replicated", "allgather"],
                    help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
                         "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step")
@@ -366,6 +367,23 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                                           "terms_per_step": NNZ.get(mm, 0) * nn,
                                           "chain_gterms": round((rs["k_stop"] - 1) * NNZ.get(mm, 0) * nn
                                                                 / float(ts[1]) / 1e9, 1)}
+
+    # orders whose dense chain takes minutes: the structured chain only (NEXT-2/NEXT-3)
+    if not args.no_e2e:
+        for mm in args.ttp_structured_only_m:
+            if world > 1:
+                dist.barrier()
+            rs = rdist.power_sequence(mm, 50, am, method=1)
+            ts = torch.tensor([rs["t_build"], rs["t_chain"]], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+            nn = rd.count_words(mm)
+            ttp[str(mm)] = {"k_stop": rs["k_stop"], "triple": [rs["n0"], rs["alpha"], rs["beta"]],
+                            "structured": {"build_s": round(float(ts[0]), 4), "chain_s": round(float(ts[1]), 4),
+                                           "total_s": round(float(ts[0] + ts[1]), 4),
+                                           "terms_per_step": NNZ.get(mm, 0) * nn,
+                                           "chain_gterms": round((rs["k_stop"] - 1) * NNZ.get(mm, 0) * nn
+                                                                 / float(ts[1]) / 1e9, 1)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
