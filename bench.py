@@ -311,7 +311,9 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         te = float(te.item())
         prods = res["k_stop"] - 1
         e2e = {"value": round(prods * float(N) ** 3 / te / 1e9, 3), "unit": "Gop/s",
-               "h2d_bytes_per_step": int(2 * N * N), "d2h_bytes_per_step": int(prods * rd.rd_stats_len(am) * 4),
+               # the chain uploads A(G)'s CSC (colptr + entries), the device builds the operands
+               "h2d_bytes_per_step": int(4 * (NNZ.get(m, 0) + N + 1)),
+               "d2h_bytes_per_step": int(prods * rd.rd_stats_len(am) * 4),
                "step": "one rd_power_sequence(m, 50) call: build + upload A, chain to first detection",
                "seconds": round(te, 3), "k_stop": res["k_stop"],
                "triple": [res["n0"], res["alpha"], res["beta"]]}
