@@ -1693,8 +1693,10 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   // tiles are combined, stored and reduced by combine_pm_kernel
   const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
   const int64_t kstages = (c->P / 2) / kBK2;
-  int nsplit = ntiles >= 888 ? 1 : (ntiles >= 296 ? 2 : 4);
-  while (nsplit > 1 && kstages < 4 * nsplit) nsplit /= 2;
+  // aim for >= 4 waves of 2 x 148 CTAs; each split keeps >= 2 pipeline stages of k
+  int nsplit = (int)std::min<int64_t>(8, std::max<int64_t>(1, (1184 + ntiles - 1) / ntiles));
+  if (ntiles >= 888) nsplit = 1;
+  while (nsplit > 1 && kstages < 2 * nsplit) --nsplit;
   if (g_split_k_off) nsplit = 1;
   if (nsplit == 1) {
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
