@@ -307,13 +307,18 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
 
 # ----------------------------------------------------- panel-sequential (one GPU) --
 def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int | None = None, method: int = 1,
-                          policy: int = 0, progress=None):
+                          policy: int = 0, progress=None, early_stop: bool = True):
     """Algorithm 2 for orders whose ring of powers does not fit one GPU (m = 11: 73 GB per
     int16 power).  Rows of A^{k+1} depend only on the same rows of A^k, so the chain
-    runs panel by panel to a fixed kmax, each panel's per-power stats vector is kept, and the
-    decision (first k with a uniform alpha, Alg 2 step 4) is taken on the MIN-combined stats
-    afterwards — the same decision the row-panel driver takes across ranks.  Returns the
-    dict of power_sequence plus per-panel timings."""
+    runs panel by panel, each panel's per-power stats vector is kept, and the decision (first
+    k with a uniform alpha, Alg 2 step 4) is taken on the MIN-combined stats afterwards — the
+    same decision the row-panel driver takes across ranks.
+
+    early_stop: the first panel runs to its own first detection plus a margin (4 powers, or
+    alpha_max under policy 1) and the other panels to the same power; combining panels can only
+    delay a detection (MIN of the stats never creates uniformity), so if the combined decision
+    is not reached there, everything is recomputed to kmax.  Returns the dict of
+    power_sequence plus per-panel timings."""
     import time
 
     import torch
@@ -323,47 +328,69 @@ def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int
     if panel_rows is None:
         panel_rows = N
     panel_rows = max(TILE, (panel_rows + TILE - 1) // TILE * TILE)
-    combined = None
-    diag1 = 2**31 - 1
-    timings = []
-    for r0 in range(0, N, panel_rows):
-        r1 = min(N, r0 + panel_rows)
+    bounds = [(r0, min(N, r0 + panel_rows)) for r0 in range(0, N, panel_rows)]
+    margin = alpha_max if policy == 1 else 4
+
+    def run(r0, r1, kstop, stop_on_detect):
         t0 = time.perf_counter()
         ch = Chain(m, alpha_max=alpha_max, row_begin=r0, row_end=r1, method=method)
         torch.cuda.synchronize()
         tb = time.perf_counter() - t0
-        diag1 = min(diag1, ch.diag1)
-        rows = []
-        for k in range(2, kmax + 1):
+        rows, k_end, seen = [], kstop, False
+        for k in range(2, kstop + 1):
             rows.append(ch.step().clone())
+            if stop_on_detect and not seen and rd_stats_decide(rows[-1].cpu().numpy(), alpha_max, k):
+                seen, k_end = True, min(kstop, k + margin)
+            if k >= k_end:
+                break
         st = torch.stack(rows).cpu().numpy()
+        d1 = ch.diag1
         ch.close()
-        combined = st if combined is None else np.minimum(combined, st)
-        timings.append({"rows": [r0, r1], "build_s": round(tb, 3), "chain_s": round(time.perf_counter() - t0 - tb, 3)})
+        t = {"rows": [r0, r1], "k_end": k_end, "build_s": round(tb, 3),
+             "chain_s": round(time.perf_counter() - t0 - tb, 3)}
         if progress:
-            progress(timings[-1])
-    diag = [2**31 - 1] * (kmax + 1)
-    diag[1] = diag1
-    found_k, n0, al, be, k_stop = -1, 0, 0, 0, kmax
-    for k in range(2, kmax + 1):
-        h = combined[k - 2]
-        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
-        if found_k < 0:
-            dec = rd_stats_decide(h, alpha_max, k)
-            if dec:
-                found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
-                if policy == 0:
+            progress(t)
+        return st, d1, t
+
+    def decide(combined, kend):
+        found_k, n0, al, be, k_stop = -1, 0, 0, 0, kend
+        for k in range(2, kend + 1):
+            h = combined[k - 2]
+            if found_k < 0:
+                dec = rd_stats_decide(h, alpha_max, k)
+                if dec:
+                    found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
+                    if policy == 0:
+                        k_stop = k
+                        break
+            else:
+                aa = k - n0
+                if aa <= alpha_max:
+                    dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
+                    if dec:
+                        al, be = dec
+                if aa >= alpha_max:
                     k_stop = k
                     break
-        else:
-            aa = k - n0
-            if aa <= alpha_max:
-                dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
-                if dec:
-                    al, be = dec
-            if aa >= alpha_max:
-                k_stop = k
-                break
-    for k in range(k_stop + 1, kmax + 1):       # powers computed past the decision are not reported
-        diag[k] = 2**31 - 1
+        complete = found_k >= 0 and (policy == 0 or k_stop - n0 >= alpha_max)
+        return complete, found_k, n0, al, be, k_stop
+
+    for attempt in (0, 1):
+        timings, combined, diag1 = [], None, 2**31 - 1
+        kend = kmax
+        for idx, (r0, r1) in enumerate(bounds):
+            st, d1, t = run(r0, r1, kend, early_stop and attempt == 0 and idx == 0)
+            if idx == 0:
+                kend = t["k_end"]
+            timings.append(t)
+            diag1 = min(diag1, d1)
+            combined = st if combined is None else np.minimum(combined, st[:combined.shape[0]])
+        complete, found_k, n0, al, be, k_stop = decide(combined, kend)
+        if complete or kend >= kmax:
+            break
+    diag = [2**31 - 1] * (kmax + 1)
+    diag[1] = diag1
+    for k in range(2, k_stop + 1):
+        h = combined[k - 2]
+        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
     return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=k_stop, diag=diag, panels=timings)
