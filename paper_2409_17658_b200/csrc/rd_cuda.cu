@@ -18,6 +18,7 @@
 // The GEMM writes its output C = A^{k+1} directly in the PM layout (pairs along j), so
 // the output of one power step is the left operand of the next one.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges cost nothing without an attached tool
 
 #include <algorithm>
 #include <climits>
@@ -28,6 +29,12 @@
 #include "rd_internal.h"
 
 using namespace rd;
+
+// Scoped NVTX range (one per power step / chain build / power sequence)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Entry of every C-ABI call of this file: clear this thread's message and drop a stale,
 // non-sticky CUDA error left by an earlier failed call (e.g. an out-of-memory cudaMalloc that
@@ -1307,6 +1314,7 @@ struct rd_chain {
 // words of length m (border = App. A rules), with no dense matrix on the host or device.
 static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_max, int64_t row_begin,
                              int64_t row_end, int method, void *cuda_stream, rd_chain **out, bool border = false) {
+  NvtxRange nvtx_range("rd_chain_create");
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
   if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_chain_create: method must be 0 (dense) or 1 (structured)");
@@ -1646,6 +1654,7 @@ extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
 
 extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   rd_enter();
+  NvtxRange nvtx_range(c && c->method == 1 ? "rd_chain_step structured" : "rd_chain_step");
   if (!c || !stats_dev) return fail(RD_EINVAL, "rd_chain_step: NULL argument");
   const int knew = c->k + 1;
   EpiArgs epi{};
@@ -1799,6 +1808,7 @@ extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, i
 // Algorithm 2's loop over a created chain (consumes c and st).
 static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
                               rd_period_t *out, int32_t *diag) {
+  NvtxRange nvtx_range("rd_power_sequence");
   const int64_t N = c->N;
   int rc = RD_OK;
 
