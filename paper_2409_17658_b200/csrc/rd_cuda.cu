@@ -1038,16 +1038,38 @@ minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, ui
     __syncthreads();
     const int32_t *cp = sa.colptr + (int64_t)ch * (N + 1);
     const bool last = ch == sa.nchunks - 1;
-    for (;;) {
-      int bcol = 0;
-      if (lane == 0) bcol = atomicAdd(&next_col, 4);
-      bcol = __shfl_sync(0xffffffffu, bcol, 0);
-      if (bcol >= N) break;
+    // software-pipelined column loop: the next batch is grabbed and its colptr loaded while the
+    // current column's entries are walked; the label and the previous powers' entries for the
+    // stats are requested before the walk so their latency overlaps it
+    int bcol = 0;
+    if (lane == 0) bcol = atomicAdd(&next_col, 4);
+    bcol = __shfl_sync(0xffffffffu, bcol, 0);
+    int s_n = 0, e_n = 0;
+    if (bcol + g < N) { s_n = __ldg(cp + bcol + g); e_n = __ldg(cp + bcol + g + 1); }
+    while (bcol < N) {
       const int64_t j = bcol + g;
       const bool valid = j < N;
+      const int s = s_n, cnt = e_n - s_n;                             // cnt: a multiple of 16
+      int nb = 0;
+      if (lane == 0) nb = atomicAdd(&next_col, 4);
+      nb = __shfl_sync(0xffffffffu, nb, 0);
+      if (nb + g < N) { s_n = __ldg(cp + nb + g); e_n = __ldg(cp + nb + g + 1); }
+      uint32_t wl = 0, pv[2][4];
+      if (valid) {
+        wl = (uint16_t)__ldg(sa.wcol + j);
+        if (STATS && last) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int al = sl + 8 * h;
+            const uint32_t *P = epi.prev[al < epi.nprev ? al : 0];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) pv[h][r] = (al < epi.nprev) ? P[(p0 + r) * ld + j] : 0u;
+          }
+        }
+      }
+      bcol = nb;
       uint32_t a[4] = {0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu};
       if (valid) {
-        const int s = __ldg(cp + j), cnt = __ldg(cp + j + 1) - s;   // cnt: a multiple of 16
         const uint32_t *ep = sa.ent + s + sl;
 #pragma unroll 2
         for (int t = 0; t < cnt; t += 2 * kSpGroup) {
@@ -1065,8 +1087,7 @@ minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, ui
 #pragma unroll
         for (int r = 0; r < 4; ++r) a[r] = __vmins2(a[r], __shfl_xor_sync(0xffffffffu, a[r], o));
       if (!valid) continue;
-      const uint32_t w = (uint16_t)__ldg(sa.wcol + j);
-      const uint32_t w2 = w | (w << 16);
+      const uint32_t w2 = wl | (wl << 16);
       uint32_t v[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {   // back to absolute: base + r + w (255 -> inf), saturating
@@ -1087,9 +1108,8 @@ minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, ui
           for (int h = 0; h < 2; ++h) {
             const int al = sl + 8 * h;
             if (al < epi.nprev) {
-              const uint32_t *P = epi.prev[al];
 #pragma unroll
-              for (int r = 0; r < 4; ++r) stats_pair(v[r], P[(p0 + r) * ld + j], lo2[h], hi2[h], mis[h], fin[h]);
+              for (int r = 0; r < 4; ++r) stats_pair(v[r], pv[h][r], lo2[h], hi2[h], mis[h], fin[h]);
             }
           }
           if (sl == 0 && j >= gi0 && j < gi0 + 8) {
