@@ -217,7 +217,10 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                     int nti, int ntj, uint32_t one, EpiArgs epi) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  // a warp covers 4 (ty) x 8 (tx) threads of the 16 x 16 grid: its fragment loads touch 4 and 8
+  // distinct 16-byte chunks (one shared-memory wavefront each)
+  const int wq = tid >> 5, lq = tid & 31;
+  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
   int64_t i0, j0;
   {
     const int bid = blockIdx.x;
