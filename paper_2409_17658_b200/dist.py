@@ -38,6 +38,45 @@ def neutral_stats(alpha_max: int) -> np.ndarray:
     return s
 
 
+class Decider:
+    """Algorithm 2 step 4 on the reduced stats of successive powers, shared by every
+    driver: feed(k, stats) records diag[k] (Cor 7) and returns True once the sequence can stop
+    — at the first detection under policy 0 (Lemma 2), or once A^{n0+alpha_max} is
+    seen under policy 1 (the largest alpha <= alpha_max with A^{n0+alpha} = beta (x) A^{n0}).
+    Same decisions as rd_power_sequence_ex (R6)."""
+
+    def __init__(self, alpha_max: int, policy: int, kmax: int, diag1: int):
+        self.alpha_max, self.policy, self.kmax = alpha_max, policy, kmax
+        self.diag = [2**31 - 1] * (kmax + 1)
+        self.diag[1] = diag1
+        self.found_k, self.n0, self.alpha, self.beta, self.k_stop = -1, 0, 0, 0, 1
+
+    def feed(self, k: int, h) -> bool:
+        from . import RD_INF, rd_stats_decide
+        self.k_stop = k
+        self.diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
+        if self.found_k < 0:
+            dec = rd_stats_decide(h, self.alpha_max, k)
+            if dec:
+                self.found_k, self.n0, self.alpha, self.beta = k, k - dec[0], dec[0], dec[1]
+                return self.policy == 0
+            return False
+        aa = k - self.n0
+        if aa <= self.alpha_max:
+            dec = rd_stats_decide(h, self.alpha_max, k, only_alpha=aa)
+            if dec:
+                self.alpha, self.beta = dec
+        return aa >= self.alpha_max
+
+    @property
+    def complete(self) -> bool:
+        return self.found_k >= 0 and (self.policy == 0 or self.k_stop - self.n0 >= self.alpha_max)
+
+    def result(self, **extra) -> dict:
+        return dict(found=self.found_k >= 0, n0=self.n0, alpha=self.alpha, beta=self.beta,
+                    k_stop=self.k_stop, diag=self.diag, **extra)
+
+
 class _EmptyPanel:
     """A rank without rows (more ranks than row tiles) still joins every collective."""
 
@@ -142,33 +181,16 @@ def power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0,
     if torch.cuda.is_available():
         torch.cuda.synchronize()
     t1 = time.perf_counter()
-    diag = [2**31 - 1] * (kmax + 1)
-    diag[1] = diag1
-    found_k, n0, al, be, k = -1, 0, 0, 0, 1
+    dec = Decider(alpha_max, policy, kmax, diag1)
     for k in range(2, kmax + 1):
         s = chain.step()
         if world > 1:
             dist.all_reduce(s, op=dist.ReduceOp.MIN, group=group)
-        h = s.cpu().numpy()
-        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
-        if found_k < 0:
-            dec = rd_stats_decide(h, alpha_max, k)
-            if dec:
-                found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
-                if policy == 0:
-                    break
-        else:
-            aa = k - n0
-            if aa <= alpha_max:
-                dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
-                if dec:
-                    al, be = dec
-            if aa >= alpha_max:
-                break
+        if dec.feed(k, s.cpu().numpy()):
+            break
     t2 = time.perf_counter()
     chain.close()
-    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
-                t_build=t1 - t0, t_chain=t2 - t1)
+    return dec.result(t_build=t1 - t0, t_chain=t2 - t1)
 
 
 # ----------------------------------------------------------- all-gather form --
@@ -273,9 +295,7 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
     if on_gpu:
         torch.cuda.synchronize()
     t1 = time.perf_counter()
-    diag = [2**31 - 1] * (kmax + 1)
-    diag[1] = d1
-    found_k, n0, al, be, k = -1, 0, 0, 0, 1
+    dec = Decider(alpha_max, policy, kmax, d1)
     for k in range(2, kmax + 1):
         Xk = minplus_mul_allgather(A_rows, ring[k - 1], bounds, group, acc=acc)
         ring[k] = Xk
@@ -283,26 +303,11 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
         s = stats(Xk, prevs)
         if world > 1:
             dist.all_reduce(s, op=dist.ReduceOp.MIN, group=group)
-        h = s.cpu().numpy()
         ring.pop(k - alpha_max - 1, None)
-        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
-        if found_k < 0:
-            dec = rd_stats_decide(h, alpha_max, k)
-            if dec:
-                found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
-                if policy == 0:
-                    break
-        else:
-            aa = k - n0
-            if aa <= alpha_max:
-                dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
-                if dec:
-                    al, be = dec
-            if aa >= alpha_max:
-                break
+        if dec.feed(k, s.cpu().numpy()):
+            break
     t2 = time.perf_counter()
-    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=min(k, kmax), diag=diag,
-                t_build=t1 - t0, t_chain=t2 - t1)
+    return dec.result(t_build=t1 - t0, t_chain=t2 - t1)
 
 
 # ----------------------------------------------------- panel-sequential (one GPU) --
@@ -352,28 +357,12 @@ def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int
             progress(t)
         return st, d1, t
 
-    def decide(combined, kend):
-        found_k, n0, al, be, k_stop = -1, 0, 0, 0, kend
+    def decide(combined, kend, diag1):
+        dec = Decider(alpha_max, policy, kmax, diag1)
         for k in range(2, kend + 1):
-            h = combined[k - 2]
-            if found_k < 0:
-                dec = rd_stats_decide(h, alpha_max, k)
-                if dec:
-                    found_k, n0, al, be = k, k - dec[0], dec[0], dec[1]
-                    if policy == 0:
-                        k_stop = k
-                        break
-            else:
-                aa = k - n0
-                if aa <= alpha_max:
-                    dec = rd_stats_decide(h, alpha_max, k, only_alpha=aa)
-                    if dec:
-                        al, be = dec
-                if aa >= alpha_max:
-                    k_stop = k
-                    break
-        complete = found_k >= 0 and (policy == 0 or k_stop - n0 >= alpha_max)
-        return complete, found_k, n0, al, be, k_stop
+            if dec.feed(k, combined[k - 2]):
+                break
+        return dec
 
     for attempt in (0, 1):
         timings, combined, diag1 = [], None, 2**31 - 1
@@ -385,12 +374,7 @@ def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int
             timings.append(t)
             diag1 = min(diag1, d1)
             combined = st if combined is None else np.minimum(combined, st[:combined.shape[0]])
-        complete, found_k, n0, al, be, k_stop = decide(combined, kend)
-        if complete or kend >= kmax:
+        dec = decide(combined, kend, diag1)
+        if dec.complete or kend >= kmax:
             break
-    diag = [2**31 - 1] * (kmax + 1)
-    diag[1] = diag1
-    for k in range(2, k_stop + 1):
-        h = combined[k - 2]
-        diag[k] = int(h[0]) if h[0] < RD_INF else 2**31 - 1
-    return dict(found=found_k >= 0, n0=n0, alpha=al, beta=be, k_stop=k_stop, diag=diag, panels=timings)
+    return dec.result(panels=timings)
