@@ -277,10 +277,19 @@ int rd_set_gemm_variant(int dpx_cols);
  * Identical results.  Always RD_OK. */
 int rd_set_split_k(int enable);
 
-/* rd_set_sparse_bytes — process-wide switch (default on) of the structured step's byte
- * kernel: chains created afterwards over column-uniform labels keep 8 rows per CTA as byte
- * offsets from each row's minimum (exact while every row's finite spread is <= 254, checked
- * on every output; the 16-bit kernel takes over otherwise).  Identical results.  RD_OK. */
+/* rd_set_sparse_bytes — process-wide choice of the structured step's kernel for chains
+ * created afterwards over column-uniform labels:
+ *   2 (default) slab layout: columns of the powers stored in in-degree order, one warp lane
+ *     per output column, 8 rows per CTA as byte offsets from each row's minimum; diag and
+ *     the periodicity stats run after the product (a row sample, then full passes only for
+ *     the alphas the sample cannot rule out);
+ *   1 byte kernel, natural order, 8-lane groups per column, fused stats;
+ *   0 16-bit kernel only.
+ * The byte forms are exact while every row's finite spread is <= 254 (checked on every
+ * output; the 16-bit kernel takes over otherwise).  Identical powers, diag and decisions;
+ * in modes 2 the stats entries of an alpha that a subset of rows already proves aperiodic
+ * cover that subset only (still MIN-reducible and decided identically).
+ * RD_EINVAL outside 0..2. */
 int rd_set_sparse_bytes(int enable);
 
 /* rd_set_sparse_variant — tuning knob of the structured step (process-wide): 0: 512

@@ -284,9 +284,12 @@ def rd_set_split_k(enable: bool):
     _check(lib().rd_set_split_k(1 if enable else 0))
 
 
-def rd_set_sparse_bytes(enable: bool):
-    """Byte kernel of the structured step for later chains (default on; identical results)."""
-    _check(lib().rd_set_sparse_bytes(1 if enable else 0))
+def rd_set_sparse_bytes(mode):
+    """Structured-step kernel for later chains: 2 slab byte kernel (default, also True),
+    1 byte kernel in natural order, 0 (False) 16-bit kernel only.  Identical results."""
+    if isinstance(mode, bool):
+        mode = 2 if mode else 0
+    _check(lib().rd_set_sparse_bytes(int(mode)))
 
 
 def rd_set_sparse_variant(v: int):

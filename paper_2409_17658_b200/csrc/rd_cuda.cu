@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(256) combine_pm_kernel(const uint32_t *__restr
   }
 }
 
-int g_dpx_cols = 3;
-int g_sparse_bytes = 1;  // rd_set_sparse_bytes(0) disables the structured step's byte kernel   // rd_set_gemm_variant (default: measured best)
+int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
+int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
 
 template <bool OUT_PM, bool STATS, int DPXC>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
@@ -1156,6 +1156,208 @@ minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, ui
   }
 }
 
+// The structured step in the slab layout (build_slab_layout): one LANE per output column
+// (columns sorted by in-degree, so a warp's 32 lanes walk lists of nearly equal length), rows as
+// bytes in shared memory as in minplus_sparse8_kernel.  Per 4 entries a lane issues 4 coalesced
+// offset loads (one 128-byte line per warp each), 4 LDS.64 gathers, 16 PRMT and 8 VIMNMX3; a
+// column has no cross-lane fold unless it was split (segmented shuffle min).  The step only
+// produces C and the spread flag; diag and periodicity stats run after it (rp_diag_kernel,
+// rp_stats_kernel), since here they would cost more than the product.
+struct SlabArgs {
+  const int4 *desc;        // per slab: entry offset, L (multiple of 4), head mask, 0
+  const int32_t *lane_col; // per slab lane: output column j' or -1
+  const uint32_t *ent8;    // lane-interleaved byte offsets
+  const int32_t *slab_start;
+  int nchunks, Qc;
+  int64_t N;
+  const int16_t *wcol;
+};
+
+__global__ void __launch_bounds__(1024, 1)
+minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, uint32_t *__restrict__ C,
+                     const int *spread_in, int *spread_out) {
+  constexpr int kT = 1024, kW = kT / 32;
+  extern __shared__ __align__(16) uint2 xs[];
+  __shared__ uint32_t smn[kW][4], smx[kW][4], sbase[4];
+  __shared__ int next_slab;
+  if (*spread_in != 0) return;                     // the 16-bit kernel handles this step
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = 4 * (int64_t)blockIdx.x;     // row pairs p0 .. p0+3
+  const int64_t N = sa.N;
+  uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, mx[4] = {0, 0, 0, 0};
+  const char *xb = reinterpret_cast<const char *>(xs);
+  for (int ch = 0; ch < sa.nchunks; ++ch) {
+    const int64_t q0 = (int64_t)ch * sa.Qc;
+    const int qn = (int)min((int64_t)sa.Qc, N - q0);
+    __syncthreads();
+    {
+      uint32_t m4[4] = {kInf2, kInf2, kInf2, kInf2};
+      for (int q = threadIdx.x; q < qn; q += kT)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) m4[r] = __vmins2(m4[r], X[(p0 + r) * ld + q0 + q]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m4[r] = __vmins2(m4[r], __shfl_xor_sync(0xffffffffu, m4[r], o));
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) smn[warp][r] = m4[r];
+      __syncthreads();
+      if (threadIdx.x < 4) {
+        uint32_t a = smn[0][threadIdx.x];
+        for (int w = 1; w < kW; ++w) a = __vmins2(a, smn[w][threadIdx.x]);
+        sbase[threadIdx.x] = a;
+      }
+      __syncthreads();
+    }
+    uint32_t base[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) base[r] = sbase[r];
+    for (int q = threadIdx.x; q < qn; q += kT) {
+      uint32_t d[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t x = X[(p0 + r) * ld + q0 + q];
+        const uint32_t im = __vcmpeq2(x, kInf2);
+        d[r] = (__vsub2(x, base[r]) & ~im) | (0x00FF00FFu & im);
+      }
+      xs[q] = make_uint2(__byte_perm(d[0], d[1], 0x6420), __byte_perm(d[2], d[3], 0x6420));
+    }
+    if (threadIdx.x == 0) { xs[sa.Qc] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu); next_slab = 0; }
+    __syncthreads();
+    const int s0 = sa.slab_start[ch], ns = sa.slab_start[ch + 1] - s0;
+    const bool last = ch == sa.nchunks - 1;
+    for (;;) {
+      int s = 0;
+      if (lane == 0) s = atomicAdd(&next_slab, 1);
+      s = __shfl_sync(0xffffffffu, s, 0);
+      if (s >= ns) break;
+      const int4 d = __ldg(sa.desc + s0 + s);
+      const int col = __ldg(sa.lane_col + (int64_t)(s0 + s) * 32 + lane);
+      const uint32_t *ep = sa.ent8 + d.x + lane;
+      uint32_t a[4] = {0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu};
+      for (int t = 0; t < d.y; t += 4) {
+        const uint32_t o0 = __ldg(ep + (t + 0) * 32), o1 = __ldg(ep + (t + 1) * 32);
+        const uint32_t o2 = __ldg(ep + (t + 2) * 32), o3 = __ldg(ep + (t + 3) * 32);
+        const uint2 v0 = *reinterpret_cast<const uint2 *>(xb + o0);
+        const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + o1);
+        const uint2 v2 = *reinterpret_cast<const uint2 *>(xb + o2);
+        const uint2 v3 = *reinterpret_cast<const uint2 *>(xb + o3);
+        a[0] = __vimin3_s16x2(a[0], __byte_perm(v0.x, 0, 0x4140), __byte_perm(v1.x, 0, 0x4140));
+        a[1] = __vimin3_s16x2(a[1], __byte_perm(v0.x, 0, 0x4342), __byte_perm(v1.x, 0, 0x4342));
+        a[2] = __vimin3_s16x2(a[2], __byte_perm(v0.y, 0, 0x4140), __byte_perm(v1.y, 0, 0x4140));
+        a[3] = __vimin3_s16x2(a[3], __byte_perm(v0.y, 0, 0x4342), __byte_perm(v1.y, 0, 0x4342));
+        a[0] = __vimin3_s16x2(a[0], __byte_perm(v2.x, 0, 0x4140), __byte_perm(v3.x, 0, 0x4140));
+        a[1] = __vimin3_s16x2(a[1], __byte_perm(v2.x, 0, 0x4342), __byte_perm(v3.x, 0, 0x4342));
+        a[2] = __vimin3_s16x2(a[2], __byte_perm(v2.y, 0, 0x4140), __byte_perm(v3.y, 0, 0x4140));
+        a[3] = __vimin3_s16x2(a[3], __byte_perm(v2.y, 0, 0x4342), __byte_perm(v3.y, 0, 0x4342));
+      }
+      const uint32_t head = (uint32_t)d.z;
+      if (head != 0xFFFFFFFFu) {   // split columns: segmented min towards each segment's head
+        const uint32_t above = head & ~((2u << lane) - 1u);
+        const int segend = above ? __ffs(above) - 1 : 32;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t u = __shfl_down_sync(0xffffffffu, a[r], o);
+            if (lane + o < segend) a[r] = __vmins2(a[r], u);
+          }
+      }
+      if (col < 0 || !((head >> lane) & 1u)) continue;
+      const uint32_t wl = (uint16_t)__ldg(sa.wcol + col);
+      const uint32_t w2 = wl | (wl << 16);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // back to absolute: base + r + w (255 -> inf), saturating
+        const uint32_t im = __vcmpeq2(a[r], 0x00FF00FFu);
+        const uint32_t val = __vmins2(__vadd2(__vadd2(a[r], base[r]), w2), kInf2);
+        uint32_t v = (val & ~im) | (kInf2 & im);
+        uint32_t *cp = C + (p0 + r) * ld + col;
+        if (ch > 0) v = __vmins2(v, *cp);
+        *cp = v;
+        if (last) spread_update(v, mn[r], mx[r]);
+      }
+    }
+  }
+  spread_finish<4>(mn, mx, spread_out, smn, smx);
+}
+
+// diag[k] for a row panel in RP layout whose columns are permuted (inv: state -> column;
+// nullptr = identity): min over local rows i of X[i][inv[r0 + i]].
+__global__ void rp_diag_kernel(const uint32_t *__restrict__ X, int64_t ld, int64_t rows, int64_t r0,
+                               const int32_t *__restrict__ inv, int32_t *stats) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t v = INT_MAX;
+  if (i < rows) {
+    const int64_t j = inv ? inv[r0 + i] : r0 + i;
+    const uint32_t w = X[(i >> 1) * ld + j];
+    v = (int32_t)((i & 1) ? (w >> 16) : (w & 0xFFFF));
+  }
+  v = __reduce_min_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v != INT_MAX) atomicMin(stats, v);
+}
+
+// Periodicity stats of an RP panel against earlier powers (rd_chain_step layout, entries
+// 1..4*nprev; elementwise, so any consistent layout works).  Warp w of a block owns alpha w+1,
+// lanes take 16-byte column chunks, a block sweeps (row pair, 128-column block) items and the
+// current power's line is re-served from L1 to the 16 warps.
+//   SAMPLE: only row pairs with (p / 4) % stride == 0 (a fixed subset of rows).
+//   otherwise: every row pair, but only alphas the vector does not already prove aperiodic
+//   (a subset that is not uniform proves the whole is not; a "survivor" is recomputed in full
+//   and MIN-merged — min over subset and full = full).  Blocks that see a survivor turn into a
+//   non-survivor while others merge skip it: it is proven aperiodic by then.
+template <bool SAMPLE>
+__global__ void __launch_bounds__(512) rp_stats_kernel(const uint32_t *__restrict__ cur, int64_t ld,
+                                                       int64_t pairs, int64_t cols, int stride,
+                                                       PanelStatsArgs pa, int32_t *stats) {
+  __shared__ int any;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bool mine = warp < pa.nprev;
+  if (!SAMPLE) {
+    if (mine) {
+      const volatile int32_t *s = stats + 1 + 4 * warp;
+      const int32_t lo = s[0], nhi = s[1], nmis = s[2], nfin = s[3];
+      mine = nmis == 0 && (nfin == 0 || lo == -nhi);
+    }
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    if (mine && lane == 0) any = 1;
+    __syncthreads();
+    if (!any) return;
+  }
+  if (!mine) return;     // no barrier below: warps without an alpha to test leave at once
+  const uint32_t *P = reinterpret_cast<const uint32_t *>(pa.prev[warp]);
+  uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+  const int64_t nb = (cols + 127) / 128;
+  const int64_t np = SAMPLE ? ((pairs + 4LL * stride - 1) / (4LL * stride)) * 4 : pairs;
+  const int64_t items = np * nb;
+  for (int64_t v = blockIdx.x; v < items; v += gridDim.x) {
+    const int64_t ip = v / nb;
+    const int64_t p = SAMPLE ? (ip / 4) * 4 * stride + (ip & 3) : ip;
+    const int64_t j = (v - ip * nb) * 128 + lane * 4;
+    if (p >= pairs || j >= cols) continue;
+    const uint4 x = *reinterpret_cast<const uint4 *>(cur + p * ld + j);
+    const uint4 y = *reinterpret_cast<const uint4 *>(P + p * ld + j);
+    stats_pair(x.x, y.x, lo2, hi2, mis, fin);
+    stats_pair(x.y, y.y, lo2, hi2, mis, fin);
+    stats_pair(x.z, y.z, lo2, hi2, mis, fin);
+    stats_pair(x.w, y.w, lo2, hi2, mis, fin);
+  }
+  int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
+  int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
+  if (!fin) { lo = INT_MAX; hi = INT_MIN + 1; }
+  const int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+  const int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+  const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
+  const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
+  if (lane == 0) {
+    atomicMin(stats + 1 + 4 * warp, v0);
+    atomicMin(stats + 2 + 4 * warp, v1);
+    atomicMin(stats + 3 + 4 * warp, v2);
+    atomicMin(stats + 4 + 4 * warp, v3);
+  }
+}
+
 // Row-major int16 rows [row0, row0+rows) of X (ld) -> RP u32 [pairs][ldr], INF padded.
 __global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
                                int64_t row0, uint32_t *__restrict__ RP, int64_t ldr, int64_t pairs) {
@@ -1189,7 +1391,8 @@ __global__ void scatter_dense_operands_kernel(const int32_t *__restrict__ colptr
 // A^1 rows [r0, r1) into an all-INF RP slot straight from the CSC (thread per column).
 __global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent, int64_t N,
                                   int nchunks, int Qc, int64_t r0, int64_t r1, uint32_t *__restrict__ RP,
-                                  int64_t ldr, const int16_t *__restrict__ wcol) {
+                                  int64_t ldr, const int16_t *__restrict__ wcol,
+                                  const int32_t *__restrict__ perm) {   // perm: CSC row q' -> state
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   uint16_t *h = reinterpret_cast<uint16_t *>(RP);
@@ -1206,7 +1409,8 @@ __global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint
         ql = ent[t] & 0x1FFFFu;
         w = (uint16_t)(ent[t] >> 17);
       }
-      const int64_t q = (int64_t)ch * Qc + ql;
+      int64_t q = (int64_t)ch * Qc + ql;
+      if (perm) q = perm[q];
       if (q < r0 || q >= r1) continue;
       const int64_t i = q - r0;
       h[((i >> 1) * ldr + j) * 2 + (i & 1)] = w;
@@ -1214,12 +1418,12 @@ __global__ void scatter_rp_kernel(const int32_t *__restrict__ colptr, const uint
   }
 }
 
-// RP -> row-major int16 rows x cols
+// RP -> row-major int16 rows x cols (inv: state -> stored column, nullptr = identity)
 __global__ void unpack_rp_kernel(const uint32_t *__restrict__ RP, int64_t ldr, int64_t rows, int64_t cols,
-                                 int16_t *__restrict__ X) {
+                                 int16_t *__restrict__ X, const int32_t *__restrict__ inv) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (i >= rows || j >= cols) return;
-  const uint32_t w = RP[(i >> 1) * ldr + j];
+  const uint32_t w = RP[(i >> 1) * ldr + (inv ? inv[j] : j)];
   X[i * cols + j] = (int16_t)((i & 1) ? (w >> 16) : (w & 0xFFFF));
 }
 
@@ -1309,6 +1513,150 @@ bool csc_to_uniform(int64_t N, int nchunks, int Qc, std::vector<int32_t> &colptr
   ent.swap(uent);
   return true;
 }
+
+// Slab layout of the structured step (minplus_slab8_kernel).  The chain runs in a column-
+// permuted basis: X'_k = A^k P^T with P sorting the states by in-degree (descending), so that
+// C' = X' (x) A' with A' = P A P^T (rows of the powers stay in natural order; diag and the
+// periodicity test are invariant).  Per q'-chunk the columns j' are dealt to
+// warp lanes in order, 32 per slab; a column longer than T is split over adjacent lanes of one
+// slab (segments, folded by a segmented shuffle min).  Entries are stored lane-interleaved,
+// ent8[off + t*32 + lane] = byte offset ql*8 of the t-th entry of that lane (Qc*8 = padding),
+// so a warp reads one coalesced 128-byte line per t.
+struct SlabHost {
+  std::vector<int32_t> perm, inv;         // new column -> state, state -> new column
+  std::vector<int32_t> ucolptr;           // uniform CSC in the new basis (16-bit fallback kernel)
+  std::vector<uint32_t> uent;
+  std::vector<int16_t> wcol;              // label of new column j'
+  std::vector<int32_t> desc;              // per slab: off, L, headmask, 0
+  std::vector<int32_t> lane_col;          // per slab lane: j' or -1
+  std::vector<uint32_t> ent8;
+  std::vector<int32_t> slab_start;        // per chunk, nchunks + 1
+};
+
+// From the natural general-format CSC (entries (q - q0) | w << 17, chunks of Qc).  Returns
+// false if some column mixes labels (then the chain keeps the natural basis).
+bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t> &colptr,
+                       const std::vector<uint32_t> &ent, SlabHost &S) {
+  std::vector<int32_t> deg((size_t)N, 0), lab((size_t)N, -1);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    for (int64_t j = 0; j < N; ++j) {
+      deg[j] += cp[j + 1] - cp[j];
+      for (int32_t t = cp[j]; t < cp[j + 1]; ++t) {
+        const int32_t w = (int32_t)(ent[t] >> 17);
+        if (lab[j] < 0) lab[j] = w;
+        else if (lab[j] != w) return false;
+      }
+    }
+  }
+  S.perm.resize((size_t)N);
+  for (int64_t j = 0; j < N; ++j) S.perm[j] = (int32_t)j;
+  std::stable_sort(S.perm.begin(), S.perm.end(), [&](int32_t a, int32_t b) { return deg[a] > deg[b]; });
+  S.inv.resize((size_t)N);
+  for (int64_t j = 0; j < N; ++j) S.inv[S.perm[j]] = (int32_t)j;
+  S.wcol.assign((size_t)N, RD_INF);
+  for (int64_t j = 0; j < N; ++j)
+    if (lab[S.perm[j]] >= 0) S.wcol[j] = (int16_t)lab[S.perm[j]];
+  // lists per (new chunk, new column) of ql = q' - chunk start, ascending
+  std::vector<int32_t> cnt((size_t)nchunks * N, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+    for (int64_t j = 0; j < N; ++j)
+      for (int32_t t = cp[j]; t < cp[j + 1]; ++t) {
+        const int64_t q = (int64_t)ch * Qc + (ent[t] & 0x1FFFFu), qn = S.inv[q];
+        cnt[(size_t)(qn / Qc) * N + S.inv[j]]++;
+      }
+  }
+  std::vector<int64_t> lp((size_t)nchunks * N + 1, 0);
+  for (size_t i = 0; i < cnt.size(); ++i) lp[i + 1] = lp[i] + cnt[i];
+  std::vector<int32_t> lists((size_t)std::max<int64_t>(lp.back(), 1));
+  {
+    std::vector<int64_t> pos(lp.begin(), lp.end() - 1);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int32_t *cp = colptr.data() + (size_t)ch * (N + 1);
+      for (int64_t j = 0; j < N; ++j)
+        for (int32_t t = cp[j]; t < cp[j + 1]; ++t) {
+          const int64_t q = (int64_t)ch * Qc + (ent[t] & 0x1FFFFu), qn = S.inv[q];
+          const int64_t c = qn / Qc;
+          lists[pos[(size_t)c * N + S.inv[j]]++] = (int32_t)(qn - c * Qc);
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < (int64_t)cnt.size(); ++i) std::sort(lists.begin() + lp[i], lists.begin() + lp[i + 1]);
+  }
+  const uint32_t pad = (uint32_t)Qc * 8u;
+  // uniform CSC (lists padded to 16) for the 16-bit fallback kernel
+  S.ucolptr.assign((size_t)nchunks * (N + 1), 0);
+  int64_t total = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int32_t *up = S.ucolptr.data() + (size_t)ch * (N + 1);
+    up[0] = (int32_t)total;
+    for (int64_t j = 0; j < N; ++j) {
+      total += (cnt[(size_t)ch * N + j] + 15) / 16 * 16;
+      up[j + 1] = (int32_t)total;
+    }
+  }
+  S.uent.assign((size_t)std::max<int64_t>(total, 1), pad);
+  for (int ch = 0; ch < nchunks; ++ch)
+    for (int64_t j = 0; j < N; ++j) {
+      const size_t li = (size_t)ch * N + j;
+      const int32_t u0 = S.ucolptr[(size_t)ch * (N + 1) + j];
+      for (int64_t t = lp[li]; t < lp[li + 1]; ++t) S.uent[u0 + (t - lp[li])] = (uint32_t)lists[t] * 8u;
+    }
+  // slabs
+  S.desc.clear(); S.lane_col.clear(); S.ent8.clear();
+  S.slab_start.assign((size_t)nchunks + 1, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    S.slab_start[ch] = (int32_t)(S.desc.size() / 4);
+    int64_t maxlen = 0;
+    for (int64_t j = 0; j < N; ++j) maxlen = std::max<int64_t>(maxlen, cnt[(size_t)ch * N + j]);
+    const int64_t T = std::max<int64_t>(256, (maxlen + 31) / 32);
+    // lanes of the slab being filled: (column, first entry index, length)
+    struct Piece { int32_t col; int64_t b; int32_t len; bool head; };
+    std::vector<Piece> cur;
+    auto flush = [&]() {
+      if (cur.empty()) return;
+      int32_t L = 0;
+      for (auto &p : cur) L = std::max(L, p.len);
+      L = (L + 3) / 4 * 4;
+      const int64_t off = (int64_t)S.ent8.size();
+      S.ent8.resize((size_t)(off + (int64_t)L * 32), pad);
+      uint32_t head = 0;
+      for (int l = 0; l < 32; ++l) {
+        if (l < (int)cur.size()) {
+          const Piece &p = cur[l];
+          if (p.head) head |= 1u << l;
+          for (int32_t t = 0; t < p.len; ++t) S.ent8[off + (int64_t)t * 32 + l] = (uint32_t)lists[p.b + t] * 8u;
+          S.lane_col.push_back(p.col);
+        } else {
+          head |= 1u << l;
+          S.lane_col.push_back(-1);
+        }
+      }
+      S.desc.push_back((int32_t)off);
+      S.desc.push_back(L);
+      S.desc.push_back((int32_t)head);
+      S.desc.push_back(0);
+      cur.clear();
+    };
+    for (int64_t j = 0; j < N; ++j) {
+      const size_t li = (size_t)ch * N + j;
+      const int64_t d = cnt[li];
+      const int64_t pieces = d <= T ? 1 : (d + T - 1) / T;
+      if ((int64_t)cur.size() + pieces > 32) flush();
+      const int64_t per = pieces == 1 ? d : (d + pieces - 1) / pieces;
+      for (int64_t p = 0; p < pieces; ++p) {
+        const int64_t b = p * per, e = std::min<int64_t>(d, b + per);
+        cur.push_back(Piece{(int32_t)j, lp[li] + b, (int32_t)std::max<int64_t>(0, e - b), p == 0});
+      }
+      if (cur.size() == 32) flush();
+    }
+    flush();
+  }
+  S.slab_start[nchunks] = (int32_t)(S.desc.size() / 4);
+  if (S.ent8.empty()) S.ent8.push_back(pad);
+  return true;
+}
 }  // namespace
 
 // ================================================================ power chain ==
@@ -1327,6 +1675,11 @@ struct rd_chain {
   uint32_t *ws = nullptr;    // method 0 split-K partial tiles (small grids), lazily allocated
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
+  // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
+  // column; the 16-bit fallback reads colptr/ent/wcol in the same basis
+  int32_t *perm = nullptr, *inv = nullptr, *lane_col = nullptr, *slab_start = nullptr;
+  int4 *desc = nullptr;
+  uint32_t *ent8 = nullptr;
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
@@ -1380,6 +1733,9 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     if (c->ent) cudaFree(c->ent);
     if (c->wcol) cudaFree(c->wcol);
     if (c->spread) cudaFree(c->spread);
+    for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
+                    (void *)c->ent8})
+      if (p) cudaFree(p);
     delete c;
     return code;
   };
@@ -1399,15 +1755,41 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     }
     c->nnz = colptr.back();
     std::vector<int16_t> wcol;
+    // slab layout (g_sparse_bytes == 2): column-permuted basis, lane-per-column byte kernel
+    // (below N = 2048 the step is launch-bound: the single fused 16-bit kernel is fastest,
+    // m = 6: 36 vs 55 us)
+    const int mode = (g_sparse_bytes == 2 && N < 2048) ? 0 : g_sparse_bytes;
+    bool slab = false;
+    if (mode == 2) {
+      SlabHost S;
+      if (build_slab_layout(N, c->nchunks, c->Qc, colptr, ent, S)) {
+        slab = true;
+        colptr.swap(S.ucolptr);
+        ent.swap(S.uent);
+        wcol.swap(S.wcol);
+        auto up = [&](void **dst, const void *src, size_t bytes) {
+          if ((e = cudaMalloc(dst, bytes)) != cudaSuccess) return false;
+          return (e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->st)) == cudaSuccess;
+        };
+        if (!up((void **)&c->perm, S.perm.data(), S.perm.size() * 4) ||
+            !up((void **)&c->inv, S.inv.data(), S.inv.size() * 4) ||
+            !up((void **)&c->lane_col, S.lane_col.data(), S.lane_col.size() * 4) ||
+            !up((void **)&c->slab_start, S.slab_start.data(), S.slab_start.size() * 4) ||
+            !up((void **)&c->desc, S.desc.data(), S.desc.size() * 4) ||
+            !up((void **)&c->ent8, S.ent8.data(), S.ent8.size() * 4) ||
+            (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
+          return cleanup(fail(RD_ENOMEM, "rd_chain_create: slab layout: %s", cudaGetErrorString(e)));
+      }
+    }
     // uniform labels (A(G): l(q,p) depends on p only) take the byte kernel (8 rows per CTA);
     // without it, the 16-bit kernel measured faster on the general format at m = 9 (24.5 vs
     // 30.0 ms) and slower at m = 10 (762 vs 521 ms), DESIGN.md §5
-    const bool want_uniform = g_sparse_bytes || c->nchunks > 1;
-    if (want_uniform && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol)) {
+    const bool want_uniform = mode || c->nchunks > 1;
+    if (slab || (want_uniform && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol))) {
       if ((e = cudaMalloc((void **)&c->wcol, wcol.size() * 2)) != cudaSuccess ||
           (e = cudaMemcpyAsync(c->wcol, wcol.data(), wcol.size() * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
         return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
-      if (g_sparse_bytes) {
+      if (mode) {
         int16_t mxl = 0;
         for (int16_t x : wcol)
           if (x < RD_INF) mxl = std::max(mxl, x);
@@ -1430,12 +1812,13 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
       return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
     int64_t n = (alpha_max + 1) * c->slot_words;
     fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(c->ring, n, kInf2);
-    if (A) {
+    if (A && !slab) {
       dim3 grid((unsigned)((c->P + 255) / 256), (unsigned)(c->Mp / 2));
       pack_rp_kernel<<<grid, 256, 0, c->st>>>(dA, N, c->Mr, N, c->r0, c->slot(1), c->P, c->Mp / 2);
     } else {
       scatter_rp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(c->colptr, c->ent, N, c->nchunks, c->Qc,
-                                                                          c->r0, c->r1, c->slot(1), c->P, c->wcol);
+                                                                          c->r0, c->r1, c->slot(1), c->P, c->wcol,
+                                                                          c->perm);
     }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
       return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
@@ -1612,7 +1995,9 @@ static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
 
 extern "C" int rd_set_sparse_bytes(int enable) {
-  g_sparse_bytes = enable ? 1 : 0;
+  rd_enter();
+  if (enable < 0 || enable > 2) return fail(RD_EINVAL, "rd_set_sparse_bytes: 0, 1 or 2");
+  g_sparse_bytes = enable;
   return RD_OK;
 }
 
@@ -1621,15 +2006,15 @@ extern "C" int rd_set_split_k(int enable) {
   return RD_OK;
 }   // rd_set_sparse_variant (default: measured best, 1024 threads)
 
-template <int THREADS, int UNROLL, bool UNIFORM>
+template <int THREADS, int UNROLL, bool UNIFORM, bool STATS = true>
 static int launch_sparse_u(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
   static bool attr_set[64] = {};
   if (c->device >= 0 && c->device < 64 && !attr_set[c->device]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<true, THREADS, UNROLL, UNIFORM>,
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_sparse_kernel<STATS, THREADS, UNROLL, UNIFORM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemMax));
     attr_set[c->device] = true;
   }
-  minplus_sparse_kernel<true, THREADS, UNROLL, UNIFORM>
+  minplus_sparse_kernel<STATS, THREADS, UNROLL, UNIFORM>
       <<<(unsigned)(c->Mp / 4), THREADS, (size_t)(c->Qc + 1) * 8, c->st>>>(c->slot(c->k), c->P, sa, c->slot(knew),
                                                                         epi);
   RD_CUDA_CHECK(cudaGetLastError());
@@ -1640,6 +2025,51 @@ template <int THREADS, int UNROLL>
 static int launch_sparse(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
   return sa.wcol ? launch_sparse_u<THREADS, UNROLL, true>(c, sa, knew, epi)
                  : launch_sparse_u<THREADS, UNROLL, false>(c, sa, knew, epi);
+}
+
+// Slab-layout step: the product (byte slab kernel, or the 16-bit kernel when the current power
+// spreads > 254; both launched, the other exits), then diag and the two-phase periodicity stats.
+static int step_slab(rd_chain *c, int knew, EpiArgs &epi) {
+  SpArgs sa{c->colptr, c->ent, c->nchunks, c->Qc, c->N, c->wcol};
+  epi.spread_in = c->spread + (c->k & 1);
+  epi.spread_out = c->spread + (knew & 1);
+  RD_CUDA_CHECK(cudaMemsetAsync(c->spread + (knew & 1), 0, 4, c->st));
+  static bool attr[64] = {};
+  if (c->device >= 0 && c->device < 64 && !attr[c->device]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_slab8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemMax));
+    attr[c->device] = true;
+  }
+  SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol};
+  minplus_slab8_kernel<<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 1) * 8, c->st>>>(
+      c->slot(c->k), c->P, sb, c->slot(knew), epi.spread_in, epi.spread_out);
+  RD_CUDA_CHECK(cudaGetLastError());
+  EpiArgs fe = epi;
+  fe.stats = nullptr;
+  if (int rc = launch_sparse_u<1024, 2, true, false>(c, sa, knew, fe)) return rc;
+  const uint32_t *X = c->slot(knew);
+  rp_diag_kernel<<<(unsigned)((c->Mr + 255) / 256), 256, 0, c->st>>>(X, c->P, c->Mr, c->r0, c->inv, epi.stats);
+  RD_CUDA_CHECK(cudaGetLastError());
+  if (epi.nprev > 0) {
+    PanelStatsArgs pa{};
+    pa.nprev = epi.nprev;
+    for (int a = 0; a < epi.nprev; ++a) pa.prev[a] = reinterpret_cast<const int16_t *>(epi.prev[a]);
+    const int64_t pairs = c->Mp / 2, nb = (c->N + 127) / 128;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    // a sample of row pairs first (1/32 of the rows), then only the alphas it cannot rule out
+    const bool small = pairs <= 256;
+    const int stride = small ? 1 : 32;
+    const int64_t np = ((pairs + 4LL * stride - 1) / (4LL * stride)) * 4;
+    unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(np * nb, (int64_t)sms * 4));
+    rp_stats_kernel<true><<<grid, 512, 0, c->st>>>(X, c->P, pairs, c->N, stride, pa, epi.stats);
+    RD_CUDA_CHECK(cudaGetLastError());
+    if (!small) {
+      grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(pairs * nb, (int64_t)sms * 4));
+      rp_stats_kernel<false><<<grid, 512, 0, c->st>>>(X, c->P, pairs, c->N, 1, pa, epi.stats);
+      RD_CUDA_CHECK(cudaGetLastError());
+    }
+  }
+  return RD_OK;
 }
 
 extern "C" int rd_set_sparse_variant(int v) {
@@ -1663,6 +2093,9 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
   if (c->wcol) cudaFree(c->wcol);
   if (c->ws) cudaFree(c->ws);
   if (c->spread) cudaFree(c->spread);
+  for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
+                  (void *)c->ent8})
+    if (p) cudaFree(p);
   delete c;
   return RD_OK;
 }
@@ -1687,6 +2120,11 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   epi.diag_row0 = c->r0;
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
+  if (c->method == 1 && c->ent8) {
+    if (int rc = step_slab(c, knew, epi)) return rc;
+    c->k = knew;
+    return RD_OK;
+  }
   if (c->method == 1 && c->spread) {
     // byte kernel (8 rows / CTA) unless the current power's flag says some row spreads > 254,
     // then the 16-bit kernel; both launched, the one not selected exits at once (no host sync)
@@ -1771,7 +2209,7 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
   if (c->method == 0)
     unpack_pm_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->Mp, c->Mr, c->N, d);
   else
-    unpack_rp_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->P, c->Mr, c->N, d);
+    unpack_rp_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->P, c->Mr, c->N, d, c->inv);
   cudaError_t e = cudaMemcpyAsync(host_out, d, (size_t)(c->Mr * c->N * 2), cudaMemcpyDeviceToHost, c->st);
   cudaFreeAsync(d, c->st);
   if (e != cudaSuccess) return fail(RD_ECUDA, "rd_chain_read_rows: %s", cudaGetErrorString(e));

@@ -523,8 +523,8 @@ def test_structured_byte_path_and_fallback(wmax, kmax):
     # column-uniform labels select the byte kernel; wider labels make row spreads cross 254
     # during the chain (wmax=100) or from the start (wmax=300), forcing the 16-bit kernel
     rng = np.random.default_rng(wmax)
-    N = 700
-    pat = rng.random((N, N)) < 0.02
+    N = 2100                      # >= 2048: the default slab layout (smaller N take the 16-bit kernel)
+    pat = rng.random((N, N)) < 0.01
     np.fill_diagonal(pat, True)
     w = rng.integers(0, wmax + 1, size=N)
     A16 = np.where(pat, w[None, :], RINF).astype(np.int16)
@@ -544,20 +544,35 @@ def test_structured_byte_path_and_fallback(wmax, kmax):
         assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
 
 
-def test_structured_bytes_on_off_identical():
+@pytest.mark.parametrize("m,r0,r1", [(7, 0, 2507), (8, 1000, 2999)])
+def test_structured_kernel_modes_identical(m, r0, r1):
+    # slab layout (2, columns permuted, stats after the product from a row sample plus full
+    # passes for survivors), byte kernel (1) and 16-bit kernel (0): the same powers, diag and
+    # per-alpha decisions at every power, past first detection (survivor passes run)
     outs = []
-    for on in (True, False):
-        rd.rd_set_sparse_bytes(on)
+    for mode in (2, 1, 0):
+        rd.rd_set_sparse_bytes(mode)
         try:
-            ch = rd.Chain(8, alpha_max=6, method=1, row_begin=1000, row_end=2999)
-            st = [ch.step().cpu().numpy() for _ in range(8)]
-            outs.append((st, ch.read_rows(9)))
+            ch = rd.Chain(m, alpha_max=6, method=1, row_begin=r0, row_end=r1)
+            diag, dec, rows = [], [], []
+            for k in range(2, 31):
+                s = ch.step().cpu().numpy()
+                diag.append(int(s[0]))
+                dec.append([rd.rd_stats_decide(s, 6, k, only_alpha=a) for a in range(1, min(6, k - 1) + 1)])
+                if k in (3, 9, 30):
+                    rows.append(ch.read_rows(k))
+            outs.append((diag, dec, rows))
             ch.close()
         finally:
-            rd.rd_set_sparse_bytes(True)
-    for a, b in zip(outs[0][0], outs[1][0]):
-        assert (a == b).all()
-    assert (outs[0][1] == outs[1][1]).all()
+            rd.rd_set_sparse_bytes(2)
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        assert o[1] == outs[0][1]
+        for a, b in zip(o[2], outs[0][2]):
+            assert (a == b).all()
+    # the decisions do detect the period (m = 7, 8: alpha = 5 at k = 26 for the full panel)
+    if r0 == 0:
+        assert outs[0][1][26 - 2][5 - 1] == (5, 16)
 
 
 @pytest.mark.parametrize("m,method", [(8, 0), (9, 0), (9, 1)])

@@ -96,6 +96,8 @@ def test_argument_validation_host_paths():
     assert L.rd_roman_cylinder(0, 5, ctypes.byref(g)) == rd.RD_EINVAL
     assert L.rd_minplus_mul(None, None, None, 4) == rd.RD_EINVAL
     assert L.rd_stats_len(10) == 41
+    assert L.rd_set_sparse_bytes(3) == rd.RD_EINVAL and L.rd_set_sparse_bytes(-1) == rd.RD_EINVAL
+    assert L.rd_set_sparse_bytes(2) == rd.RD_OK
 
 
 def test_build_matrix_border_bit_exact():
