@@ -1226,7 +1226,8 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
       }
       xs[q] = make_uint2(__byte_perm(d[0], d[1], 0x6420), __byte_perm(d[2], d[3], 0x6420));
     }
-    if (threadIdx.x == 0) { xs[sa.Qc] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu); next_slab = 0; }
+    if (threadIdx.x < 16) xs[sa.Qc + threadIdx.x] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);   // sentinels
+    if (threadIdx.x == 0) next_slab = 0;
     __syncthreads();
     const int s0 = sa.slab_start[ch], ns = sa.slab_start[ch + 1] - s0;
     const bool last = ch == sa.nchunks - 1;
@@ -1616,21 +1617,112 @@ bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t
     const int64_t T = std::max<int64_t>(256, (maxlen + 31) / 32);
     // lanes of the slab being filled: (column, first entry index, length)
     struct Piece { int32_t col; int64_t b; int32_t len; bool head; };
+    bool colour_ok = true;
     std::vector<Piece> cur;
     auto flush = [&]() {
       if (cur.empty()) return;
+      // per half-warp, schedule the entries into rounds so that no two lanes of the half-warp
+      // read different slots of one bank pair in a round (8-byte slot q uses banks 2q, 2q+1:
+      // class q mod 16): a proper edge colouring of the bipartite multigraph lanes x classes
+      // with Delta colours (Koenig's theorem; alternating-path recolouring)
+      std::vector<std::vector<int32_t>> rounds(32);   // rounds[lane][r] = slot or -1
       int32_t L = 0;
-      for (auto &p : cur) L = std::max(L, p.len);
+      for (int h = 0; h < 2; ++h) {
+        int D = 0;
+        int dv[16] = {0};
+        for (int u = 0; u < 16; ++u) {
+          const int l = 16 * h + u;
+          if (l >= (int)cur.size()) continue;
+          D = std::max(D, (int)cur[l].len);
+          for (int32_t t = 0; t < cur[l].len; ++t) D = std::max(D, ++dv[lists[cur[l].b + t] & 15]);
+        }
+        std::vector<int32_t> cu((size_t)16 * D, -1), cq((size_t)16 * D, -1), cv((size_t)16 * D, -1);
+        auto freeU = [&](int u) { int c = 0; while (cu[(size_t)u * D + c] >= 0) ++c; return c; };
+        auto freeV = [&](int v) { int c = 0; while (cv[(size_t)v * D + c] >= 0) ++c; return c; };
+        struct E { int u, v, c; int32_t q; };
+        std::vector<E> path;
+        for (int u = 0; u < 16; ++u) {
+          const int l = 16 * h + u;
+          if (l >= (int)cur.size()) continue;
+          for (int32_t t = 0; t < cur[l].len; ++t) {
+            const int32_t q = lists[cur[l].b + t];
+            const int v = q & 15;
+            const int a = freeU(u), b = freeV(v);
+            if (cv[(size_t)v * D + a] >= 0) {
+              // swap colours a <-> b along the alternating path from v (a, b, a, ...); it
+              // cannot reach u (bipartite parity), so a becomes free at both ends
+              path.clear();
+              int x = v, c = a;
+              bool onV = true;
+              for (;;) {
+                if (onV) {
+                  const int y = cv[(size_t)x * D + c];
+                  if (y < 0) break;
+                  path.push_back(E{y, x, c, cq[(size_t)y * D + c]});
+                  x = y;
+                } else {
+                  const int y = cu[(size_t)x * D + c];
+                  if (y < 0) break;
+                  path.push_back(E{x, y, c, cq[(size_t)x * D + c]});
+                  x = y;
+                }
+                onV = !onV;
+                c = (c == a) ? b : a;
+              }
+              for (auto &e : path) {
+                cu[(size_t)e.u * D + e.c] = -1;
+                cq[(size_t)e.u * D + e.c] = -1;
+                cv[(size_t)e.v * D + e.c] = -1;
+              }
+              for (auto &e : path) {
+                const int nc = e.c == a ? b : a;
+                cu[(size_t)e.u * D + nc] = e.v;
+                cq[(size_t)e.u * D + nc] = e.q;
+                cv[(size_t)e.v * D + nc] = e.u;
+              }
+            }
+            cu[(size_t)u * D + a] = v;
+            cq[(size_t)u * D + a] = q;
+            cv[(size_t)v * D + a] = u;
+          }
+        }
+        for (int u = 0; u < 16; ++u) {
+          const int l = 16 * h + u;
+          rounds[l].assign((size_t)D, -1);
+          if (l >= (int)cur.size()) continue;
+          int32_t got = 0;
+          for (int c = 0; c < D; ++c) got += (rounds[l][c] = cq[(size_t)u * D + c]) >= 0;
+          if (got != cur[l].len) colour_ok = false;   // every entry scheduled exactly once
+        }
+        L = std::max(L, (int32_t)D);
+      }
       L = (L + 3) / 4 * 4;
       const int64_t off = (int64_t)S.ent8.size();
       S.ent8.resize((size_t)(off + (int64_t)L * 32), pad);
+      for (int h = 0; h < 2; ++h)
+        for (int32_t r = 0; r < L; ++r) {
+          // padding reads the sentinel slot of a class no real entry of the half-warp uses in
+          // this round (slots Qc .. Qc+15 hold inf, one per class)
+          bool used[16] = {false};
+          for (int u = 0; u < 16; ++u) {
+            const auto &R = rounds[16 * h + u];
+            if (r < (int32_t)R.size() && R[r] >= 0) used[R[r] & 15] = true;
+          }
+          int fc = 0;
+          while (fc < 15 && used[fc]) ++fc;
+          const uint32_t sent = (uint32_t)(Qc + ((fc - Qc % 16 + 32) % 16)) * 8u;
+          for (int u = 0; u < 16; ++u) {
+            const int l = 16 * h + u;
+            const auto &R = rounds[l];
+            const bool real = r < (int32_t)R.size() && R[r] >= 0;
+            S.ent8[off + (int64_t)r * 32 + l] = real ? (uint32_t)R[r] * 8u : sent;
+          }
+        }
       uint32_t head = 0;
       for (int l = 0; l < 32; ++l) {
         if (l < (int)cur.size()) {
-          const Piece &p = cur[l];
-          if (p.head) head |= 1u << l;
-          for (int32_t t = 0; t < p.len; ++t) S.ent8[off + (int64_t)t * 32 + l] = (uint32_t)lists[p.b + t] * 8u;
-          S.lane_col.push_back(p.col);
+          if (cur[l].head) head |= 1u << l;
+          S.lane_col.push_back(cur[l].col);
         } else {
           head |= 1u << l;
           S.lane_col.push_back(-1);
@@ -1655,6 +1747,7 @@ bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t
       if (cur.size() == 32) flush();
     }
     flush();
+    if (!colour_ok) return false;
   }
   S.slab_start[nchunks] = (int32_t)(S.desc.size() / 4);
   if (S.ent8.empty()) S.ent8.push_back(pad);
@@ -2039,11 +2132,12 @@ static int step_slab(rd_chain *c, int knew, EpiArgs &epi) {
   RD_CUDA_CHECK(cudaMemsetAsync(c->spread + (knew & 1), 0, 4, c->st));
   static bool attr[64] = {};
   if (c->device >= 0 && c->device < 64 && !attr[c->device]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_slab8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpSmemMax));
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_slab8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSpSmemMax + 16 * 8));
     attr[c->device] = true;
   }
   SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol};
-  minplus_slab8_kernel<<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 1) * 8, c->st>>>(
+  minplus_slab8_kernel<<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 16) * 8, c->st>>>(
       c->slot(c->k), c->P, sb, c->slot(knew), epi.spread_in, epi.spread_out);
   RD_CUDA_CHECK(cudaGetLastError());
   EpiArgs fe = epi;
