@@ -24,6 +24,8 @@
 #include <climits>
 #include <cstdio>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "rd_internal.h"
@@ -1537,6 +1539,114 @@ struct SlabHost {
   std::vector<int32_t> slab_start;        // per chunk, nchunks + 1
 };
 
+// One slab of the slab layout: the lanes' pieces (column, first index into lists, length),
+// scheduled into L rounds (multiple of 4) of bank-conflict-free gathers; out = L x 32 byte
+// offsets (lane-interleaved).  Returns false if some entry was not scheduled exactly once.
+struct SlabPiece { int32_t col; int64_t b; int32_t len; bool head; };
+static bool colour_slab(const std::vector<SlabPiece> &cur, const int32_t *lists, int Qc,
+                        std::vector<uint32_t> &out, int32_t &Lout) {
+  bool colour_ok = true;
+  // per half-warp, schedule the entries into rounds so that no two lanes of the half-warp
+  // read different slots of one bank pair in a round (8-byte slot q uses banks 2q, 2q+1:
+  // class q mod 16): a proper edge colouring of the bipartite multigraph lanes x classes
+  // with Delta colours (Koenig's theorem; alternating-path recolouring)
+  std::vector<std::vector<int32_t>> rounds(32);   // rounds[lane][r] = slot or -1
+  int32_t L = 0;
+  for (int h = 0; h < 2; ++h) {
+    int D = 0;
+    int dv[16] = {0};
+    for (int u = 0; u < 16; ++u) {
+      const int l = 16 * h + u;
+      if (l >= (int)cur.size()) continue;
+      D = std::max(D, (int)cur[l].len);
+      for (int32_t t = 0; t < cur[l].len; ++t) D = std::max(D, ++dv[lists[cur[l].b + t] & 15]);
+    }
+    std::vector<int32_t> cu((size_t)16 * D, -1), cq((size_t)16 * D, -1), cv((size_t)16 * D, -1);
+    auto freeU = [&](int u) { int c = 0; while (cu[(size_t)u * D + c] >= 0) ++c; return c; };
+    auto freeV = [&](int v) { int c = 0; while (cv[(size_t)v * D + c] >= 0) ++c; return c; };
+    struct E { int u, v, c; int32_t q; };
+    std::vector<E> path;
+    for (int u = 0; u < 16; ++u) {
+      const int l = 16 * h + u;
+      if (l >= (int)cur.size()) continue;
+      for (int32_t t = 0; t < cur[l].len; ++t) {
+        const int32_t q = lists[cur[l].b + t];
+        const int v = q & 15;
+        const int a = freeU(u), b = freeV(v);
+        if (cv[(size_t)v * D + a] >= 0) {
+          // swap colours a <-> b along the alternating path from v (a, b, a, ...); it
+          // cannot reach u (bipartite parity), so a becomes free at both ends
+          path.clear();
+          int x = v, c = a;
+          bool onV = true;
+          for (;;) {
+            if (onV) {
+              const int y = cv[(size_t)x * D + c];
+              if (y < 0) break;
+              path.push_back(E{y, x, c, cq[(size_t)y * D + c]});
+              x = y;
+            } else {
+              const int y = cu[(size_t)x * D + c];
+              if (y < 0) break;
+              path.push_back(E{x, y, c, cq[(size_t)x * D + c]});
+              x = y;
+            }
+            onV = !onV;
+            c = (c == a) ? b : a;
+          }
+          for (auto &e : path) {
+            cu[(size_t)e.u * D + e.c] = -1;
+            cq[(size_t)e.u * D + e.c] = -1;
+            cv[(size_t)e.v * D + e.c] = -1;
+          }
+          for (auto &e : path) {
+            const int nc = e.c == a ? b : a;
+            cu[(size_t)e.u * D + nc] = e.v;
+            cq[(size_t)e.u * D + nc] = e.q;
+            cv[(size_t)e.v * D + nc] = e.u;
+          }
+        }
+        cu[(size_t)u * D + a] = v;
+        cq[(size_t)u * D + a] = q;
+        cv[(size_t)v * D + a] = u;
+      }
+    }
+    for (int u = 0; u < 16; ++u) {
+      const int l = 16 * h + u;
+      rounds[l].assign((size_t)D, -1);
+      if (l >= (int)cur.size()) continue;
+      int32_t got = 0;
+      for (int c = 0; c < D; ++c) got += (rounds[l][c] = cq[(size_t)u * D + c]) >= 0;
+      if (got != cur[l].len) colour_ok = false;   // every entry scheduled exactly once
+    }
+    L = std::max(L, (int32_t)D);
+  }
+  L = (L + 3) / 4 * 4;
+  const uint32_t pad = (uint32_t)Qc * 8u;
+  out.assign((size_t)L * 32, pad);
+  for (int h = 0; h < 2; ++h)
+    for (int32_t r = 0; r < L; ++r) {
+      bool used[16] = {false};
+      for (int u = 0; u < 16; ++u) {
+        const auto &R = rounds[16 * h + u];
+        if (r < (int32_t)R.size() && R[r] >= 0) used[R[r] & 15] = true;
+      }
+      int fc = 0;
+      while (fc < 15 && used[fc]) ++fc;
+      // padding reads the inf sentinel (slots Qc .. Qc+15, one per class) of a class no real
+      // entry of the half-warp uses in this round
+      const uint32_t sent = (uint32_t)(Qc + ((fc - Qc % 16 + 32) % 16)) * 8u;
+      for (int u = 0; u < 16; ++u) {
+        const int l = 16 * h + u;
+        const auto &R = rounds[l];
+        const bool real = r < (int32_t)R.size() && R[r] >= 0;
+        out[(size_t)r * 32 + l] = real ? (uint32_t)R[r] * 8u : sent;
+      }
+    }
+  Lout = L;
+  return colour_ok;
+}
+
 // From the natural general-format CSC (entries (q - q0) | w << 17, chunks of Qc).  Returns
 // false if some column mixes labels (then the chain keeps the natural basis).
 bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t> &colptr,
@@ -1607,153 +1717,91 @@ bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t
       const int32_t u0 = S.ucolptr[(size_t)ch * (N + 1) + j];
       for (int64_t t = lp[li]; t < lp[li + 1]; ++t) S.uent[u0 + (t - lp[li])] = (uint32_t)lists[t] * 8u;
     }
-  // slabs
+  // slabs: columns dealt to lanes in order (sequential), each slab scheduled in parallel
   S.desc.clear(); S.lane_col.clear(); S.ent8.clear();
   S.slab_start.assign((size_t)nchunks + 1, 0);
+  std::vector<std::vector<SlabPiece>> slabs;
   for (int ch = 0; ch < nchunks; ++ch) {
-    S.slab_start[ch] = (int32_t)(S.desc.size() / 4);
+    S.slab_start[ch] = (int32_t)slabs.size();
     int64_t maxlen = 0;
     for (int64_t j = 0; j < N; ++j) maxlen = std::max<int64_t>(maxlen, cnt[(size_t)ch * N + j]);
     const int64_t T = std::max<int64_t>(256, (maxlen + 31) / 32);
-    // lanes of the slab being filled: (column, first entry index, length)
-    struct Piece { int32_t col; int64_t b; int32_t len; bool head; };
-    bool colour_ok = true;
-    std::vector<Piece> cur;
-    auto flush = [&]() {
-      if (cur.empty()) return;
-      // per half-warp, schedule the entries into rounds so that no two lanes of the half-warp
-      // read different slots of one bank pair in a round (8-byte slot q uses banks 2q, 2q+1:
-      // class q mod 16): a proper edge colouring of the bipartite multigraph lanes x classes
-      // with Delta colours (Koenig's theorem; alternating-path recolouring)
-      std::vector<std::vector<int32_t>> rounds(32);   // rounds[lane][r] = slot or -1
-      int32_t L = 0;
-      for (int h = 0; h < 2; ++h) {
-        int D = 0;
-        int dv[16] = {0};
-        for (int u = 0; u < 16; ++u) {
-          const int l = 16 * h + u;
-          if (l >= (int)cur.size()) continue;
-          D = std::max(D, (int)cur[l].len);
-          for (int32_t t = 0; t < cur[l].len; ++t) D = std::max(D, ++dv[lists[cur[l].b + t] & 15]);
-        }
-        std::vector<int32_t> cu((size_t)16 * D, -1), cq((size_t)16 * D, -1), cv((size_t)16 * D, -1);
-        auto freeU = [&](int u) { int c = 0; while (cu[(size_t)u * D + c] >= 0) ++c; return c; };
-        auto freeV = [&](int v) { int c = 0; while (cv[(size_t)v * D + c] >= 0) ++c; return c; };
-        struct E { int u, v, c; int32_t q; };
-        std::vector<E> path;
-        for (int u = 0; u < 16; ++u) {
-          const int l = 16 * h + u;
-          if (l >= (int)cur.size()) continue;
-          for (int32_t t = 0; t < cur[l].len; ++t) {
-            const int32_t q = lists[cur[l].b + t];
-            const int v = q & 15;
-            const int a = freeU(u), b = freeV(v);
-            if (cv[(size_t)v * D + a] >= 0) {
-              // swap colours a <-> b along the alternating path from v (a, b, a, ...); it
-              // cannot reach u (bipartite parity), so a becomes free at both ends
-              path.clear();
-              int x = v, c = a;
-              bool onV = true;
-              for (;;) {
-                if (onV) {
-                  const int y = cv[(size_t)x * D + c];
-                  if (y < 0) break;
-                  path.push_back(E{y, x, c, cq[(size_t)y * D + c]});
-                  x = y;
-                } else {
-                  const int y = cu[(size_t)x * D + c];
-                  if (y < 0) break;
-                  path.push_back(E{x, y, c, cq[(size_t)x * D + c]});
-                  x = y;
-                }
-                onV = !onV;
-                c = (c == a) ? b : a;
-              }
-              for (auto &e : path) {
-                cu[(size_t)e.u * D + e.c] = -1;
-                cq[(size_t)e.u * D + e.c] = -1;
-                cv[(size_t)e.v * D + e.c] = -1;
-              }
-              for (auto &e : path) {
-                const int nc = e.c == a ? b : a;
-                cu[(size_t)e.u * D + nc] = e.v;
-                cq[(size_t)e.u * D + nc] = e.q;
-                cv[(size_t)e.v * D + nc] = e.u;
-              }
-            }
-            cu[(size_t)u * D + a] = v;
-            cq[(size_t)u * D + a] = q;
-            cv[(size_t)v * D + a] = u;
-          }
-        }
-        for (int u = 0; u < 16; ++u) {
-          const int l = 16 * h + u;
-          rounds[l].assign((size_t)D, -1);
-          if (l >= (int)cur.size()) continue;
-          int32_t got = 0;
-          for (int c = 0; c < D; ++c) got += (rounds[l][c] = cq[(size_t)u * D + c]) >= 0;
-          if (got != cur[l].len) colour_ok = false;   // every entry scheduled exactly once
-        }
-        L = std::max(L, (int32_t)D);
-      }
-      L = (L + 3) / 4 * 4;
-      const int64_t off = (int64_t)S.ent8.size();
-      S.ent8.resize((size_t)(off + (int64_t)L * 32), pad);
-      for (int h = 0; h < 2; ++h)
-        for (int32_t r = 0; r < L; ++r) {
-          // padding reads the sentinel slot of a class no real entry of the half-warp uses in
-          // this round (slots Qc .. Qc+15 hold inf, one per class)
-          bool used[16] = {false};
-          for (int u = 0; u < 16; ++u) {
-            const auto &R = rounds[16 * h + u];
-            if (r < (int32_t)R.size() && R[r] >= 0) used[R[r] & 15] = true;
-          }
-          int fc = 0;
-          while (fc < 15 && used[fc]) ++fc;
-          const uint32_t sent = (uint32_t)(Qc + ((fc - Qc % 16 + 32) % 16)) * 8u;
-          for (int u = 0; u < 16; ++u) {
-            const int l = 16 * h + u;
-            const auto &R = rounds[l];
-            const bool real = r < (int32_t)R.size() && R[r] >= 0;
-            S.ent8[off + (int64_t)r * 32 + l] = real ? (uint32_t)R[r] * 8u : sent;
-          }
-        }
-      uint32_t head = 0;
-      for (int l = 0; l < 32; ++l) {
-        if (l < (int)cur.size()) {
-          if (cur[l].head) head |= 1u << l;
-          S.lane_col.push_back(cur[l].col);
-        } else {
-          head |= 1u << l;
-          S.lane_col.push_back(-1);
-        }
-      }
-      S.desc.push_back((int32_t)off);
-      S.desc.push_back(L);
-      S.desc.push_back((int32_t)head);
-      S.desc.push_back(0);
-      cur.clear();
-    };
+    std::vector<SlabPiece> cur;
     for (int64_t j = 0; j < N; ++j) {
       const size_t li = (size_t)ch * N + j;
       const int64_t d = cnt[li];
       const int64_t pieces = d <= T ? 1 : (d + T - 1) / T;
-      if ((int64_t)cur.size() + pieces > 32) flush();
+      if ((int64_t)cur.size() + pieces > 32) { slabs.push_back(std::move(cur)); cur.clear(); }
       const int64_t per = pieces == 1 ? d : (d + pieces - 1) / pieces;
       for (int64_t p = 0; p < pieces; ++p) {
         const int64_t b = p * per, e = std::min<int64_t>(d, b + per);
-        cur.push_back(Piece{(int32_t)j, lp[li] + b, (int32_t)std::max<int64_t>(0, e - b), p == 0});
+        cur.push_back(SlabPiece{(int32_t)j, lp[li] + b, (int32_t)std::max<int64_t>(0, e - b), p == 0});
       }
-      if (cur.size() == 32) flush();
+      if (cur.size() == 32) { slabs.push_back(std::move(cur)); cur.clear(); }
     }
-    flush();
-    if (!colour_ok) return false;
+    if (!cur.empty()) slabs.push_back(std::move(cur));
   }
-  S.slab_start[nchunks] = (int32_t)(S.desc.size() / 4);
-  if (S.ent8.empty()) S.ent8.push_back(pad);
+  const int64_t ns = (int64_t)slabs.size();
+  std::vector<std::vector<uint32_t>> sent8((size_t)ns);
+  std::vector<int32_t> sL((size_t)ns, 0);
+  bool all_ok = true;
+#pragma omp parallel for schedule(dynamic, 16) reduction(&& : all_ok)
+  for (int64_t s = 0; s < ns; ++s) all_ok = colour_slab(slabs[s], lists.data(), Qc, sent8[s], sL[s]) && all_ok;
+  if (!all_ok) return false;
+  int64_t total8 = 0;
+  for (int64_t s = 0; s < ns; ++s) total8 += (int64_t)sL[s] * 32;
+  S.ent8.resize((size_t)std::max<int64_t>(total8, 1), pad);
+  S.desc.resize((size_t)ns * 4);
+  S.lane_col.resize((size_t)ns * 32);
+  int64_t off = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    std::copy(sent8[s].begin(), sent8[s].end(), S.ent8.begin() + off);
+    uint32_t head = 0;
+    for (int l = 0; l < 32; ++l) {
+      const bool real = l < (int)slabs[s].size();
+      if (!real || slabs[s][l].head) head |= 1u << l;
+      S.lane_col[(size_t)s * 32 + l] = real ? slabs[s][l].col : -1;
+    }
+    S.desc[(size_t)s * 4 + 0] = (int32_t)off;
+    S.desc[(size_t)s * 4 + 1] = sL[s];
+    S.desc[(size_t)s * 4 + 2] = (int32_t)head;
+    S.desc[(size_t)s * 4 + 3] = 0;
+    off += (int64_t)sL[s] * 32;
+  }
+  S.slab_start[nchunks] = (int32_t)ns;
   return true;
 }
 }  // namespace
+
+// Host slab layout of A(G) for words of length m, built from the successor generator once per
+// process and shared by later chains of the same order (e.g. the row panels of
+// dist.power_sequence_panels: 4 panels at m = 11 rebuilt it for 7 s each).  One entry.
+struct SlabCached {
+  int m = 0, nchunks = 0, Qc = 0;
+  bool border = false;
+  int64_t nnz = 0;
+  std::vector<int16_t> dg;
+  SlabHost S;
+};
+static std::mutex g_slab_mu;
+static std::shared_ptr<const SlabCached> g_slab_cache;
+
+static std::shared_ptr<const SlabCached> slab_cached(int m, bool border, int nchunks, int Qc) {
+  std::lock_guard<std::mutex> lk(g_slab_mu);
+  const auto &g = g_slab_cache;
+  if (g && g->m == m && g->border == border && g->nchunks == nchunks && g->Qc == Qc) return g;
+  g_slab_cache.reset();                                  // release the old layout first
+  auto n = std::make_shared<SlabCached>();
+  n->m = m; n->border = border; n->nchunks = nchunks; n->Qc = Qc;
+  std::vector<int32_t> colptr;
+  std::vector<uint32_t> ent;
+  build_csc_direct(m, border, nchunks, Qc, colptr, ent, n->dg);
+  n->nnz = colptr.back();
+  const int64_t N = (int64_t)n->dg.size();
+  if (!build_slab_layout(N, nchunks, Qc, colptr, ent, n->S)) return nullptr;
+  g_slab_cache = n;
+  return n;
+}
 
 // ================================================================ power chain ==
 struct rd_chain {
@@ -1839,56 +1887,76 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
   if (method == 1) {
     c->nchunks = (int)(((N + 1) * 8 + kSpSmemMax - 1) / kSpSmemMax);
     c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);   // (Qc + 1) * 8 B of shared memory
-    std::vector<int32_t> colptr;
-    std::vector<uint32_t> ent;
-    if (A) {
-      build_csc(A, N, c->nchunks, c->Qc, colptr, ent);
-    } else {
-      std::vector<int16_t> dg;
-      build_csc_direct(m, border, c->nchunks, c->Qc, colptr, ent, dg);
-      for (int64_t p = c->r0; p < c->r1; ++p)
-        if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
-    }
-    c->nnz = colptr.back();
-    std::vector<int16_t> wcol;
     // slab layout (g_sparse_bytes == 2): column-permuted basis, lane-per-column byte kernel
     // (below N = 2048 the step is launch-bound: the single fused 16-bit kernel is fastest,
     // m = 6: 36 vs 55 us)
     const int mode = (g_sparse_bytes == 2 && N < 2048) ? 0 : g_sparse_bytes;
-    bool slab = false;
-    if (mode == 2) {
-      SlabHost S;
-      if (build_slab_layout(N, c->nchunks, c->Qc, colptr, ent, S)) {
-        slab = true;
-        colptr.swap(S.ucolptr);
-        ent.swap(S.uent);
-        wcol.swap(S.wcol);
-        auto up = [&](void **dst, const void *src, size_t bytes) {
-          if ((e = cudaMalloc(dst, bytes)) != cudaSuccess) return false;
-          return (e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->st)) == cudaSuccess;
-        };
-        if (!up((void **)&c->perm, S.perm.data(), S.perm.size() * 4) ||
-            !up((void **)&c->inv, S.inv.data(), S.inv.size() * 4) ||
-            !up((void **)&c->lane_col, S.lane_col.data(), S.lane_col.size() * 4) ||
-            !up((void **)&c->slab_start, S.slab_start.data(), S.slab_start.size() * 4) ||
-            !up((void **)&c->desc, S.desc.data(), S.desc.size() * 4) ||
-            !up((void **)&c->ent8, S.ent8.data(), S.ent8.size() * 4) ||
-            (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
-          return cleanup(fail(RD_ENOMEM, "rd_chain_create: slab layout: %s", cudaGetErrorString(e)));
+    std::vector<int32_t> colptr;
+    std::vector<uint32_t> ent;
+    std::vector<int16_t> wcol;
+    std::shared_ptr<const SlabCached> sc;
+    if (!A && mode == 2) sc = slab_cached(m, border, c->nchunks, c->Qc);
+    const SlabHost *S = nullptr;
+    if (sc) {   // A(G) of words of length m: the host layout is built once per process
+      S = &sc->S;
+      for (int64_t p = c->r0; p < c->r1; ++p)
+        if (sc->dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, sc->dg[p]);
+      c->nnz = sc->nnz;
+    } else {
+      if (A) {
+        build_csc(A, N, c->nchunks, c->Qc, colptr, ent);
+      } else {
+        std::vector<int16_t> dg;
+        build_csc_direct(m, border, c->nchunks, c->Qc, colptr, ent, dg);
+        for (int64_t p = c->r0; p < c->r1; ++p)
+          if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
+      }
+      c->nnz = colptr.back();
+    }
+    std::unique_ptr<SlabHost> own;
+    if (!S && mode == 2) {
+      own.reset(new SlabHost);
+      if (build_slab_layout(N, c->nchunks, c->Qc, colptr, ent, *own)) S = own.get();
+    }
+    const bool slab = S != nullptr;
+    const int32_t *cp_p = colptr.data();
+    const uint32_t *ent_p = ent.data();
+    const int16_t *wcol_p = nullptr;
+    size_t cp_n = colptr.size(), ent_n = ent.size(), wcol_n = 0;
+    if (slab) {
+      cp_p = S->ucolptr.data(); cp_n = S->ucolptr.size();
+      ent_p = S->uent.data(); ent_n = S->uent.size();
+      wcol_p = S->wcol.data(); wcol_n = S->wcol.size();
+      auto up = [&](void **dst, const void *src, size_t bytes) {
+        if ((e = cudaMalloc(dst, bytes)) != cudaSuccess) return false;
+        return (e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->st)) == cudaSuccess;
+      };
+      if (!up((void **)&c->perm, S->perm.data(), S->perm.size() * 4) ||
+          !up((void **)&c->inv, S->inv.data(), S->inv.size() * 4) ||
+          !up((void **)&c->lane_col, S->lane_col.data(), S->lane_col.size() * 4) ||
+          !up((void **)&c->slab_start, S->slab_start.data(), S->slab_start.size() * 4) ||
+          !up((void **)&c->desc, S->desc.data(), S->desc.size() * 4) ||
+          !up((void **)&c->ent8, S->ent8.data(), S->ent8.size() * 4))
+        return cleanup(fail(RD_ENOMEM, "rd_chain_create: slab layout: %s", cudaGetErrorString(e)));
+    } else {
+      // uniform labels (A(G): l(q,p) depends on p only) take the byte kernel (8 rows per CTA);
+      // without it, the 16-bit kernel measured faster on the general format at m = 9 (24.5 vs
+      // 30.0 ms) and slower at m = 10 (762 vs 521 ms), DESIGN.md §5
+      const bool want_uniform = mode || c->nchunks > 1;
+      if (want_uniform && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol)) {
+        cp_p = colptr.data(); cp_n = colptr.size();
+        ent_p = ent.data(); ent_n = ent.size();
+        wcol_p = wcol.data(); wcol_n = wcol.size();
       }
     }
-    // uniform labels (A(G): l(q,p) depends on p only) take the byte kernel (8 rows per CTA);
-    // without it, the 16-bit kernel measured faster on the general format at m = 9 (24.5 vs
-    // 30.0 ms) and slower at m = 10 (762 vs 521 ms), DESIGN.md §5
-    const bool want_uniform = mode || c->nchunks > 1;
-    if (slab || (want_uniform && csc_to_uniform(N, c->nchunks, c->Qc, colptr, ent, wcol))) {
-      if ((e = cudaMalloc((void **)&c->wcol, wcol.size() * 2)) != cudaSuccess ||
-          (e = cudaMemcpyAsync(c->wcol, wcol.data(), wcol.size() * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
+    if (wcol_p) {
+      if ((e = cudaMalloc((void **)&c->wcol, wcol_n * 2)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(c->wcol, wcol_p, wcol_n * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
         return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
       if (mode) {
         int16_t mxl = 0;
-        for (int16_t x : wcol)
-          if (x < RD_INF) mxl = std::max(mxl, x);
+        for (size_t i = 0; i < wcol_n; ++i)
+          if (wcol_p[i] < RD_INF) mxl = std::max(mxl, wcol_p[i]);
         const int init[2] = {0, mxl > 254 ? 1 : 0};   // flags[1] describes A^1 (row spread <= max label)
         if ((e = cudaMalloc((void **)&c->spread, 8)) != cudaSuccess ||
             (e = cudaMemcpyAsync(c->spread, init, 8, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
@@ -1896,14 +1964,13 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
           return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
       }
     }
-    if ((e = cudaMalloc((void **)&c->colptr, colptr.size() * 4)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->ent, ent.size() * 4)) != cudaSuccess ||
+    if ((e = cudaMalloc((void **)&c->colptr, cp_n * 4)) != cudaSuccess ||
+        (e = cudaMalloc((void **)&c->ent, ent_n * 4)) != cudaSuccess ||
         (A && (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess) ||
         (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
       return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
-    if ((e = cudaMemcpyAsync(c->colptr, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st)) !=
-            cudaSuccess ||
-        (e = cudaMemcpyAsync(c->ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
+    if ((e = cudaMemcpyAsync(c->colptr, cp_p, cp_n * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(c->ent, ent_p, ent_n * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
         (A && (e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess))
       return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
     int64_t n = (alpha_max + 1) * c->slot_words;
