@@ -1171,7 +1171,7 @@ minplus_sparse8_kernel(const uint32_t *__restrict__ X, int64_t ld, SpArgs sa, ui
 struct SlabArgs {
   const int4 *desc;        // per slab: entry offset, L (multiple of 4), head mask, 0
   const int32_t *lane_col; // per slab lane: output column j' or -1
-  const uint32_t *ent8;    // lane-interleaved byte offsets
+  const uint32_t *ent8;    // lane-interleaved shared-memory slot pairs (rounds t, t+1)
   const int32_t *slab_start;
   int nchunks, Qc;
   int64_t N;
@@ -1190,7 +1190,6 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
   const int64_t p0 = 4 * (int64_t)blockIdx.x;     // row pairs p0 .. p0+3
   const int64_t N = sa.N;
   uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, mx[4] = {0, 0, 0, 0};
-  const char *xb = reinterpret_cast<const char *>(xs);
   for (int ch = 0; ch < sa.nchunks; ++ch) {
     const int64_t q0 = (int64_t)ch * sa.Qc;
     const int qn = (int)min((int64_t)sa.Qc, N - q0);
@@ -1241,36 +1240,48 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
       const int4 d = __ldg(sa.desc + s0 + s);
       const int col = __ldg(sa.lane_col + (int64_t)(s0 + s) * 32 + lane);
       const uint32_t *ep = sa.ent8 + d.x + lane;
-      uint32_t a[4] = {0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu, 0x00FF00FFu};
+      // Fold without unpacking the bytes: as an unsigned 16-bit lane, (hi << 8 | lo) orders by
+      // hi first, so the high byte of a lane-wise min is the min of the high bytes.  Raw words
+      // give rows 1, 3 (5, 7) in the high bytes, words * 256 (IMAD, fma pipe) rows 0, 2 (4, 6).
+      uint32_t ev0 = 0xFFFFFFFFu, od0 = 0xFFFFFFFFu, ev1 = 0xFFFFFFFFu, od1 = 0xFFFFFFFFu;
       for (int t = 0; t < d.y; t += 4) {
-        const uint32_t o0 = __ldg(ep + (t + 0) * 32), o1 = __ldg(ep + (t + 1) * 32);
-        const uint32_t o2 = __ldg(ep + (t + 2) * 32), o3 = __ldg(ep + (t + 3) * 32);
-        const uint2 v0 = *reinterpret_cast<const uint2 *>(xb + o0);
-        const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + o1);
-        const uint2 v2 = *reinterpret_cast<const uint2 *>(xb + o2);
-        const uint2 v3 = *reinterpret_cast<const uint2 *>(xb + o3);
-        a[0] = __vimin3_s16x2(a[0], __byte_perm(v0.x, 0, 0x4140), __byte_perm(v1.x, 0, 0x4140));
-        a[1] = __vimin3_s16x2(a[1], __byte_perm(v0.x, 0, 0x4342), __byte_perm(v1.x, 0, 0x4342));
-        a[2] = __vimin3_s16x2(a[2], __byte_perm(v0.y, 0, 0x4140), __byte_perm(v1.y, 0, 0x4140));
-        a[3] = __vimin3_s16x2(a[3], __byte_perm(v0.y, 0, 0x4342), __byte_perm(v1.y, 0, 0x4342));
-        a[0] = __vimin3_s16x2(a[0], __byte_perm(v2.x, 0, 0x4140), __byte_perm(v3.x, 0, 0x4140));
-        a[1] = __vimin3_s16x2(a[1], __byte_perm(v2.x, 0, 0x4342), __byte_perm(v3.x, 0, 0x4342));
-        a[2] = __vimin3_s16x2(a[2], __byte_perm(v2.y, 0, 0x4140), __byte_perm(v3.y, 0, 0x4140));
-        a[3] = __vimin3_s16x2(a[3], __byte_perm(v2.y, 0, 0x4342), __byte_perm(v3.y, 0, 0x4342));
+        const uint32_t w01 = __ldg(ep + (t / 2) * 32), w23 = __ldg(ep + (t / 2 + 1) * 32);
+        const uint2 v0 = xs[w01 & 0xFFFFu], v1 = xs[w01 >> 16];
+        const uint2 v2 = xs[w23 & 0xFFFFu], v3 = xs[w23 >> 16];
+        od0 = __vimin3_u16x2(od0, v0.x, v1.x);
+        od1 = __vimin3_u16x2(od1, v0.y, v1.y);
+        ev0 = __vimin3_u16x2(ev0, v0.x * 256u, v1.x * 256u);
+        ev1 = __vimin3_u16x2(ev1, v0.y * 256u, v1.y * 256u);
+        od0 = __vimin3_u16x2(od0, v2.x, v3.x);
+        od1 = __vimin3_u16x2(od1, v2.y, v3.y);
+        ev0 = __vimin3_u16x2(ev0, v2.x * 256u, v3.x * 256u);
+        ev1 = __vimin3_u16x2(ev1, v2.y * 256u, v3.y * 256u);
       }
       const uint32_t head = (uint32_t)d.z;
       if (head != 0xFFFFFFFFu) {   // split columns: segmented min towards each segment's head
         const uint32_t above = head & ~((2u << lane) - 1u);
         const int segend = above ? __ffs(above) - 1 : 32;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const uint32_t u = __shfl_down_sync(0xffffffffu, a[r], o);
-            if (lane + o < segend) a[r] = __vmins2(a[r], u);
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u0 = __shfl_down_sync(0xffffffffu, ev0, o), u1 = __shfl_down_sync(0xffffffffu, od0, o);
+          const uint32_t u2 = __shfl_down_sync(0xffffffffu, ev1, o), u3 = __shfl_down_sync(0xffffffffu, od1, o);
+          if (lane + o < segend) {
+            ev0 = __vminu2(ev0, u0); od0 = __vminu2(od0, u1);
+            ev1 = __vminu2(ev1, u2); od1 = __vminu2(od1, u3);
           }
+        }
       }
       if (col < 0 || !((head >> lane) & 1u)) continue;
+      // high bytes -> row pairs (2r, 2r+1) as s16x2 byte offsets, 255 = inf
+      uint32_t a[4];
+      {
+        const uint32_t e0 = (ev0 >> 8) & 0x00FF00FFu, q0 = (od0 >> 8) & 0x00FF00FFu;
+        const uint32_t e1 = (ev1 >> 8) & 0x00FF00FFu, q1 = (od1 >> 8) & 0x00FF00FFu;
+        a[0] = __byte_perm(e0, q0, 0x5410);
+        a[1] = __byte_perm(e0, q0, 0x7632);
+        a[2] = __byte_perm(e1, q1, 0x5410);
+        a[3] = __byte_perm(e1, q1, 0x7632);
+      }
       const uint32_t wl = (uint16_t)__ldg(sa.wcol + col);
       const uint32_t w2 = wl | (wl << 16);
 #pragma unroll
@@ -1526,8 +1537,8 @@ bool csc_to_uniform(int64_t N, int nchunks, int Qc, std::vector<int32_t> &colptr
 // periodicity test are invariant).  Per q'-chunk the columns j' are dealt to
 // warp lanes in order, 32 per slab; a column longer than T is split over adjacent lanes of one
 // slab (segments, folded by a segmented shuffle min).  Entries are stored lane-interleaved,
-// ent8[off + t*32 + lane] = byte offset ql*8 of the t-th entry of that lane (Qc*8 = padding),
-// so a warp reads one coalesced 128-byte line per t.
+// ent8[off + (t/2)*32 + lane] = the slots ql of that lane's entries in rounds t and t+1 as two
+// u16 (Qc .. Qc+15 = inf padding), so a warp reads one coalesced 128-byte line per two rounds.
 struct SlabHost {
   std::vector<int32_t> perm, inv;         // new column -> state, state -> new column
   std::vector<int32_t> ucolptr;           // uniform CSC in the new basis (16-bit fallback kernel)
@@ -1748,14 +1759,18 @@ bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t
 #pragma omp parallel for schedule(dynamic, 16) reduction(&& : all_ok)
   for (int64_t s = 0; s < ns; ++s) all_ok = colour_slab(slabs[s], lists.data(), Qc, sent8[s], sL[s]) && all_ok;
   if (!all_ok) return false;
-  int64_t total8 = 0;
-  for (int64_t s = 0; s < ns; ++s) total8 += (int64_t)sL[s] * 32;
-  S.ent8.resize((size_t)std::max<int64_t>(total8, 1), pad);
+  // two rounds per word: slot indices (byte offset / 8, < Qc + 16 <= 27664) of rounds t, t+1
+  int64_t total2 = 0;
+  for (int64_t s = 0; s < ns; ++s) total2 += (int64_t)sL[s] * 16;
+  S.ent8.resize((size_t)std::max<int64_t>(total2, 1), (pad / 8) * 0x10001u);
   S.desc.resize((size_t)ns * 4);
   S.lane_col.resize((size_t)ns * 32);
   int64_t off = 0;
   for (int64_t s = 0; s < ns; ++s) {
-    std::copy(sent8[s].begin(), sent8[s].end(), S.ent8.begin() + off);
+    for (int32_t r = 0; r < sL[s]; r += 2)
+      for (int l = 0; l < 32; ++l)
+        S.ent8[off + (int64_t)(r / 2) * 32 + l] =
+            (sent8[s][(size_t)r * 32 + l] >> 3) | ((sent8[s][(size_t)(r + 1) * 32 + l] >> 3) << 16);
     uint32_t head = 0;
     for (int l = 0; l < 32; ++l) {
       const bool real = l < (int)slabs[s].size();
@@ -1766,7 +1781,7 @@ bool build_slab_layout(int64_t N, int nchunks, int Qc, const std::vector<int32_t
     S.desc[(size_t)s * 4 + 1] = sL[s];
     S.desc[(size_t)s * 4 + 2] = (int32_t)head;
     S.desc[(size_t)s * 4 + 3] = 0;
-    off += (int64_t)sL[s] * 32;
+    off += (int64_t)sL[s] * 16;
   }
   S.slab_start[nchunks] = (int32_t)ns;
   return true;
