@@ -31,7 +31,7 @@ DPX_MINPLUS_PER_CLK_SM = 128      # VIADDMNMX.S16x2 at half rate: 64 lanes x 2 (
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 33863033600}   # profiles/r01e_gemm_ncu_summary.txt: 32.883 GB read + 0.980 GB write
+TRAFFIC = {9: 35323029888}   # profiles/r01i_gemm_ncu_summary.txt: 34.342 GB read + 0.981 GB write
 
 
 def parse():
