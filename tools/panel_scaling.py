@@ -11,13 +11,15 @@ import paper_2409_17658_b200 as rd  # noqa: E402
 from paper_2409_17658_b200 import dist as D  # noqa: E402
 
 out = {}
-for m in [int(x) for x in sys.argv[1:]] or [8, 9]:
+# arguments: orders, "10s" = the structured step only
+for arg in sys.argv[1:] or ["8", "9"]:
+    m, methods = (int(arg[:-1]), (1,)) if arg.endswith("s") else (int(arg), (0, 1))
     N = rd.count_words(m)
     t1 = None
     for p in (1, 2, 4, 8):
         # the slowest rank holds the largest panel
         r0, r1 = max((D.panel_bounds(N, p, r) for r in range(p)), key=lambda b: b[1] - b[0])
-        for method in (0, 1):
+        for method in methods:
             ch = rd.Chain(m, alpha_max=10, row_begin=r0, row_end=r1, method=method)
             for _ in range(3):
                 ch.step()
