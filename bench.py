@@ -28,6 +28,11 @@ PAPER_K80_GOPS = {6: 99.6, 7: 156.9, 8: 143.1, 9: 166.2}   # BASELINE.md §1.1 (
 SM_COUNT = 148
 NNZ = {1: 7, 2: 33, 3: 167, 4: 836, 5: 4195, 6: 21043, 7: 105566, 8: 529584, 9: 2656733, 10: 13327868}  # nnz A(G)
 DPX_MINPLUS_PER_CLK_SM = 128      # VIADDMNMX.S16x2 at half rate: 64 lanes x 2 (measured)
+# Unit-count bound of the (min,+) term over every instruction form the GEMM can use (DESIGN.md
+# §5): alu and fma pipes 2 warp-instr/clk/SM each (rt_SMSP = 2, B300_MICROARCH "Pipe rates"),
+# issue 4/clk/SM.  DPX VIADDMNMX.S16x2 = 2 terms on alu; IMAD packed add (fma) x2 + VIMNMX3
+# (alu) = 4 terms.  Best mix 1 DPX : 1 (2 IMAD + VIMNMX3) per SMSP-pair slot -> 64 + 128 terms.
+PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
@@ -287,7 +292,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
     # roofline of the dominant kernel (the GEMM): algorithmic ops per launch / launch time
     ops_launch = float(r1 - r0) * N * N
     achieved = ops_launch / gemm_s / 1e9 if gemm_s > 0 else 0.0
-    peak = SM_COUNT * DPX_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
+    peak = SM_COUNT * PIPE_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
+    dpx_peak = SM_COUNT * DPX_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
     mix_peak = SM_COUNT * probe["mixed_minplus_per_clk_sm"] * SM_MAX_MHZ * 1e6 / 1e9
     if chain is not None:
         chain.close()
@@ -421,7 +427,10 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
                          "frac": round(achieved / peak, 4), "traffic": TRAFFIC.get(m),
                          "kernel": "minplus_gemm_kernel<PM,STATS,3>",
-                         "peak_basis": "DPX issue peak: 148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2 at 2 warp-instr/clk/SM, measured) x 1965 MHz",
+                         "peak_basis": "unit-count bound: 148 SMs x 192 (min,+)/clk/SM x 1965 MHz (alu 2 + fma 2 warp-instr/clk/SM, issue 4; "
+                                       "best mix 1 VIADDMNMX.S16x2 : 1 [2 IMAD + 1 VIMNMX3.S16x2]; DESIGN.md 5)",
+                         "dpx_issue_peak": round(dpx_peak, 1), "frac_of_dpx_issue_peak": round(achieved / dpx_peak, 4),
+                         "dpx_issue_peak_basis": "DPX-only: 148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2 at 2 warp-instr/clk/SM, measured) x 1965 MHz",
                          "mix_ceiling": round(mix_peak, 1), "frac_of_mix_ceiling": round(achieved / mix_peak, 4),
                          "mix_ceiling_basis": "register-tile probe of the GEMM's DPX+IMAD/VIMNMX3 mix (rd_alu_probe, live) x 148 SMs x 1965 MHz",
                          "probe": {k: round(v, 2) for k, v in probe.items()}},
