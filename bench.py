@@ -7,7 +7,7 @@ periodicity stats (a2-a4), the stats all_reduce(MIN) across ranks, the device->h
 of the stats and the host decision (a5).  The right operand A is packed once before the
 timed region (a1).  One process per GPU; ranks own 128-row panels of the output.
 
-    python bench.py [--gpus N --steps K --warmup W] [--order-m 9] [--form replicated|allgather] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--order-m 9] [--form replicated|allgather|peer] [--impl reference]
 
 Prints ONE JSON line on rank 0 (contract in DESIGN.md §Measurement).
 """
@@ -55,9 +55,11 @@ def parse():
     p.add_argument("--oracle-ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--gops-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--ttp-structured-only-m", type=int, nargs="*", default=[10])
-    p.add_argument("--form", default="replicated", choices=["replicated", "allgather"],
+    p.add_argument("--form", default="replicated", choices=["replicated", "allgather", "peer"],
                    help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
-                        "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step")
+                        "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step; "
+                        "peer: A^k = A (x) A^(k-1) with the GEMM reading A^(k-1) from every rank's ring "
+                        "(CUDA IPC / NVLink peer memory, the gather fused into the product)")
     return p.parse_args()
 
 
@@ -196,7 +198,12 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
     r0, r1 = rdist.panel_bounds(N, world, rank)
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        if world > 1 and args.form == "replicated":
+        if args.form == "peer":
+            # fused all-gather: each rank's GEMM reads A^(k-1) from every rank's ring (CUDA IPC)
+            chain = rdist.peer_chain(m, am, stream=stream)
+            if world > 1:
+                dist.barrier()
+        elif world > 1 and args.form == "replicated":
             # A(G) built and packed once on rank 0, broadcast over NVLink (not rebuilt per rank)
             chain = rdist.broadcast_chain(m, am, r0, r1)
         else:
@@ -425,8 +432,9 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                        "l2": "operands (2N^2 B = %.0f MB each) exceed L2; no flush" % (2 * N * N / 1e6),
                        "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
-                         "frac": round(achieved / peak, 4), "traffic": TRAFFIC.get(m),
-                         "kernel": "minplus_gemm_kernel<PM,STATS,3>",
+                         "frac": round(achieved / peak, 4), "traffic": TRAFFIC.get(m) if args.form == "replicated" else None,
+                         "kernel": "minplus_gemm_kernel<RP,STATS,3> (peer B)" if args.form == "peer"
+                                   else "minplus_gemm_kernel<PM,STATS,3>",
                          "peak_basis": "unit-count bound: 148 SMs x 192 (min,+)/clk/SM x 1965 MHz (alu 2 + fma 2 warp-instr/clk/SM, issue 4; "
                                        "best mix 1 VIADDMNMX.S16x2 : 1 [2 IMAD + 1 VIMNMX3.S16x2]; DESIGN.md 5)",
                          "dpx_issue_peak": round(dpx_peak, 1), "frac_of_dpx_issue_peak": round(achieved / dpx_peak, 4),

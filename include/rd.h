@@ -264,6 +264,45 @@ int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, 
                     int32_t *beta);
 
 /* ---------------------------------------------------------------------------
+ * Peer all-gather chain — the north star's all-gather form with the gather inside the
+ * product.  A^{k+1} = A (x) A^k (powers of A commute); rank r of
+ * `world` owns rows R_r = [bounds[r], bounds[r+1]) of every power and the fixed left operand
+ * A[R_r, :].  Each step's GEMM reads the right operand A^k straight from every rank's ring
+ * slot (its own, and the peers' through CUDA IPC mappings, i.e. NVLink peer memory on a
+ * multi-GPU node), 64 k-pairs per pipeline stage: no gather buffer, no copy kernel, and the
+ * transfer of power k overlaps the product of power k+1 tile by tile.
+ *
+ * Ordering contract (the caller's): every rank's step k must have completed before any rank
+ * enqueues step k+1.  The per-step stats all_reduce(MIN) provides it (NCCL on the chain's
+ * stream, or a host-synchronised gloo reduce); ring slots are reused only alpha_max+1 steps
+ * later, so no extra barrier is needed.
+ *
+ *   bounds   HOST int64[world+1]: 0 = bounds[0] < bounds[1] < ... < bounds[world] = N = C_m,
+ *            every bounds[s] (s < world) a multiple of 128.  world <= 16.
+ *   Errors: RD_EINVAL (bad bounds / ranks / handles), RD_ENOMEM, RD_ECUDA (IPC open).
+ */
+#define RD_IPC_HANDLE_BYTES 64
+typedef struct rd_agchain rd_agchain;
+int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, int world, int rank, void *cuda_stream,
+                      rd_agchain **out);
+int rd_agchain_destroy(rd_agchain *c);
+/* This rank's ring as a CUDA IPC handle (RD_IPC_HANDLE_BYTES bytes written to handle_out) and
+ * the u32 words of one ring slot, for exchange with the peers (e.g. all_gather_object). */
+int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int64_t *slot_words);
+/* This rank's ring as a device pointer of this process (for peers in the same process). */
+int rd_agchain_ring(const rd_agchain *c, const void **ring_dev, int64_t *slot_words);
+/* Registers rank s's ring: opened from its IPC handle (ipc_handle != NULL, another process),
+ * or a device pointer valid in this process (ipc_handle == NULL).  s == own rank: no-op. */
+int rd_agchain_set_peer(rd_agchain *c, int s, const void *ipc_handle, const void *ring_dev, int64_t slot_words);
+/* Rows R_r of A^{k+1} into the ring with the fused stats of rd_chain_step (same layout,
+ * MIN-reducible).  Requires every peer registered.  Asynchronous on the chain's stream. */
+int rd_agchain_step(rd_agchain *c, int32_t *stats_dev);
+/* Rows R_r of A^k to host int16 row-major (|R_r| x N); synchronises the chain's stream. */
+int rd_agchain_read_rows(rd_agchain *c, int k, int16_t *host_out);
+int32_t rd_agchain_diag1(const rd_agchain *c);
+int64_t rd_agchain_order(const rd_agchain *c);
+
+/* ---------------------------------------------------------------------------
  * rd_set_gemm_variant — tuning knob of the GEMM mainloop (process-wide, not thread-safe;
  * set it before launching work).  dpx_cols in {0, 2, 3, 4, 8}: of each thread's 8
  * accumulator columns, that many use one VIADDMNMX.S16x2 (alu pipe) per k-pair; the rest

@@ -83,6 +83,18 @@ def lib():
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_sparse_bytes.argtypes = [ci]
+        L.rd_agchain_create.argtypes = [ci, ci, p, ci, ci, p, p]
+        L.rd_agchain_destroy.argtypes = [p]
+        L.rd_agchain_ipc_handle.argtypes = [p, p, p]
+        L.rd_agchain_set_peer.argtypes = [p, ci, p, p, i64]
+        L.rd_agchain_ring.argtypes = [p, p, p]
+        L.rd_agchain_step.argtypes = [p, p]
+        L.rd_agchain_read_rows.argtypes = [p, ci, p]
+        L.rd_agchain_diag1.argtypes = [p]; L.rd_agchain_diag1.restype = i32
+        L.rd_agchain_order.argtypes = [p]; L.rd_agchain_order.restype = i64
+        for f in ("rd_agchain_create", "rd_agchain_destroy", "rd_agchain_ipc_handle", "rd_agchain_set_peer", "rd_agchain_ring",
+                  "rd_agchain_step", "rd_agchain_read_rows"):
+            getattr(L, f).restype = ci
         for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
                   "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
@@ -372,6 +384,76 @@ class Chain:
     def close(self):
         if getattr(self, "_h", None):
             lib().rd_chain_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+RD_IPC_HANDLE_BYTES = 64
+
+
+class AgChain:
+    """Rows [bounds[rank], bounds[rank+1]) of every power of A(G) in the peer all-gather form
+    (rd_agchain_*): A^{k+1} = A (x) A^k with A^k read from every rank's ring inside the GEMM.
+    Register the other ranks with set_peer (IPC handle from another process, or a device
+    pointer of this process) before the first step."""
+
+    def __init__(self, m: int, bounds, rank: int, alpha_max: int = 10, stream=None):
+        import torch
+        _sync_device()
+        self.m, self.alpha_max, self.rank = m, alpha_max, rank
+        self.bounds = [int(b) for b in bounds]
+        self.world = len(self.bounds) - 1
+        self.row_begin, self.row_end = self.bounds[rank], self.bounds[rank + 1]
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        b = np.ascontiguousarray(self.bounds, dtype=np.int64)
+        h = ctypes.c_void_p()
+        _check(lib().rd_agchain_create(m, alpha_max, _np_ptr(b), self.world, rank, _stream_ptr(self.stream),
+                                       ctypes.byref(h)))
+        self._h = h
+        self.N = lib().rd_agchain_order(h)
+        self.stats = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device="cuda")
+
+    def ipc_handle(self):
+        """(handle bytes, slot words) of this rank's ring, to send to the peers."""
+        buf = ctypes.create_string_buffer(RD_IPC_HANDLE_BYTES)
+        words = ctypes.c_int64()
+        _check(lib().rd_agchain_ipc_handle(self._h, ctypes.cast(buf, ctypes.c_void_p), ctypes.byref(words)))
+        return buf.raw, words.value
+
+    def ring(self):
+        """(device pointer, slot words) of this rank's ring, for peers in the same process."""
+        ptr, words = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib().rd_agchain_ring(self._h, ctypes.byref(ptr), ctypes.byref(words)))
+        return ptr.value, words.value
+
+    def set_peer(self, s: int, handle: bytes | None = None, ring_ptr: int | None = None,
+                 slot_words: int = 0):
+        hb = ctypes.create_string_buffer(handle, RD_IPC_HANDLE_BYTES) if handle is not None else None
+        _check(lib().rd_agchain_set_peer(self._h, s, ctypes.cast(hb, ctypes.c_void_p) if hb is not None else None,
+                                         ctypes.c_void_p(ring_ptr) if ring_ptr else None, slot_words))
+
+    @property
+    def diag1(self) -> int:
+        return lib().rd_agchain_diag1(self._h)
+
+    def step(self, stats=None):
+        s = self.stats if stats is None else stats
+        _check(lib().rd_agchain_step(self._h, ctypes.c_void_p(s.data_ptr())))
+        return s
+
+    def read_rows(self, k: int) -> np.ndarray:
+        out = np.empty((self.row_end - self.row_begin, self.N), dtype=np.int16)
+        _check(lib().rd_agchain_read_rows(self._h, k, _np_ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rd_agchain_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -201,8 +201,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // 8 x 8 register micro-tile: rows {ty*4 + 0..3, 64 + ty*4 + 0..3}, columns
 // {tx*4 + 0..3, 64 + tx*4 + 0..3}.  Per k-pair a thread reads 4 x LDS.128 and issues 64
 // VIADDMNMX.S16x2 (128 (min,+) terms).
-//   OUT_PM = true : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
-//   OUT_PM = false: C is row-major int16 with ldc, predicated to (M, N).
+//   OUT = kOutPM : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
+//   OUT = kOutRow: C is row-major int16 with ldc, predicated to (M, N).
+//   OUT = kOutRP : C is RP u32 [M/2][ldc] (pairs along i: C[2p][j] | C[2p+1][j] << 16), and the
+//                  right operand is read straight from the ranks' memory (PeerB): k-pairs
+//                  [t0[s], t0[s+1]) of B live at base[s] (the packed layout, pitch ldb), e.g.
+//                  peer GPUs' ring slots mapped over NVLink (CUDA IPC).  Each 64-k-pair stage
+//                  lies inside one rank's range (ranges are whole 128-row tiles), so the
+//                  all-gather of B happens inside the mainloop's cp.async pipeline, tile by tile.
 //
 // Two instruction forms share the mainloop: for accumulator columns
 // c < DPXC each k-pair costs one VIADDMNMX.S16x2 (alu pipe); for c >= DPXC two k-pairs
@@ -212,11 +218,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // equal to 1, opaque to the compiler so that the add stays an IMAD.
 // Tiles are rasterised in groups of kGroup row-tiles so CTAs resident together share
 // right-operand panels in L2.
-template <bool OUT_PM, bool STATS, int DPXC>
+constexpr int kOutRow = 0, kOutPM = 1, kOutRP = 2;
+constexpr int kMaxPeers = 16;
+struct PeerB {
+  const uint32_t *base[kMaxPeers];  // rank s: packed rows of B for k-pairs [t0[s], t0[s+1])
+  int32_t t0[kMaxPeers + 1];
+  int n;
+};
+
+template <int OUT, bool STATS, int DPXC>
 __global__ void __launch_bounds__(kThreads, 2)
 minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
                     int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
-                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup) {
+                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int tid = threadIdx.x;
   // a warp covers 4 (ty) x 8 (tx) threads of the 16 x 16 grid: its fragment loads touch 4 and 8
@@ -243,11 +257,20 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   auto load_stage = [&](int stage, int kb) {
     uint32_t *sx = smem + stage * kStageWords;
     uint32_t *sb = sx + kBK2 * kTile;
-    const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
+    const int64_t ox = (int64_t)kb * kBK2 * ldx;
+    const uint32_t *gbk;
+    if constexpr (OUT == kOutRP) {   // the rank holding k-pairs [kb * kBK2, +kBK2)
+      const int tk = kb * kBK2;
+      int s = 0;
+      while (s + 1 < pb.n && tk >= pb.t0[s + 1]) ++s;
+      gbk = pb.base[s] + (int64_t)(tk - pb.t0[s] + ld_row) * ldb + j0 + ld_col;
+    } else {
+      gbk = gb + (int64_t)kb * kBK2 * ldb;
+    }
 #pragma unroll
     for (int r = 0; r < kBK2; r += 8) {
       cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
-      cp_async16(sb + (ld_row + r) * kTile + ld_col, gb + ob + (r / 8) * gb_step8);
+      cp_async16(sb + (ld_row + r) * kTile + ld_col, gbk + (r / 8) * gb_step8);
     }
   };
 
@@ -340,7 +363,24 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
     }
 
-  if (OUT_PM) {
+  // RP word (rows 2q', 2q'+1 of row group g; columns h*64 + tx*4 + e) from the folded pairs
+  auto rp_word = [&](int g, int q, int h, int e) -> uint32_t {
+    const uint32_t a = out[g * 4 + 2 * q][2 * h + (e >> 1)], b = out[g * 4 + 2 * q + 1][2 * h + (e >> 1)];
+    return prmt(a, b, (e & 1) ? 0x7632 : 0x5410);
+  };
+  if constexpr (OUT == kOutRP) {
+    uint32_t *C = reinterpret_cast<uint32_t *>(Cv);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
+          const uint4 v = make_uint4(rp_word(g, q, h, 0), rp_word(g, q, h, 1), rp_word(g, q, h, 2), rp_word(g, q, h, 3));
+          *reinterpret_cast<uint4 *>(C + pr * ldc + j0 + h * 64 + tx * 4) = v;
+        }
+  } else if constexpr (OUT == kOutPM) {
     uint32_t *C = reinterpret_cast<uint32_t *>(Cv) + (int64_t)blockIdx.y * epi.split_stride;
 #pragma unroll
     for (int g = 0; g < 2; ++g)
@@ -402,16 +442,31 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   for (int a = 0; a < epi.nprev; ++a) {
     const uint32_t *P = epi.prev[a];
     uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+    if constexpr (OUT == kOutRP) {
 #pragma unroll
-    for (int g = 0; g < 2; ++g)
+      for (int g = 0; g < 2; ++g)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-        uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
-        const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+        for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
-      }
+          for (int h = 0; h < 2; ++h) {
+            const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
+            const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + pr * ldc + j0 + h * 64 + tx * 4));
+            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) stats_pair(rp_word(g, q, h, e), pw[e], lo2, hi2, mis, fin);
+          }
+    } else {
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+          uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
+          const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
+        }
+    }
     int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
     int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
     if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
@@ -516,21 +571,21 @@ int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel
 // 12 -> 41.3, 16 -> 47.4, 24 -> 68.5, 32 -> 85.8 GB, the same 276 ms
 int g_raster_group = kGroup;
 
-template <bool OUT_PM, bool STATS, int DPXC>
+template <int OUT, bool STATS, int DPXC>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                  cudaStream_t st, int nsplit) {
+                  cudaStream_t st, int nsplit, const PeerB &pb) {
   static bool attr_set[64] = {};
   int dev = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT_PM, STATS, DPXC>,
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
-  minplus_gemm_kernel<OUT_PM, STATS, DPXC><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads, kSmemBytes, st>>>(
-      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group);
+  minplus_gemm_kernel<OUT, STATS, DPXC><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads, kSmemBytes, st>>>(
+      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
 }
@@ -539,7 +594,8 @@ template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
                 cudaStream_t st, int nsplit = 1) {
-#define RD_LG(D) launch_gemm_v<OUT_PM, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit)
+  const PeerB pb{};
+#define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
   switch (g_dpx_cols) {
     case 0: return RD_LG(0);
     case 2: return RD_LG(2);
@@ -1400,8 +1456,8 @@ __global__ void scatter_dense_operands_kernel(const int32_t *__restrict__ colptr
   for (int t = colptr[j]; t < colptr[j + 1]; ++t) {
     const int64_t q = ent[t] & 0x1FFFFu;
     const uint16_t w = (uint16_t)(ent[t] >> 17);
-    hb[((q >> 1) * ldp + j) * 2 + (q & 1)] = w;
-    if (q >= r0 && q < r1) hx[((j >> 1) * ldt + (q - r0)) * 2 + (j & 1)] = w;
+    if (BP) hb[((q >> 1) * ldp + j) * 2 + (q & 1)] = w;
+    if (XT && q >= r0 && q < r1) hx[((j >> 1) * ldt + (q - r0)) * 2 + (j & 1)] = w;
   }
 }
 
@@ -2395,6 +2451,213 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
   RD_CUDA_CHECK(cudaStreamSynchronize(c->st));
   return RD_OK;
 }
+
+// ======================================================= peer all-gather chain ==
+// The north star's all-gather form with the gather fused into the product:
+// A^{k+1} = A (x) A^k (powers of A commute), rank r owns rows R_r = [b_r, b_{r+1}) of
+// every power and keeps the fixed left operand A[R_r, :] (PM).  Its rows of A^k sit in its
+// ring in RP layout, which is exactly the packed right-operand layout of k-pairs
+// [b_r/2, b_{r+1}/2); the GEMM (OUT = kOutRP) reads every rank's slot of A^k directly through
+// CUDA IPC mappings (NVLink peer memory), stage by stage, so power k+1 consumes the panels of
+// power k while they stream in — no gather buffer and no separate copy.  The only
+// synchronisation is the per-step stats all_reduce(MIN), which orders every rank's step k
+// before any rank's step k+1 (rd.h rd_agchain_step).
+struct rd_agchain {
+  int m = 0, alpha_max = 0, k = 0, device = 0, world = 0, rank = 0;
+  int64_t N = 0, P = 0, r0 = 0, r1 = 0, Mr = 0, Mp = 0, slot_words = 0;
+  cudaStream_t st = nullptr;
+  uint32_t *XL = nullptr;    // A[R_r, :] in PM layout, [P/2][Mp]
+  uint32_t *ring = nullptr;  // (alpha_max+1) RP slots [Mp/2][P] of rows R_r
+  int32_t diag1 = INT32_MAX;
+  std::vector<int64_t> bounds;
+  std::vector<const uint32_t *> peer_ring;
+  std::vector<int64_t> peer_slot_words;
+  std::vector<void *> ipc_mapped;
+  uint32_t *slot(int kk) const { return ring + (int64_t)(kk % (alpha_max + 1)) * slot_words; }
+};
+
+extern "C" int rd_agchain_destroy(rd_agchain *c) {
+  if (!c) return RD_OK;
+  for (void *p : c->ipc_mapped)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (c->XL) cudaFree(c->XL);
+  if (c->ring) cudaFree(c->ring);
+  delete c;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, int world, int rank, void *cuda_stream,
+                                 rd_agchain **out) {
+  rd_enter();
+  NvtxRange nvtx_range("rd_agchain_create");
+  if (!out || !bounds) return fail(RD_EINVAL, "rd_agchain_create: NULL argument");
+  *out = nullptr;
+  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_agchain_create: m=%d out of range", m);
+  if (alpha_max < 1 || alpha_max > kMaxAlpha) return fail(RD_EINVAL, "rd_agchain_create: alpha_max out of 1..32");
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(RD_EINVAL, "rd_agchain_create: world=%d rank=%d (world <= %d)", world, rank, kMaxPeers);
+  const int64_t N = count_words(m);
+  if (bounds[0] != 0 || bounds[world] != N)
+    return fail(RD_EINVAL, "rd_agchain_create: bounds must run from 0 to N=%lld", (long long)N);
+  for (int s = 0; s < world; ++s)
+    if (bounds[s + 1] <= bounds[s] || bounds[s] % kTile != 0)
+      return fail(RD_EINVAL, "rd_agchain_create: panel %d = [%lld, %lld) must be non-empty and start on a %d-row tile",
+                  s, (long long)bounds[s], (long long)bounds[s + 1], kTile);
+  rd_agchain *c = new rd_agchain;
+  c->m = m; c->alpha_max = alpha_max; c->world = world; c->rank = rank; c->N = N;
+  c->bounds.assign(bounds, bounds + world + 1);
+  c->r0 = bounds[rank]; c->r1 = bounds[rank + 1]; c->Mr = c->r1 - c->r0;
+  c->P = round_up(N, kTile);
+  c->Mp = round_up(c->Mr, kTile);
+  c->slot_words = (c->Mp / 2) * c->P;
+  c->st = (cudaStream_t)cuda_stream;
+  c->peer_ring.assign(world, nullptr);
+  c->peer_slot_words.assign(world, 0);
+  c->ipc_mapped.assign(world, nullptr);
+  cudaGetDevice(&c->device);
+  std::vector<int32_t> colptr;
+  std::vector<uint32_t> ent;
+  std::vector<int16_t> dg;
+  build_csc_direct(m, false, 1, (int)N, colptr, ent, dg);
+  for (int64_t p = c->r0; p < c->r1; ++p)
+    if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
+  int32_t *dcp = nullptr;
+  uint32_t *dent = nullptr;
+  cudaError_t e;
+  // the ring is a plain cudaMalloc allocation so that cudaIpcGetMemHandle can export it
+  if ((e = cudaMalloc((void **)&c->XL, (size_t)(c->P / 2 * c->Mp * 4))) != cudaSuccess ||
+      (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess ||
+      (e = cudaMalloc((void **)&dcp, colptr.size() * 4)) != cudaSuccess ||
+      (e = cudaMalloc((void **)&dent, ent.size() * 4)) != cudaSuccess) {
+    if (dcp) cudaFree(dcp);
+    rd_agchain_destroy(c);
+    return fail(RD_ENOMEM, "rd_agchain_create: device allocation: %s", cudaGetErrorString(e));
+  }
+  cudaMemcpyAsync(dcp, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st);
+  cudaMemcpyAsync(dent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice, c->st);
+  const int64_t nxl = c->P / 2 * c->Mp, nring = (alpha_max + 1) * c->slot_words;
+  fill_u32_kernel<<<(unsigned)((nxl + 255) / 256), 256, 0, c->st>>>(c->XL, nxl, kInf2);
+  fill_u32_kernel<<<(unsigned)((nring + 255) / 256), 256, 0, c->st>>>(c->ring, nring, kInf2);
+  const unsigned g = (unsigned)((N + 255) / 256);
+  scatter_dense_operands_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, nullptr, 0, c->XL, c->Mp, c->r0, c->r1);
+  scatter_rp_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, 1, (int)N, c->r0, c->r1, c->slot(1), c->P, nullptr, nullptr);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  cudaFree(dcp);
+  cudaFree(dent);
+  if (e != cudaSuccess) {
+    rd_agchain_destroy(c);
+    return fail(RD_ECUDA, "rd_agchain_create: %s", cudaGetErrorString(e));
+  }
+  c->peer_ring[rank] = c->ring;
+  c->peer_slot_words[rank] = c->slot_words;
+  c->k = 1;
+  *out = c;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int64_t *slot_words) {
+  rd_enter();
+  if (!c || !handle_out) return fail(RD_EINVAL, "rd_agchain_ipc_handle: NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == RD_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  RD_CUDA_CHECK(cudaIpcGetMemHandle(&h, c->ring));
+  memcpy(handle_out, &h, sizeof h);
+  if (slot_words) *slot_words = c->slot_words;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_ring(const rd_agchain *c, const void **ring_dev, int64_t *slot_words) {
+  rd_enter();
+  if (!c || !ring_dev) return fail(RD_EINVAL, "rd_agchain_ring: NULL argument");
+  *ring_dev = c->ring;
+  if (slot_words) *slot_words = c->slot_words;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_set_peer(rd_agchain *c, int s, const void *ipc_handle, const void *ring_dev,
+                                   int64_t slot_words) {
+  rd_enter();
+  if (!c || s < 0 || s >= c->world) return fail(RD_EINVAL, "rd_agchain_set_peer: bad chain or rank");
+  if (s == c->rank) return RD_OK;
+  const int64_t want = (round_up(c->bounds[s + 1] - c->bounds[s], kTile) / 2) * c->P;
+  if (slot_words != want)
+    return fail(RD_EINVAL, "rd_agchain_set_peer: rank %d slot has %lld words, expected %lld", s,
+                (long long)slot_words, (long long)want);
+  if (c->ipc_mapped[s]) {
+    cudaIpcCloseMemHandle(c->ipc_mapped[s]);
+    c->ipc_mapped[s] = nullptr;
+  }
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof h);
+    void *p = nullptr;
+    RD_CUDA_CHECK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_mapped[s] = p;
+    c->peer_ring[s] = reinterpret_cast<const uint32_t *>(p);
+  } else {
+    if (!ring_dev) return fail(RD_EINVAL, "rd_agchain_set_peer: neither an IPC handle nor a device pointer");
+    c->peer_ring[s] = reinterpret_cast<const uint32_t *>(ring_dev);
+  }
+  c->peer_slot_words[s] = slot_words;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) {
+  rd_enter();
+  NvtxRange nvtx_range("rd_agchain_step");
+  if (!c || !stats_dev) return fail(RD_EINVAL, "rd_agchain_step: NULL argument");
+  PeerB pb{};
+  pb.n = c->world;
+  const int ks = c->k % (c->alpha_max + 1);
+  for (int s = 0; s < c->world; ++s) {
+    if (!c->peer_ring[s]) return fail(RD_EINVAL, "rd_agchain_step: rank %d's ring is not set", s);
+    pb.base[s] = c->peer_ring[s] + (int64_t)ks * c->peer_slot_words[s];
+    pb.t0[s] = (int32_t)(c->bounds[s] / 2);
+  }
+  pb.t0[c->world] = (int32_t)(c->P / 2);
+  const int knew = c->k + 1;
+  EpiArgs epi{};
+  epi.nprev = std::min(c->alpha_max, knew - 1);
+  for (int a = 1; a <= epi.nprev; ++a) epi.prev[a - 1] = c->slot(knew - a);
+  epi.stats = stats_dev;
+  epi.diag_row0 = c->r0;
+  stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
+  RD_CUDA_CHECK(cudaGetLastError());
+  int rc;
+#define RD_AG(D) launch_gemm_v<kOutRP, true, D>(c->XL, c->Mp, nullptr, c->P, c->P / 2, c->slot(knew), c->P, c->Mr, \
+                                                 c->N, c->Mp, c->P, epi, c->st, 1, pb)
+  switch (g_dpx_cols) {
+    case 0: rc = RD_AG(0); break;
+    case 2: rc = RD_AG(2); break;
+    case 3: rc = RD_AG(3); break;
+    case 4: rc = RD_AG(4); break;
+    default: rc = RD_AG(8); break;
+  }
+#undef RD_AG
+  if (rc != RD_OK) return rc;
+  c->k = knew;
+  return RD_OK;
+}
+
+extern "C" int rd_agchain_read_rows(rd_agchain *c, int k, int16_t *host_out) {
+  rd_enter();
+  if (!c || !host_out) return fail(RD_EINVAL, "rd_agchain_read_rows: NULL argument");
+  if (k < 1 || k > c->k || k < c->k - c->alpha_max)
+    return fail(RD_EINVAL, "rd_agchain_read_rows: power %d not in the ring (current %d)", k, c->k);
+  int16_t *d = nullptr;
+  RD_CUDA_CHECK(cudaMallocAsync((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
+  dim3 grid((unsigned)((c->N + 255) / 256), (unsigned)c->Mr);
+  unpack_rp_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->P, c->Mr, c->N, d, nullptr);
+  cudaError_t e = cudaMemcpyAsync(host_out, d, (size_t)(c->Mr * c->N * 2), cudaMemcpyDeviceToHost, c->st);
+  cudaFreeAsync(d, c->st);
+  if (e != cudaSuccess) return fail(RD_ECUDA, "rd_agchain_read_rows: %s", cudaGetErrorString(e));
+  RD_CUDA_CHECK(cudaStreamSynchronize(c->st));
+  return RD_OK;
+}
+
+extern "C" int32_t rd_agchain_diag1(const rd_agchain *c) { return c ? c->diag1 : INT32_MAX; }
+extern "C" int64_t rd_agchain_order(const rd_agchain *c) { return c ? c->N : -1; }
 
 // ============================================================ power sequence ==
 // Argument checks shared by the power-sequence entries; maxlab = the largest label (entries

@@ -310,6 +310,80 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
     return dec.result(t_build=t1 - t0, t_chain=t2 - t1)
 
 
+# ------------------------------------------------- peer all-gather form (fused) --
+def peer_bounds(N: int, world: int):
+    """Row boundaries [b_0 = 0, b_1, ..., b_world = N] of the peer all-gather form: whole
+    128-row tiles, balanced within one tile, every panel non-empty."""
+    b = [panel_bounds(N, world, s)[0] for s in range(world)] + [N]
+    if any(b[s + 1] <= b[s] for s in range(world)):
+        raise ValueError(f"N={N} has fewer 128-row tiles than the {world} ranks")
+    return b
+
+
+def peer_chain(m: int, alpha_max: int = 10, group=None, stream=None, factory=None):
+    """This rank's AgChain with every peer's ring registered: the IPC handles (64 B each) and
+    slot sizes are exchanged with all_gather_object; every rank must call it.  `factory(m,
+    bounds, rank, alpha_max)` overrides the chain (CPU tests)."""
+    import torch.distributed as dist
+
+    from . import AgChain, count_words
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bounds = peer_bounds(count_words(m), world)
+    if factory is None:
+        chain = AgChain(m, bounds, rank, alpha_max=alpha_max, stream=stream)
+    else:
+        chain = factory(m, bounds, rank, alpha_max)
+    if world > 1:
+        info = [None] * world
+        dist.all_gather_object(info, chain.ipc_handle(), group=group)
+        for s in range(world):
+            if s != rank:
+                chain.set_peer(s, handle=info[s][0], slot_words=info[s][1])
+    return chain
+
+
+def power_sequence_peer(m: int, kmax: int = 50, alpha_max: int = 10, policy: int = 0, group=None,
+                        factory=None):
+    """Algorithm 2 in the peer all-gather form (rd_agchain): rank r
+    computes rows R_r of A^{k+1} = A (x) A^k with the GEMM reading A^k from every rank's ring
+    (NVLink peer memory via CUDA IPC).  The stats all_reduce(MIN) of step k is the only
+    synchronisation and orders all ranks' step k before any step k+1.  Same result dict as
+    power_sequence."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    t0 = time.perf_counter()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    on_gpu = factory is None
+    device = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    chain = peer_chain(m, alpha_max, group, factory=factory)
+    d1 = chain.diag1
+    if world > 1:
+        t = torch.tensor([d1], dtype=torch.int64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        d1 = int(t.item())
+    if on_gpu:
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group=group)    # every peer mapped before any rank reads peer memory
+    t1 = time.perf_counter()
+    dec = Decider(alpha_max, policy, kmax, d1)
+    for k in range(2, kmax + 1):
+        s = chain.step()
+        if world > 1:
+            dist.all_reduce(s, op=dist.ReduceOp.MIN, group=group)
+        if dec.feed(k, s.cpu().numpy()):
+            break
+    t2 = time.perf_counter()
+    if world > 1:
+        dist.barrier(group=group)    # no rank frees its ring while a peer may still map it
+    chain.close()
+    return dec.result(t_build=t1 - t0, t_chain=t2 - t1)
+
+
 # ----------------------------------------------------- panel-sequential (one GPU) --
 def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int | None = None, method: int = 1,
                           policy: int = 0, progress=None, early_stop: bool = True):

@@ -211,3 +211,95 @@ def test_gloo_allgather_product_and_chain(world, m):
         assert (res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
                                                                          ref["k_stop"])
         assert res["diag"][1:res["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+# ------------------------------------------------- peer all-gather form (fused) --
+class OraclePeerPanel:
+    """Stand-in for rd.AgChain on CPU: rows R_r of A^{k+1} = A (x) A^k by the oracle.  The
+    GEMM's reads of the peers' ring slots are emulated by an all_gather_object of the current
+    rows; the handle exchange, the stats reduction and the decision loop of
+    dist.power_sequence_peer run unchanged."""
+
+    def __init__(self, m, bounds, rank, alpha_max):
+        self.A = O.matrix(m)
+        self.bounds, self.rank, self.am = bounds, rank, alpha_max
+        self.r0, self.r1 = bounds[rank], bounds[rank + 1]
+        self.k = 1
+        self.ring = {1: self.A[self.r0:self.r1].copy()}
+        self.peers = {}
+        d = np.diag(self.A)[self.r0:self.r1]
+        self.diag1 = int(d[d != OINF].min()) if (d != OINF).any() else 2**31 - 1
+
+    def ipc_handle(self):
+        return bytes([self.rank]) * 64, (self.r1 - self.r0) * self.A.shape[0]
+
+    def set_peer(self, s, handle=None, ring_ptr=None, slot_words=0):
+        assert handle == bytes([s]) * 64
+        assert slot_words == (self.bounds[s + 1] - self.bounds[s]) * self.A.shape[0]
+        self.peers[s] = handle
+
+    def step(self):
+        assert len(self.peers) == len(self.bounds) - 2
+        parts = [None] * (len(self.bounds) - 1)
+        dist.all_gather_object(parts, self.ring[self.k])
+        Ak = np.concatenate(parts, axis=0)
+        k = self.k + 1
+        X = O.minplus(self.A[self.r0:self.r1], Ak, skip=True)
+        self.ring[k] = X
+        s = rdist.neutral_stats(self.am)
+        d = [X[i, self.r0 + i] for i in range(X.shape[0])]
+        s[0] = min(min(d), RINF)
+        for a in range(1, min(self.am, k - 1) + 1):
+            P = self.ring[k - a]
+            fx, fp = X != OINF, P != OINF
+            both = fx & fp
+            e = 1 + 4 * (a - 1)
+            if both.any():
+                diff = X[both].astype(np.int64) - P[both].astype(np.int64)
+                s[e], s[e + 1] = int(diff.min()), -int(diff.max())
+            s[e + 2] = -1 if (fx != fp).any() else 0
+            s[e + 3] = -1 if both.any() else 0
+        self.ring.pop(k - self.am - 1, None)
+        self.k = k
+        return torch.from_numpy(s)
+
+    def close(self):
+        pass
+
+
+def _peer_worker(rank, world, port, m, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = rdist.power_sequence_peer(m, 50, 10, 0, factory=OraclePeerPanel)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_bounds():
+    assert rdist.peer_bounds(287, 2) == [0, 256, 287]
+    assert rdist.peer_bounds(21909, 8)[1:3] == [2816, 5632]
+    with pytest.raises(ValueError):
+        rdist.peer_bounds(287, 4)       # 3 tiles, 4 ranks: the fused form needs non-empty panels
+
+
+@pytest.mark.parametrize("world,m", [(2, 5), (3, 6)])
+def test_gloo_peer_allgather_chain(world, m):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, m, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = O.power_chain(m, 50, 10, 0)
+    for r in range(world):
+        res = out[r]
+        assert (res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                         ref["k_stop"])
+        assert res["diag"][1:res["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]

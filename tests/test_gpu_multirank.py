@@ -89,3 +89,59 @@ def test_bench_two_ranks_one_gpu_gloo():
     assert d["config"]["detected"] == [21, 5, 16]
     assert d["e2e"]["triple"] == [21, 5, 16]
     assert d["time_to_periodicity"]["5"]["triple"] == [16, 5, 12]
+
+
+PEER_WORKER = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import numpy as np
+import torch, torch.distributed as dist
+import paper_2409_17658_b200 as rd
+from paper_2409_17658_b200 import dist as D
+torch.cuda.set_device(0)
+dist.init_process_group("gloo")
+out = {}
+for m in (5, 6, 7):
+    r = D.power_sequence_peer(m, 50, 10)
+    out["peer%d" % m] = [r["n0"], r["alpha"], r["beta"], r["k_stop"], r["diag"][1:r["k_stop"] + 1]]
+# rows of A^6 at m = 6 from the peer chain, gathered on rank 0 (checked against the oracle)
+ch = D.peer_chain(6, 4)
+dist.barrier()
+for k in range(2, 7):
+    s = ch.step()
+    dist.all_reduce(s, op=dist.ReduceOp.MIN)
+    s.cpu()
+rows = ch.read_rows(6)
+got = [None] * dist.get_world_size()
+dist.all_gather_object(got, rows.tolist())
+dist.barrier()
+ch.close()
+if dist.get_rank() == 0:
+    out["rows6"] = [r for part in got for r in part]
+    print("RESULT " + json.dumps(out), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_two_ranks_one_gpu_peer_allgather(tmp_path):
+    # the fused peer all-gather form across 2 processes: each GEMM reads the other process's
+    # ring through a CUDA IPC mapping (the NVLink path on a multi-GPU node)
+    script = tmp_path / "p.py"
+    script.write_text(PEER_WORKER)
+    env = dict(os.environ, ROOT=ROOT, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), WORLD_SIZE="2")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    line = [l for l in outs[0].splitlines() if l.startswith("RESULT ")][0]
+    res = json.loads(line[7:])
+    for m in (5, 6, 7):
+        ref = O.power_chain(m, 50, 10, 0)
+        assert res["peer%d" % m] == [ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"],
+                                     ref["diag"][1:ref["k_stop"] + 1]], m
+    A = O.matrix(6)
+    P = A.copy()
+    for _ in range(5):
+        P = O.minplus(P, A, skip=True)
+    want = np.where(P >= O.INF, 0x3FFF, P).astype(np.int16)
+    assert (np.array(res["rows6"], dtype=np.int16) == want).all()

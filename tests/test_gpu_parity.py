@@ -604,3 +604,78 @@ def test_device_allocation_failure_is_reported():
     assert e.value.status == rd.RD_EINVAL
     C = rd.rd_minplus_mul(_gpu(operand(64, 64, 1)), _gpu(operand(64, 64, 2)))
     assert C.shape == (64, 64)
+
+
+# ------------------------------------------------ peer all-gather chain (fused) --
+@pytest.mark.parametrize("m", [1, 3, 5, 7])
+def test_agchain_single_rank_every_power_bit_exact(m):
+    # A^{k+1} = A (x) A^k with the right operand read through the peer table (one rank):
+    # every power and every alpha's stats against the oracle (Alg 2 step 4)
+    ref = O.power_chain(m, 50, 10, 0)
+    kstop = ref["k_stop"]
+    P = _oracle_powers(m, kstop)
+    N = P[1].shape[0]
+    ch = rd.AgChain(m, [0, N], 0, alpha_max=10)
+    assert (ch.read_rows(1) == P[1]).all()
+    for k in range(2, kstop + 1):
+        st = ch.step().cpu().numpy()
+        assert (ch.read_rows(k) == P[k]).all(), (m, k)
+        d = int(np.diag(P[k]).min())
+        assert st[0] == min(d, RINF), (m, k)
+        for a in range(1, min(10, k - 1) + 1):
+            b = O.shift(to_inf(P[k], RINF, OINF, np.int32), to_inf(P[k - a], RINF, OINF, np.int32))
+            dec = rd.rd_stats_decide(st, 10, k, only_alpha=a)
+            assert (dec[1] if dec else None) == b, (m, k, a)
+    ch.close()
+
+
+@pytest.mark.parametrize("m,cuts", [(5, [0, 128, 287]), (6, [0, 256, 384, 848]),
+                                    (7, [0, 640, 1280, 1920, 2507])])
+def test_agchain_panels_in_process_equal_full_chain(m, cuts):
+    # several ranks emulated in one process on one device: each panel's GEMM reads the other
+    # panels' ring slots through device pointers (the IPC path maps the same layout); steps
+    # are separated by a device sync, as the stats all_reduce separates them across GPUs
+    K = 9
+    full = rd.Chain(m, alpha_max=4)
+    ranks = [rd.AgChain(m, cuts, r, alpha_max=4) for r in range(len(cuts) - 1)]
+    for r, c in enumerate(ranks):
+        for s, o in enumerate(ranks):
+            if s != r:
+                ptr, words = o.ring()
+                c.set_peer(s, ring_ptr=ptr, slot_words=words)
+    for k in range(2, K + 1):
+        sf = full.step().cpu().numpy()
+        sp = [c.step(torch.empty_like(c.stats)) for c in ranks]
+        torch.cuda.synchronize()
+        sp = np.min(np.stack([x.cpu().numpy() for x in sp]), axis=0)
+        assert (sf == sp).all(), (m, k)
+        fr = full.read_rows(k)
+        for c, a, b in zip(ranks, cuts[:-1], cuts[1:]):
+            assert (c.read_rows(k) == fr[a:b]).all(), (m, k, a)
+    for c in ranks:
+        c.close()
+    full.close()
+
+
+@pytest.mark.parametrize("m", [4, 7, 8])
+def test_power_sequence_peer_single_rank(m):
+    from paper_2409_17658_b200 import dist as rdist
+    ref = O.power_chain(m, 50, 10, 0)
+    got = rdist.power_sequence_peer(m, 50, 10)
+    assert (got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
+                                                                      ref["k_stop"])
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+def test_agchain_bad_arguments():
+    N = rd.count_words(5)
+    with pytest.raises(rd.RDError):
+        rd.AgChain(5, [0, 100, N], 0)          # panel 1 does not start on a 128-row tile
+    with pytest.raises(rd.RDError):
+        rd.AgChain(5, [0, N - 1], 0)           # bounds must end at N
+    c = rd.AgChain(5, [0, 128, N], 0)
+    with pytest.raises(rd.RDError):
+        c.step()                               # rank 1's ring not registered
+    with pytest.raises(rd.RDError):
+        c.set_peer(1, ring_ptr=c.ring()[0], slot_words=7)   # wrong slot size
+    c.close()
