@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8, 9])
     p.add_argument("--oracle-ttp-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--gops-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
+    p.add_argument("--invariance-m", type=int, default=8, help="order of the operand-invariance check (0: off)")
     p.add_argument("--ttp-structured-only-m", type=int, nargs="*", default=[10])
     p.add_argument("--form", default="replicated", choices=["replicated", "allgather", "peer"],
                    help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
@@ -74,7 +75,7 @@ class ClockSampler:
     }
 
     def __init__(self, device_index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.power, self.reasons, self.max_mhz = [], [], set(), None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -89,6 +90,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
@@ -112,7 +114,8 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w": round(statistics.median(self.power), 1) if self.power else None}
 
 
 # -------------------------------------------------------------- CPU oracle --
@@ -331,26 +334,59 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                "seconds": round(te, 3), "k_stop": res["k_stop"],
                "triple": [res["n0"], res["alpha"], res["beta"]]}
 
-    # dense power-step Gop/s at every order N = C_m (SURVEY §8(d) shapes), one rank, CUDA events
+    # dense power-step Gop/s at every order N = C_m (SURVEY §8(d) shapes and protocol: 3 warm-up
+    # steps, then median and best of 10 individually event-timed steps A^(k-1) (x) A, k = 5..14)
+    def timed(fn, warm=3, reps=10):
+        with torch.cuda.stream(stream):
+            for _ in range(warm):
+                fn()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+            for a, b in ev:
+                a.record(stream)
+                fn()
+                b.record(stream)
+        torch.cuda.synchronize()
+        t = sorted(a.elapsed_time(b) * 1e-3 for a, b in ev)
+        return statistics.median(t), t[0]
+
     gops_by_m = {}
     if rank == 0 and not args.no_e2e:
         for mm in args.gops_m:
             chm = rd.Chain(mm, alpha_max=am, stream=stream)
             nn = chm.N
-            with torch.cuda.stream(stream):
-                for _ in range(3):
-                    chm.step()
-                reps = 20 if mm <= 8 else 3
-                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ea.record(stream)
-                for _ in range(reps):
-                    chm.step()
-                eb.record(stream)
-            torch.cuda.synchronize()
-            dtm = ea.elapsed_time(eb) / reps * 1e-3
-            gops_by_m[str(mm)] = {"N": nn, "ms_per_step": round(dtm * 1e3, 4),
-                                  "gops": round(float(nn) ** 3 / dtm / 1e9, 1)}
+            med, best = timed(chm.step)
+            gops_by_m[str(mm)] = {"N": nn, "ms_per_step": round(med * 1e3, 4), "ms_best": round(best * 1e3, 4),
+                                  "gops": round(float(nn) ** 3 / med / 1e9, 1),
+                                  "gops_best": round(float(nn) ** 3 / best / 1e9, 1)}
             chm.close()
+
+    # operand invariance: the dense kernel is data-oblivious, so the generic
+    # product rd_minplus_mul (packing included) takes the same time on the real A^4 (x) A, on
+    # A (x) A and on synthetic uniform [0, 1000] operands with 1% inf (seeds 0, 1, 2)
+    invariance = None
+    if rank == 0 and not args.no_e2e and args.invariance_m:
+        from rd_inputs import operand
+        mi = args.invariance_m
+        chi = rd.Chain(mi, alpha_max=4, stream=stream)
+        for _ in range(3):
+            chi.step()
+        A4 = torch.from_numpy(chi.read_rows(4)).to(dev)
+        A1 = torch.from_numpy(chi.read_rows(1)).to(dev)
+        chi.close()
+        ni = A1.shape[0]
+        C = torch.empty_like(A1)
+        cases = {"A^4 (x) A": (A4, A1), "A (x) A": (A1, A1)}
+        for sd in (0, 1, 2):
+            cases[f"uniform[0,1000] 1% inf, seed {sd}"] = (
+                torch.from_numpy(operand(ni, ni, sd)).to(dev), torch.from_numpy(operand(ni, ni, sd + 100)).to(dev))
+        invariance = {"m": mi, "N": ni, "call": "rd_minplus_mul (pack + GEMM)", "ms_median": {}, "ms_best": {}}
+        for name, (X, Y) in cases.items():
+            med, best = timed(lambda: rd.rd_minplus_mul_ex(X, ni, Y, ni, C, ni, ni, ni, ni, stream=stream))
+            invariance["ms_median"][name] = round(med * 1e3, 4)
+            invariance["ms_best"][name] = round(best * 1e3, 4)
+        v = list(invariance["ms_median"].values())
+        invariance["spread"] = round(max(v) / min(v) - 1, 4)
+        del cases, A4, A1, C
 
     # time to periodicity per m (Alg 2 to first detection): build (words, A(G), upload,
     # packing) and chain (products + fused checks + per-step stats decision), max over ranks
@@ -448,6 +484,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             "cpu_baseline": cpu,
             "time_to_periodicity": ttp,
             "gops_by_m": gops_by_m,
+            "operand_invariance": invariance,
             "paper_context": {"k80_cumatrixtrop_gops_derived": PAPER_K80_GOPS.get(m),
                               "source": "BASELINE.md 1.1, 49 N^3 / Table 3 kernel time"},
         }
