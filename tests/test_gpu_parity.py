@@ -679,3 +679,25 @@ def test_agchain_bad_arguments():
     with pytest.raises(rd.RDError):
         c.set_peer(1, ring_ptr=c.ring()[0], slot_words=7)   # wrong slot size
     c.close()
+
+
+def test_agchain_m9_every_power_sampled_rows_and_detection():
+    # the peer all-gather form at the bench's full size (m = 9, world 1, the launch bench.py
+    # --form peer times): sampled rows of every power to first detection against the oracle's
+    # row recurrence, and the stats decision (22, 5, 20) at k = 27 (Table 2)
+    m = 9
+    A = O.matrix(m)
+    N = A.shape[0]
+    rows = sample_rows(N, 24, seed=309)
+    R = A[rows].copy()
+    ch = rd.AgChain(m, [0, N], 0, alpha_max=10)
+    dec = None
+    for k in range(2, 28):
+        st = ch.step().cpu().numpy()
+        R = O.minplus(R, A, skip=True)
+        assert (ch.read_rows(k)[rows] == to_inf(R, OINF, RINF, np.int16)).all(), k
+        d = rd.rd_stats_decide(st, 10, k)
+        if dec is None and d:
+            dec = (k, k - d[0], d[0], d[1])
+    assert dec == (27, 22, 5, 20)
+    ch.close()
