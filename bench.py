@@ -151,6 +151,17 @@ class OracleSample:
         return rows * self.N * self.N / dt / 1e9, dt
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cores_used():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
@@ -452,6 +463,28 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             r = O.power_chain(mm, 50, am, 0)
             ttp_o[str(mm)] = {"seconds": round(time.perf_counter() - t0, 4), "triple": [r["n0"], r["alpha"], r["beta"]]}
         cpu["time_to_periodicity"] = ttp_o
+        # SURVEY §8(d) oracle timings: the dense product at each small order (full N^3, same
+        # OpenMP i-j-k loop) and the independent checkers on points of their domains
+        dense = {}
+        for mm in (3, 4, 5, 6, 7):
+            Am = O.matrix(mm)
+            BTm = np.ascontiguousarray(Am.T)
+            t0 = time.perf_counter()
+            O.minplus_bt(Am, BTm)
+            dt = time.perf_counter() - t0
+            dense[str(mm)] = {"N": Am.shape[0], "seconds": round(dt, 4),
+                              "gops": round(float(Am.shape[0]) ** 3 / max(dt, 1e-9) / 1e9, 3)}
+        cpu["dense_product_by_m"] = dense
+        checks = {}
+        for name, fn, a in (("X1 exhaustive f: V -> {0,1,2}", O.gamma_bruteforce3, (3, 5)),
+                            ("X2 S2-subset brute force", O.gamma_s2subset, (4, 6)),
+                            ("X3 row DP along the path", O.gamma_rowdp, (9, 8)),
+                            ("X5 S2-pair trace DP", O.gamma_pairtrace, (4, 30))):
+            t0 = time.perf_counter()
+            v = fn(*a)
+            checks[name] = {"m_n": list(a), "gamma": int(v), "seconds": round(time.perf_counter() - t0, 4)}
+        cpu["checkers"] = checks
+        cpu["host"] = {"cpu_model": _cpu_model(), "nproc": os.cpu_count()}
 
     if rank == 0:
         line = {
