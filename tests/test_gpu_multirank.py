@@ -145,3 +145,21 @@ def test_two_ranks_one_gpu_peer_allgather(tmp_path):
         P = O.minplus(P, A, skip=True)
     want = np.where(P >= O.INF, 0x3FFF, P).astype(np.int16)
     assert (np.array(res["rows6"], dtype=np.int16) == want).all()
+
+
+def test_bench_two_ranks_one_gpu_gloo_peer_form():
+    # bench.py --form peer under torchrun with 2 ranks on one GPU (gloo): each rank's GEMM
+    # reads the other's ring through CUDA IPC; the detected triple is right (not a perf number)
+    env = dict(os.environ, RD_DIST_BACKEND="gloo", RD_FORCE_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--order-m", "7", "--form", "peer", "--steps", "3", "--warmup", "22",
+           "--no-cpu-baseline", "--no-e2e"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["form"] == "peer"
+    assert d["config"]["detected"] == [21, 5, 16]
+    assert d["gpu_launches"] == 2 * 3 * 2
