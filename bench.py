@@ -398,6 +398,16 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         v = list(invariance["ms_median"].values())
         invariance["spread"] = round(max(v) / min(v) - 1, 4)
         del cases, A4, A1, C
+        # the 32-bit generic product (rd_minplus_mul32: entries beyond the int16 headroom) at the
+        # same N, uniform [0, 2^29) with 1% inf
+        X32 = torch.from_numpy(operand(ni, ni, 7, hi=2**29 - 1, inf=rd.RD_INF32, dtype=np.int32)).to(dev)
+        Y32 = torch.from_numpy(operand(ni, ni, 8, hi=2**29 - 1, inf=rd.RD_INF32, dtype=np.int32)).to(dev)
+        C32 = torch.empty_like(X32)
+        med, best = timed(lambda: rd.rd_minplus_mul32(X32, Y32, C32, stream=stream))
+        invariance["mul32"] = {"ms_median": round(med * 1e3, 4), "ms_best": round(best * 1e3, 4),
+                               "gops": round(float(ni) ** 3 / med / 1e9, 1),
+                               "data": "uniform [0, 2^29) int32, 1% inf, seeds 7, 8"}
+        del X32, Y32, C32
 
     # time to periodicity per m (Alg 2 to first detection): build (words, A(G), upload,
     # packing) and chain (products + fused checks + per-step stats decision), max over ranks

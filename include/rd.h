@@ -28,6 +28,7 @@ extern "C" {
 #endif
 
 #define RD_INF ((int16_t)0x3FFF)
+#define RD_INF32 ((int32_t)0x3FFFFFFF)   /* the 32-bit API's infinity (rd_minplus_mul32) */
 
 enum rd_status {
   RD_OK = 0,        /* success */
@@ -96,6 +97,23 @@ int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t l
  * arrive over NVLink. */
 int rd_minplus_mul_acc(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb,
                        int16_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream);
+
+/* rd_minplus_mul32[_ex] — the (min,+) product c_ij = min_k (a_ik + b_kj) for int32
+ * entries, when the values exceed the int16 headroom of rd_minplus_mul (the
+ * 32-bit DPX form: one VIADDMNMX per term plus the IMAD + VIMNMX3 mix).
+ *   A, B, C   DEVICE int32, row-major (lda/ldb/ldc in elements); C must not alias A or B.
+ *   M x K times K x N -> M x N (rd_minplus_mul32: square N, legacy default stream;
+ *             _ex: on cuda_stream, NULL = legacy default).  Asynchronous.
+ * Domain: x >= RD_INF32 (0x3FFFFFFF) is +inf and is clamped to RD_INF32 on load; finite
+ * entries lie in [0, RD_INF32).  Sums never overflow (<= 0x7FFFFFFE); results hold exactly
+ * RD_INF32 for +inf, and a finite sum >= RD_INF32 saturates to RD_INF32 (keep finite inputs
+ * below RD_INF32 / 2 for exact finite results).  Negative entries are a precondition
+ * violation (unchecked).  Workspace (stream-ordered, from the device's default pool):
+ * (Mp + Np) * Kp * 4 bytes, Mp, Np rounded up to 128 and Kp to 32.
+ * Errors: RD_EINVAL (M, N, K < 1, NULL, ld too small), RD_ENOMEM, RD_ECUDA. */
+int rd_minplus_mul32(const int32_t *A, const int32_t *B, int32_t *C, int64_t N);
+int rd_minplus_mul32_ex(const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
+                        int32_t *C, int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream);
 
 /* rd_panel_stats — the standalone (HBM-bound) form of the fused epilogue reductions:
  * the stats vector (layout of rd_chain_step) of the row-major int16 panel `cur`

@@ -83,6 +83,10 @@ def lib():
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_sparse_bytes.argtypes = [ci]
+        L.rd_minplus_mul32.argtypes = [p, p, p, i64]
+        L.rd_minplus_mul32_ex.argtypes = [p, i64, p, i64, p, i64, i64, i64, i64, p]
+        L.rd_minplus_mul32.restype = ci
+        L.rd_minplus_mul32_ex.restype = ci
         L.rd_agchain_create.argtypes = [ci, ci, p, ci, ci, p, p]
         L.rd_agchain_destroy.argtypes = [p]
         L.rd_agchain_ipc_handle.argtypes = [p, p, p]
@@ -217,6 +221,25 @@ def rd_minplus_mul(A, B, C=None):
     _sync_device()
     _check(lib().rd_minplus_mul_ex(A.data_ptr(), K, B.data_ptr(), N, C.data_ptr(), N, M, N, K,
                                    _stream_ptr(None)))
+    return C
+
+
+RD_INF32 = 0x3FFFFFFF
+
+
+def rd_minplus_mul32(A, B, C=None, stream=None):
+    """C = A (x) B for int32 CUDA tensors (row-major, A: M x K, B: K x N) beyond the int16
+    headroom; RD_INF32 = 0x3FFFFFFF is +inf (rd.h rd_minplus_mul32_ex)."""
+    import torch
+    assert A.is_cuda and A.dtype == torch.int32 and A.is_contiguous() and A.dim() == 2
+    M, K = A.shape
+    K2, N = B.shape
+    assert K == K2 and B.dtype == torch.int32 and B.is_contiguous() and B.device == A.device
+    if C is None:
+        C = torch.empty((M, N), dtype=torch.int32, device=A.device)
+    _sync_device()
+    _check(lib().rd_minplus_mul32_ex(A.data_ptr(), K, B.data_ptr(), N, C.data_ptr(), N, M, N, K,
+                                     _stream_ptr(stream)))
     return C
 
 

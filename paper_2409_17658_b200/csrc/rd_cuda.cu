@@ -571,6 +571,148 @@ int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel
 // 12 -> 41.3, 16 -> 47.4, 24 -> 68.5, 32 -> 85.8 GB, the same 276 ms
 int g_raster_group = kGroup;
 
+// ----------------------------------------------------------- 32-bit GEMM --
+// The generic product for entries beyond the int16 headroom (the
+// `__viaddmin_s32` variant; rd.h rd_minplus_mul32).  Same CTA tile, thread tile, cp.async
+// pipeline and rasterisation as minplus_gemm_kernel, one int32 per k instead of a k-pair:
+//   XT[k][i] = X[i][k]  (left operand transposed, [Kp][Mp]),  BP[k][j] = B[k][j]  ([Kp][Np]),
+// both INF32-padded to the tile, entries clamped to [., RD_INF32] on packing.  Per k a thread
+// reads 4 x LDS.128 and updates 64 accumulators: columns c < DPXC with one VIADDMNMX (32-bit,
+// alu), the others two k at a time with two IMAD adds (fma; exact: sums <= 0x7FFFFFFE) and one
+// VIMNMX3 (alu).  RD_INF32 + anything >= RD_INF32, and accumulators start at RD_INF32, so
+// infinite results come out exactly RD_INF32 (finite sums >= RD_INF32 saturate to it).
+constexpr int32_t kInf32 = RD_INF32;
+
+__global__ void pack_t32_kernel(const int32_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+                                int32_t *__restrict__ XT, int64_t ldt, int64_t kp) {
+  __shared__ int32_t tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int64_t i = i0 + yy, k = k0 + tx;
+    tile[yy][tx] = (i < rows && k < cols) ? min(X[i * ld + k], kInf32) : kInf32;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int64_t k = k0 + yy, i = i0 + tx;
+    if (k < kp && i < ldt) XT[k * ldt + i] = tile[tx][yy];
+  }
+}
+
+__global__ void pack_copy32_kernel(const int32_t *__restrict__ B, int64_t ld, int64_t K, int64_t N,
+                                   int32_t *__restrict__ BP, int64_t ldp, int64_t kp) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (j >= ldp || k >= kp) return;
+  BP[k * ldp + j] = (j < N && k < K) ? min(B[k * ld + j], kInf32) : kInf32;
+}
+
+template <int DPXC>
+__global__ void __launch_bounds__(kThreads, 2)
+minplus_gemm32_kernel(const int32_t *__restrict__ XT, int64_t ldx, const int32_t *__restrict__ BP, int64_t ldb,
+                      int kp, int32_t *__restrict__ C, int64_t ldc, int64_t M, int64_t N, int nti, int ntj,
+                      int32_t one, int accumulate, int kgroup) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int tid = threadIdx.x;
+  const int wq = tid >> 5, lq = tid & 31;
+  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
+  int64_t i0, j0;
+  {
+    const int bid = blockIdx.x;
+    const int per_group = kgroup * ntj;
+    const int g = bid / per_group, first = g * kgroup;
+    const int gsz = min(nti - first, kgroup);
+    const int w = bid - g * per_group;
+    i0 = (int64_t)(first + w % gsz) * kTile;
+    j0 = (int64_t)(w / gsz) * kTile;
+  }
+  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
+  const int32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
+  const int32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
+  auto load_stage = [&](int stage, int kb) {
+    uint32_t *sx = smem + stage * kStageWords;
+    uint32_t *sb = sx + kBK2 * kTile;
+    const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
+#pragma unroll
+    for (int r = 0; r < kBK2; r += 8) {
+      cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * 8 * ldx);
+      cp_async16(sb + (ld_row + r) * kTile + ld_col, gb + ob + (r / 8) * 8 * ldb);
+    }
+  };
+  int32_t acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = kInf32;
+  const int KB = kp / kBK2;
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (st < KB) load_stage(st, st);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < KB; ++kb) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + kStages - 1;
+      if (nk < KB) load_stage(nk % kStages, nk);
+      cp_async_commit();
+    }
+    const int32_t *sx = reinterpret_cast<const int32_t *>(smem + (kb % kStages) * kStageWords);
+    const int32_t *sb = sx + kBK2 * kTile;
+#pragma unroll
+    for (int t = 0; t < kBK2; t += 2) {
+      int32_t x0[8], x1[8], b0[8], b1[8];
+      {
+        const int4 p = *reinterpret_cast<const int4 *>(sx + t * kTile + ty * 4);
+        const int4 q = *reinterpret_cast<const int4 *>(sx + t * kTile + 64 + ty * 4);
+        const int4 u = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + ty * 4);
+        const int4 v = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
+        x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
+        x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
+      }
+      {
+        const int4 p = *reinterpret_cast<const int4 *>(sb + t * kTile + tx * 4);
+        const int4 q = *reinterpret_cast<const int4 *>(sb + t * kTile + 64 + tx * 4);
+        const int4 u = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + tx * 4);
+        const int4 v = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
+        b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
+        b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < DPXC) {
+            acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
+            acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
+          } else {
+            const int32_t s0 = x0[r] * one + b0[c];
+            const int32_t s1 = x1[r] * one + b1[c];
+            acc[r][c] = __vimin3_s32(acc[r][c], s0, s1);
+          }
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+    if (i >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int64_t j = j0 + (c >> 2) * 64 + tx * 4 + (c & 3);
+      if (j >= N) continue;
+      int32_t v = acc[r][c];
+      if (accumulate) v = min(v, min(C[i * ldc + j], kInf32));
+      C[i * ldc + j] = v;
+    }
+  }
+}
+
+template <int DPXC>
+int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st);
+
 template <int OUT, bool STATS, int DPXC>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
@@ -604,6 +746,37 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
     default: return RD_LG(8);
   }
 #undef RD_LG
+}
+
+template <int DPXC>
+int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm32_kernel<DPXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
+  minplus_gemm32_kernel<DPXC><<<(unsigned)(nti * ntj), kThreads, kSmemBytes, st>>>(
+      XT, ldx, BP, ldb, (int)kp, C, ldc, M, N, nti, ntj, 1, accumulate, g_raster_group);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+int launch_gemm32(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
+                  int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
+#define RD_LG32(D) launch_gemm32_v<D>(XT, ldx, BP, ldb, kp, C, ldc, M, N, Mp, Np, accumulate, st)
+  switch (g_dpx_cols) {
+    case 0: return RD_LG32(0);
+    case 2: return RD_LG32(2);
+    case 3: return RD_LG32(3);
+    case 4: return RD_LG32(4);
+    default: return RD_LG32(8);
+  }
+#undef RD_LG32
 }
 
 int pack_left(const int16_t *X, int64_t ld, int64_t rows, int64_t cols, int64_t row0, uint32_t *XT,
@@ -690,6 +863,42 @@ extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B
 extern "C" int rd_minplus_mul_acc(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
                                   int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
   return minplus_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, 1, "rd_minplus_mul_acc");
+}
+
+static int minplus32_rowmajor(const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb, int32_t *C,
+                              int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, const char *who) {
+  rd_enter();
+  if (!A || !B || !C) return fail(RD_EINVAL, "%s: NULL pointer", who);
+  if (M < 1 || N < 1 || K < 1) return fail(RD_EINVAL, "%s: M, N, K must be >= 1", who);
+  if (lda < K || ldb < N || ldc < N) return fail(RD_EINVAL, "%s: leading dimension too small", who);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, kBK2);
+  int32_t *XT = nullptr, *BP = nullptr;
+  if (int rc0 = retain_default_pool()) return rc0;
+  RD_CUDA_CHECK(cudaMallocAsync((void **)&XT, (size_t)(Kp * Mp * 4), st));
+  cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(Kp * Np * 4), st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(XT, st);
+    return fail(RD_ENOMEM, "%s: workspace: %s", who, cudaGetErrorString(e));
+  }
+  pack_t32_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((Mp + 31) / 32)), dim3(32, 8), 0, st>>>(
+      A, lda, M, K, XT, Mp, Kp);
+  pack_copy32_kernel<<<dim3((unsigned)((Np + 255) / 256), (unsigned)Kp), 256, 0, st>>>(B, ldb, K, N, BP, Np, Kp);
+  int rc = RD_OK;
+  if ((e = cudaGetLastError()) != cudaSuccess) rc = fail(RD_ECUDA, "%s: %s", who, cudaGetErrorString(e));
+  if (rc == RD_OK) rc = launch_gemm32(XT, Mp, BP, Np, Kp, C, ldc, M, N, Mp, Np, 0, st);
+  cudaFreeAsync(XT, st);
+  cudaFreeAsync(BP, st);
+  return rc;
+}
+
+extern "C" int rd_minplus_mul32_ex(const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb, int32_t *C,
+                                   int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+  return minplus32_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, "rd_minplus_mul32_ex");
+}
+
+extern "C" int rd_minplus_mul32(const int32_t *A, const int32_t *B, int32_t *C, int64_t N) {
+  return minplus32_rowmajor(A, N, B, N, C, N, N, N, N, nullptr, "rd_minplus_mul32");
 }
 
 // ------------------------------------------------------- standalone stats --

@@ -701,3 +701,60 @@ def test_agchain_m9_every_power_sampled_rows_and_detection():
             dec = (k, k - d[0], d[0], d[1])
     assert dec == (27, 22, 5, 20)
     ch.close()
+
+
+# ------------------------------------------------------ 32-bit generic product --
+RINF32 = rd.RD_INF32
+
+
+def _oracle_mul32(A32, B32):
+    A = to_inf(A32, RINF32, OINF, np.int32)
+    B = to_inf(B32, RINF32, OINF, np.int32)
+    return to_inf(O.minplus(A, B), OINF, RINF32, np.int32)
+
+
+@pytest.mark.parametrize("N", [1, 33, 129, 300, 1000])
+@pytest.mark.parametrize("inf_frac", [0.0, 0.05, 1.0])
+def test_minplus_mul32_random(N, inf_frac):
+    # values far beyond the int16 headroom (up to 2^29 - 1): exact against the oracle
+    A = operand(N, N, seed=N * 11 + 1, inf_frac=inf_frac, hi=2**29 - 1, inf=RINF32, dtype=np.int32)
+    B = operand(N, N, seed=N * 11 + 2, inf_frac=inf_frac, hi=2**29 - 1, inf=RINF32, dtype=np.int32)
+    C = rd.rd_minplus_mul32(_gpu(A), _gpu(B)).cpu().numpy()
+    assert (C == _oracle_mul32(A, B)).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(5, 300, 7), (300, 5, 129), (129, 257, 1000), (1000, 33, 31)])
+def test_minplus_mul32_rectangular(M, N, K):
+    A = operand(M, K, seed=M + K, inf_frac=0.1, hi=10**6, inf=RINF32, dtype=np.int32)
+    B = operand(K, N, seed=N + K, inf_frac=0.1, hi=10**6, inf=RINF32, dtype=np.int32)
+    C = rd.rd_minplus_mul32(_gpu(A), _gpu(B)).cpu().numpy()
+    assert (C == _oracle_mul32(A, B)).all()
+
+
+def test_minplus_mul32_saturation_and_clamp():
+    # finite sums >= RD_INF32 saturate to RD_INF32 (rd.h); inputs above RD_INF32 clamp to it
+    N = 130
+    A = operand(N, N, 41, inf_frac=0.1, lo=2**29, hi=RINF32 - 1, inf=RINF32, dtype=np.int32)
+    B = operand(N, N, 42, inf_frac=0.1, lo=0, hi=2**29 + 5, inf=2**31 - 1, dtype=np.int32)
+    C = rd.rd_minplus_mul32(_gpu(A), _gpu(B)).cpu().numpy()
+    Bc = np.minimum(B, RINF32)
+    want = np.minimum(_oracle_mul32(A, Bc).astype(np.int64), RINF32).astype(np.int32)
+    assert (C == want).all()
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3, 4, 8])
+def test_minplus_mul32_every_variant_and_int16_agreement(variant):
+    # every mainloop mix is bit-identical; on int16-range data the 32-bit product equals the
+    # 16-bit one (infinities mapped)
+    N = 257
+    A16 = operand(N, N, 51, inf_frac=0.02, hi=5000)
+    B16 = operand(N, N, 52, inf_frac=0.02, hi=5000)
+    try:
+        rd.rd_set_gemm_variant(variant)
+        C32 = rd.rd_minplus_mul32(_gpu(to_inf(A16, RINF, RINF32, np.int32)),
+                                  _gpu(to_inf(B16, RINF, RINF32, np.int32))).cpu().numpy()
+        C16 = rd.rd_minplus_mul(_gpu(A16), _gpu(B16)).cpu().numpy()
+    finally:
+        rd.rd_set_gemm_variant(3)
+    assert (C32 == to_inf(C16, RINF, RINF32, np.int32)).all()
+    assert (C32 == _oracle_mul32(to_inf(A16, RINF, RINF32, np.int32), to_inf(B16, RINF, RINF32, np.int32))).all()
