@@ -269,6 +269,10 @@ int rd_stats_len(int alpha_max);
  * Asynchronous: returns after enqueueing. */
 #define RD_STAT_NONE INT32_MAX
 int rd_chain_step(rd_chain *c, int32_t *stats_dev);
+/* rd_panel_step — the multi-GPU entry named in SURVEY §8(b): one power step of this rank's
+ * row panel with the fused stats written to a caller DEVICE buffer that the ranks then
+ * all-reduce with MIN (NCCL).  Identical to rd_chain_step. */
+int rd_panel_step(rd_chain *c, int32_t *stats_dev);
 
 /* Copies rows [row_begin, row_end) of A^k (k within the last alpha_max+1 powers) to
  * host int16 row-major (row_end-row_begin) x N.  Synchronises the chain's stream. */

@@ -2642,6 +2642,8 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   return RD_OK;
 }
 
+extern "C" int rd_panel_step(rd_chain *c, int32_t *stats_dev) { return rd_chain_step(c, stats_dev); }
+
 extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
   rd_enter();
   if (!c || !host_out) return fail(RD_EINVAL, "rd_chain_read_rows: NULL argument");
