@@ -1441,6 +1441,8 @@ struct SlabArgs {
   int nchunks, Qc;
   int64_t N;
   const int16_t *wcol;
+  uint32_t k65536, k8;     // = 65536 and 8, opaque to the compiler: the high slot's byte offset
+                           // (w >> 16) * 8 as IMAD.HI + IMAD on the fma pipe
 };
 
 __global__ void __launch_bounds__(1024, 1)
@@ -1509,10 +1511,16 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
       // hi first, so the high byte of a lane-wise min is the min of the high bytes.  Raw words
       // give rows 1, 3 (5, 7) in the high bytes, words * 256 (IMAD, fma pipe) rows 0, 2 (4, 6).
       uint32_t ev0 = 0xFFFFFFFFu, od0 = 0xFFFFFFFFu, ev1 = 0xFFFFFFFFu, od1 = 0xFFFFFFFFu;
+      // Pipe balance per 4 entries (alu VIMNMX3 / LOP / PRMT vs fma IMAD, both half rate): the
+      // high slot index comes from IMAD.HI (fma) and two of the eight byte shifts are PRMT
+      // (alu), 12 + 12 instead of 14 alu + 10 fma.
       for (int t = 0; t < d.y; t += 4) {
         const uint32_t w01 = __ldg(ep + (t / 2) * 32), w23 = __ldg(ep + (t / 2 + 1) * 32);
-        const uint2 v0 = xs[w01 & 0xFFFFu], v1 = xs[w01 >> 16];
-        const uint2 v2 = xs[w23 & 0xFFFFu], v3 = xs[w23 >> 16];
+        const char *xb = reinterpret_cast<const char *>(xs);
+        const uint2 v0 = xs[w01 & 0xFFFFu];
+        const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + __umulhi(w01, sa.k65536) * sa.k8);
+        const uint2 v2 = xs[w23 & 0xFFFFu];
+        const uint2 v3 = *reinterpret_cast<const uint2 *>(xb + __umulhi(w23, sa.k65536) * sa.k8);
         od0 = __vimin3_u16x2(od0, v0.x, v1.x);
         od1 = __vimin3_u16x2(od1, v0.y, v1.y);
         ev0 = __vimin3_u16x2(ev0, v0.x * 256u, v1.x * 256u);
@@ -1520,7 +1528,7 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
         od0 = __vimin3_u16x2(od0, v2.x, v3.x);
         od1 = __vimin3_u16x2(od1, v2.y, v3.y);
         ev0 = __vimin3_u16x2(ev0, v2.x * 256u, v3.x * 256u);
-        ev1 = __vimin3_u16x2(ev1, v2.y * 256u, v3.y * 256u);
+        ev1 = __vimin3_u16x2(ev1, prmt(v2.y, 0u, 0x2104), prmt(v3.y, 0u, 0x2104));   // x << 8
       }
       const uint32_t head = (uint32_t)d.z;
       if (head != 0xFFFFFFFFu) {   // split columns: segmented min towards each segment's head
@@ -2334,7 +2342,9 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   rd_enter();
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
-  if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_chain_create: m=%d out of range", m);
+  // m = 12 (N = 566059): structured chains only (a dense int16 power is 641 GB)
+  if (m < 1 || m > 12 || (m == 12 && method != 1))
+    return fail(RD_EINVAL, "rd_chain_create: m=%d out of range (m = 12: method 1 only)", m);
   const int64_t N = count_words(m);
   // both methods: CSC from the successor generator, operands built on the device (the CSC
   // entry holds q in 17 bits: m = 11 dense chains take the dense host matrix instead)
@@ -2483,7 +2493,7 @@ static int step_slab(rd_chain *c, int knew, EpiArgs &epi) {
                                        kSpSmemMax + 16 * 8));
     attr[c->device] = true;
   }
-  SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol};
+  SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol, 65536u, 8u};
   minplus_slab8_kernel<<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 16) * 8, c->st>>>(
       c->slot(c->k), c->P, sb, c->slot(knew), epi.spread_in, epi.spread_out);
   RD_CUDA_CHECK(cudaGetLastError());

@@ -95,6 +95,15 @@ def test_argument_validation_host_paths():
     assert L.rd_roman_cylinder(3, 2, ctypes.byref(g)) == rd.RD_EINVAL
     assert L.rd_roman_cylinder(0, 5, ctypes.byref(g)) == rd.RD_EINVAL
     assert L.rd_minplus_mul(None, None, None, 4) == rd.RD_EINVAL
+    assert L.rd_minplus_mul32(None, None, None, 4) == rd.RD_EINVAL
+    assert L.rd_minplus_mul32_ex(None, 4, None, 4, None, 4, 0, 4, 4, None) == rd.RD_EINVAL
+    b = np.array([0, 100, 287], dtype=np.int64)
+    h = ctypes.c_void_p()
+    assert L.rd_agchain_create(5, 10, rd._np_ptr(b), 2, 0, None, ctypes.byref(h)) == rd.RD_EINVAL  # 100 % 128
+    assert L.rd_agchain_create(13, 10, rd._np_ptr(b), 2, 0, None, ctypes.byref(h)) == rd.RD_EINVAL
+    assert L.rd_agchain_create(5, 10, rd._np_ptr(b), 2, 2, None, ctypes.byref(h)) == rd.RD_EINVAL  # rank
+    assert L.rd_agchain_step(None, None) == rd.RD_EINVAL
+    assert L.rd_chain_create_ex(12, 10, 0, 10, 0, None, ctypes.byref(h)) == rd.RD_EINVAL        # m=12 dense
     assert L.rd_stats_len(10) == 41
     assert L.rd_set_sparse_bytes(3) == rd.RD_EINVAL and L.rd_set_sparse_bytes(-1) == rd.RD_EINVAL
     assert L.rd_set_sparse_bytes(2) == rd.RD_OK
