@@ -1441,8 +1441,6 @@ struct SlabArgs {
   int nchunks, Qc;
   int64_t N;
   const int16_t *wcol;
-  uint32_t k65536, k8;     // = 65536 and 8, opaque to the compiler: the high slot's byte offset
-                           // (w >> 16) * 8 as IMAD.HI + IMAD on the fma pipe
 };
 
 __global__ void __launch_bounds__(1024, 1)
@@ -1511,16 +1509,10 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
       // hi first, so the high byte of a lane-wise min is the min of the high bytes.  Raw words
       // give rows 1, 3 (5, 7) in the high bytes, words * 256 (IMAD, fma pipe) rows 0, 2 (4, 6).
       uint32_t ev0 = 0xFFFFFFFFu, od0 = 0xFFFFFFFFu, ev1 = 0xFFFFFFFFu, od1 = 0xFFFFFFFFu;
-      // Pipe balance per 4 entries (alu VIMNMX3 / LOP / PRMT vs fma IMAD, both half rate): the
-      // high slot index comes from IMAD.HI (fma) and two of the eight byte shifts are PRMT
-      // (alu), 12 + 12 instead of 14 alu + 10 fma.
       for (int t = 0; t < d.y; t += 4) {
         const uint32_t w01 = __ldg(ep + (t / 2) * 32), w23 = __ldg(ep + (t / 2 + 1) * 32);
-        const char *xb = reinterpret_cast<const char *>(xs);
-        const uint2 v0 = xs[w01 & 0xFFFFu];
-        const uint2 v1 = *reinterpret_cast<const uint2 *>(xb + __umulhi(w01, sa.k65536) * sa.k8);
-        const uint2 v2 = xs[w23 & 0xFFFFu];
-        const uint2 v3 = *reinterpret_cast<const uint2 *>(xb + __umulhi(w23, sa.k65536) * sa.k8);
+        const uint2 v0 = xs[w01 & 0xFFFFu], v1 = xs[w01 >> 16];
+        const uint2 v2 = xs[w23 & 0xFFFFu], v3 = xs[w23 >> 16];
         od0 = __vimin3_u16x2(od0, v0.x, v1.x);
         od1 = __vimin3_u16x2(od1, v0.y, v1.y);
         ev0 = __vimin3_u16x2(ev0, v0.x * 256u, v1.x * 256u);
@@ -1528,7 +1520,7 @@ minplus_slab8_kernel(const uint32_t *__restrict__ X, int64_t ld, SlabArgs sa, ui
         od0 = __vimin3_u16x2(od0, v2.x, v3.x);
         od1 = __vimin3_u16x2(od1, v2.y, v3.y);
         ev0 = __vimin3_u16x2(ev0, v2.x * 256u, v3.x * 256u);
-        ev1 = __vimin3_u16x2(ev1, prmt(v2.y, 0u, 0x2104), prmt(v3.y, 0u, 0x2104));   // x << 8
+        ev1 = __vimin3_u16x2(ev1, v2.y * 256u, v3.y * 256u);
       }
       const uint32_t head = (uint32_t)d.z;
       if (head != 0xFFFFFFFFu) {   // split columns: segmented min towards each segment's head
@@ -2493,7 +2485,7 @@ static int step_slab(rd_chain *c, int knew, EpiArgs &epi) {
                                        kSpSmemMax + 16 * 8));
     attr[c->device] = true;
   }
-  SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol, 65536u, 8u};
+  SlabArgs sb{c->desc, c->lane_col, c->ent8, c->slab_start, c->nchunks, c->Qc, c->N, c->wcol};
   minplus_slab8_kernel<<<(unsigned)(c->Mp / 8), 1024, (size_t)(c->Qc + 16) * 8, c->st>>>(
       c->slot(c->k), c->P, sb, c->slot(knew), epi.spread_in, epi.spread_out);
   RD_CUDA_CHECK(cudaGetLastError());
