@@ -772,3 +772,18 @@ def test_m12_panel_sequential_pins():
         assert d[n] == 26 * n // 5, n
     for n in range(3, 11):
         assert d[n] == O.gamma_rowdp(12, n), n
+
+
+@pytest.mark.parametrize("M,N,K", [(7, 130, 33), (129, 5, 300)])
+def test_minplus_mul32_ex_strided_guard(M, N, K):
+    # leading dimensions larger than the shapes; nothing written outside the N columns of C
+    A = operand(M, K + 3, 61 + M, inf_frac=0.05, hi=2**28, inf=RINF32, dtype=np.int32)
+    B = operand(K, N + 5, 62 + N, inf_frac=0.05, hi=2**28, inf=RINF32, dtype=np.int32)
+    dA, dB = _gpu(A), _gpu(B)
+    dC = torch.full((M, N + 2), -7, dtype=torch.int32, device="cuda")
+    rc = rd.lib().rd_minplus_mul32_ex(dA.data_ptr(), K + 3, dB.data_ptr(), N + 5, dC.data_ptr(), N + 2, M, N, K,
+                                      None)
+    assert rc == rd.RD_OK
+    C = dC.cpu().numpy()
+    assert (C[:, :N] == _oracle_mul32(np.ascontiguousarray(A[:, :K]), np.ascontiguousarray(B[:, :N]))).all()
+    assert (C[:, N:] == -7).all()
