@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 35323029888}   # profiles/r01i_gemm_ncu_summary.txt: 34.342 GB read + 0.981 GB write
+TRAFFIC = {9: 34818964096}   # profiles/r01l_gemm_ncu_summary.txt: 33.840 GB read + 0.979 GB write
 
 
 def parse():
@@ -416,7 +416,10 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         for mm in args.ttp_m:
             if world > 1:
                 dist.barrier()
-            res = rdist.power_sequence(mm, 50, am, broadcast=world > 1)
+            # one GPU: the library's own loop (rd_power_sequence: speculative depth, C decisions);
+            # several: the row-panel driver with the stats all_reduce
+            res = (rd.rd_power_sequence(mm, 50, am) if world == 1
+                   else rdist.power_sequence(mm, 50, am, broadcast=True))
             tt = torch.tensor([res["t_build"], res["t_chain"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -429,7 +432,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             # same results; its Gop/s counts its own terms (rows x nnz(A) per step)
             if world > 1:
                 dist.barrier()
-            rs = rdist.power_sequence(mm, 50, am, method=1)
+            rs = (rd.rd_power_sequence(mm, 50, am, method=1) if world == 1
+                  else rdist.power_sequence(mm, 50, am, method=1))
             ts = torch.tensor([rs["t_build"], rs["t_chain"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(ts, op=dist.ReduceOp.MAX)
@@ -445,7 +449,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         for mm in args.ttp_structured_only_m:
             if world > 1:
                 dist.barrier()
-            rs = rdist.power_sequence(mm, 50, am, method=1)
+            rs = (rd.rd_power_sequence(mm, 50, am, method=1) if world == 1
+                  else rdist.power_sequence(mm, 50, am, method=1))
             ts = torch.tensor([rs["t_build"], rs["t_chain"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(ts, op=dist.ReduceOp.MAX)

@@ -160,6 +160,11 @@ int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t
  *             alpha_max <= 16 for method 1. */
 int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
                           int32_t *diag);
+/* As rd_power_sequence_ex2, also reporting seconds[0] = build (words, A(G), upload, operand
+ * construction) and seconds[1] = the chain to the decision, wall clock (seconds: HOST double[2],
+ * nullable). */
+int rd_power_sequence_timed(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                            int32_t *diag, double *seconds);
 
 /* ---------------------------------------------------------------------------
  * Any matrix: Algorithm 2 / chains over a caller-supplied HOST matrix A (N x N int16

@@ -63,6 +63,8 @@ def lib():
         L.rd_chain_create_ex.argtypes = [ci, ci, i64, i64, ci, p, p]
         L.rd_chain_terms_per_step.argtypes = [p]; L.rd_chain_terms_per_step.restype = ctypes.c_double
         L.rd_power_sequence_ex2.argtypes = [ci, ci, ci, ci, ci, p, p]
+        L.rd_power_sequence_timed.argtypes = [ci, ci, ci, ci, ci, p, p, p]
+        L.rd_power_sequence_timed.restype = ci
         L.rd_power_sequence_matrix.argtypes = [p, i64, ci, ci, ci, ci, p, p]
         L.rd_build_matrix_border.argtypes = [p, p]
         L.rd_chain_create_matrix.argtypes = [p, i64, ci, i64, i64, ci, p, p]
@@ -282,10 +284,11 @@ def rd_power_sequence(m: int, kmax: int = 50, alpha_max: int = 10, policy: int =
     _sync_device()
     out = _Period()
     diag = np.zeros(kmax + 1, dtype=np.int32)
-    rc = _check(lib().rd_power_sequence_ex2(m, kmax, alpha_max, policy, method, ctypes.byref(out),
-                                            _np_ptr(diag)), allow=(RD_OK, RD_NOTFOUND))
+    sec = (ctypes.c_double * 2)()
+    rc = _check(lib().rd_power_sequence_timed(m, kmax, alpha_max, policy, method, ctypes.byref(out),
+                                              _np_ptr(diag), sec), allow=(RD_OK, RD_NOTFOUND))
     return dict(found=bool(out.found), n0=out.n0, alpha=out.alpha, beta=out.beta, k_stop=out.k_stop,
-                diag=[int(x) for x in diag], status=rc)
+                diag=[int(x) for x in diag], status=rc, t_build=sec[0], t_chain=sec[1])
 
 
 def rd_power_sequence_matrix(A: np.ndarray, kmax: int = 50, alpha_max: int = 10, policy: int = 0,

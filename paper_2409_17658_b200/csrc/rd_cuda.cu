@@ -21,6 +21,7 @@
 #include <nvtx3/nvToolsExt.h>   // header-only; ranges cost nothing without an attached tool
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -2106,8 +2107,67 @@ struct rd_chain {
   uint32_t *ent8 = nullptr;
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
+  std::vector<void *> pooled;   // buffers taken from the library's stream-ordered pool
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
 };
+
+// Device memory of chains.  cudaMalloc / cudaFree cost 0.05-20 ms each, depending on the
+// driver's state, and a small-order chain makes ten of them — more than its whole
+// computation (m = 5: 20 power steps in ~0.5 ms).  Buffers up to kPoolMax come from a
+// library-owned stream-ordered pool instead (µs after warm-up; up to 1 GB kept between
+// chains); larger ones (the m >= 9 rings) from cudaMalloc.
+constexpr size_t kPoolMax = (size_t)256 << 20;
+static cudaMemPool_t chain_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      (void)cudaGetLastError();
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = (uint64_t)1 << 30;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+
+template <typename T>
+static cudaError_t chain_malloc(rd_chain *c, T **p, size_t bytes) {
+  *p = nullptr;
+  if (bytes <= kPoolMax) {
+    if (cudaMemPool_t pool = chain_pool(c->device)) {
+      void *q = nullptr;
+      if (cudaMallocFromPoolAsync(&q, bytes, pool, c->st) == cudaSuccess) {
+        c->pooled.push_back(q);
+        *p = reinterpret_cast<T *>(q);
+        return cudaSuccess;
+      }
+      (void)cudaGetLastError();
+    }
+  }
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  *p = reinterpret_cast<T *>(q);
+  return e;
+}
+
+static void chain_free(rd_chain *c, void *p) {
+  if (!p) return;
+  auto it = std::find(c->pooled.begin(), c->pooled.end(), p);
+  if (it != c->pooled.end()) {
+    cudaFreeAsync(p, c->st);
+    c->pooled.erase(it);
+  } else {
+    cudaFree(p);
+  }
+}
 
 // Creates a chain over the host matrix A (N x N int16 row-major, entries in [0, RD_INF]).
 // Ahost == nullptr (method 1 only): the CSC comes straight from the successor generator of
@@ -2150,16 +2210,16 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
 
   int16_t *dA = nullptr;
   auto cleanup = [&](int code) {
-    if (dA) cudaFree(dA);
-    if (c->BP) cudaFree(c->BP);
-    if (c->ring) cudaFree(c->ring);
-    if (c->colptr) cudaFree(c->colptr);
-    if (c->ent) cudaFree(c->ent);
-    if (c->wcol) cudaFree(c->wcol);
-    if (c->spread) cudaFree(c->spread);
+    chain_free(c, dA);
+    chain_free(c, c->BP);
+    chain_free(c, c->ring);
+    chain_free(c, c->colptr);
+    chain_free(c, c->ent);
+    chain_free(c, c->wcol);
+    chain_free(c, c->spread);
     for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
                     (void *)c->ent8})
-      if (p) cudaFree(p);
+      chain_free(c, p);
     delete c;
     return code;
   };
@@ -2208,7 +2268,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
       ent_p = S->uent.data(); ent_n = S->uent.size();
       wcol_p = S->wcol.data(); wcol_n = S->wcol.size();
       auto up = [&](void **dst, const void *src, size_t bytes) {
-        if ((e = cudaMalloc(dst, bytes)) != cudaSuccess) return false;
+        if ((e = chain_malloc(c, dst, bytes)) != cudaSuccess) return false;
         return (e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, c->st)) == cudaSuccess;
       };
       if (!up((void **)&c->perm, S->perm.data(), S->perm.size() * 4) ||
@@ -2230,7 +2290,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
       }
     }
     if (wcol_p) {
-      if ((e = cudaMalloc((void **)&c->wcol, wcol_n * 2)) != cudaSuccess ||
+      if ((e = chain_malloc(c, &c->wcol, wcol_n * 2)) != cudaSuccess ||
           (e = cudaMemcpyAsync(c->wcol, wcol_p, wcol_n * 2, cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
         return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
       if (mode) {
@@ -2238,16 +2298,16 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
         for (size_t i = 0; i < wcol_n; ++i)
           if (wcol_p[i] < RD_INF) mxl = std::max(mxl, wcol_p[i]);
         const int init[2] = {0, mxl > 254 ? 1 : 0};   // flags[1] describes A^1 (row spread <= max label)
-        if ((e = cudaMalloc((void **)&c->spread, 8)) != cudaSuccess ||
+        if ((e = chain_malloc(c, &c->spread, 8)) != cudaSuccess ||
             (e = cudaMemcpyAsync(c->spread, init, 8, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
             (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
           return cleanup(fail(RD_ENOMEM, "rd_chain_create: %s", cudaGetErrorString(e)));
       }
     }
-    if ((e = cudaMalloc((void **)&c->colptr, cp_n * 4)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->ent, ent_n * 4)) != cudaSuccess ||
-        (A && (e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess) ||
-        (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
+    if ((e = chain_malloc(c, &c->colptr, cp_n * 4)) != cudaSuccess ||
+        (e = chain_malloc(c, &c->ent, ent_n * 4)) != cudaSuccess ||
+        (A && (e = chain_malloc(c, &dA, (size_t)(N * N * 2))) != cudaSuccess) ||
+        (e = chain_malloc(c, &c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
       return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
     if ((e = cudaMemcpyAsync(c->colptr, cp_p, cp_n * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
         (e = cudaMemcpyAsync(c->ent, ent_p, ent_n * 4, cudaMemcpyHostToDevice, c->st)) != cudaSuccess ||
@@ -2265,7 +2325,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
       return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
-    cudaFree(dA);
+    chain_free(c, dA);
     dA = nullptr;
     c->k = 1;
     *out = c;
@@ -2283,11 +2343,11 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
       if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
     int32_t *dcp = nullptr;
     uint32_t *dent = nullptr;
-    if ((e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
-        (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess ||
-        (e = cudaMalloc((void **)&dcp, colptr.size() * 4)) != cudaSuccess ||
-        (e = cudaMalloc((void **)&dent, ent.size() * 4)) != cudaSuccess) {
-      if (dcp) cudaFree(dcp);
+    if ((e = chain_malloc(c, &c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
+        (e = chain_malloc(c, &c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess ||
+        (e = chain_malloc(c, &dcp, colptr.size() * 4)) != cudaSuccess ||
+        (e = chain_malloc(c, &dent, ent.size() * 4)) != cudaSuccess) {
+      chain_free(c, dcp);
       return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
     }
     cudaMemcpyAsync(dcp, colptr.data(), colptr.size() * 4, cudaMemcpyHostToDevice, c->st);
@@ -2299,16 +2359,16 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
                                                                                   c->slot(1), c->Mp, c->r0, c->r1);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
-    cudaFree(dcp);
-    cudaFree(dent);
+    chain_free(c, dcp);
+    chain_free(c, dent);
     if (e != cudaSuccess) return cleanup(fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e)));
     c->k = 1;
     *out = c;
     return RD_OK;
   }
-  if ((e = cudaMalloc((void **)&dA, (size_t)(N * N * 2))) != cudaSuccess ||
-      (e = cudaMalloc((void **)&c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
-      (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
+  if ((e = chain_malloc(c, &dA, (size_t)(N * N * 2))) != cudaSuccess ||
+      (e = chain_malloc(c, &c->BP, (size_t)(c->P / 2 * c->P * 4))) != cudaSuccess ||
+      (e = chain_malloc(c, &c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess)
     return cleanup(fail(RD_ENOMEM, "rd_chain_create: device allocation: %s", cudaGetErrorString(e)));
   if ((e = cudaMemcpyAsync(dA, A, (size_t)(N * N * 2), cudaMemcpyHostToDevice, c->st)) != cudaSuccess)
     return cleanup(fail(RD_ECUDA, "rd_chain_create: H2D: %s", cudaGetErrorString(e)));
@@ -2321,7 +2381,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
   if (rc == RD_OK) rc = pack_left(dA, N, c->Mr, N, c->r0, c->slot(1), c->Mp, c->P / 2, c->st);
   if (rc == RD_OK && (e = cudaStreamSynchronize(c->st)) != cudaSuccess)
     rc = fail(RD_ECUDA, "rd_chain_create: %s", cudaGetErrorString(e));
-  cudaFree(dA);
+  chain_free(c, dA);
   dA = nullptr;
   if (rc != RD_OK) return cleanup(rc);
   c->k = 1;
@@ -2395,8 +2455,8 @@ extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, i
   c->diag1 = diag1;
   cudaError_t e;
   const size_t bp_bytes = (size_t)(c->P / 2 * c->P * 4);
-  if ((e = cudaMalloc((void **)&c->BP, bp_bytes)) != cudaSuccess ||
-      (e = cudaMalloc((void **)&c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess) {
+  if ((e = chain_malloc(c, &c->BP, bp_bytes)) != cudaSuccess ||
+      (e = chain_malloc(c, &c->ring, (size_t)((alpha_max + 1) * c->slot_words * 4))) != cudaSuccess) {
     rd_chain_destroy(c);
     return fail(RD_ENOMEM, "rd_chain_create_packed: %s", cudaGetErrorString(e));
   }
@@ -2532,13 +2592,13 @@ extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t 
 
 extern "C" int rd_chain_destroy(rd_chain *c) {
   if (!c) return RD_OK;
-  if (c->BP) cudaFree(c->BP);
-  if (c->ring) cudaFree(c->ring);
-  if (c->colptr) cudaFree(c->colptr);
-  if (c->ent) cudaFree(c->ent);
-  if (c->wcol) cudaFree(c->wcol);
-  if (c->ws) cudaFree(c->ws);
-  if (c->spread) cudaFree(c->spread);
+  chain_free(c, c->BP);
+  chain_free(c, c->ring);
+  chain_free(c, c->colptr);
+  chain_free(c, c->ent);
+  chain_free(c, c->wcol);
+  chain_free(c, c->ws);
+  chain_free(c, c->spread);
   for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
                   (void *)c->ent8})
     if (p) cudaFree(p);
@@ -2620,9 +2680,9 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
     if (rc != RD_OK) return rc;
   } else {
     if (!c->ws || c->nsplit < nsplit) {
-      if (c->ws) cudaFree(c->ws);
+      chain_free(c, c->ws);
       c->ws = nullptr;
-      RD_CUDA_CHECK(cudaMalloc((void **)&c->ws, (size_t)nsplit * c->slot_words * 4));
+      RD_CUDA_CHECK(chain_malloc(c, &c->ws, (size_t)nsplit * c->slot_words * 4));
       c->nsplit = nsplit;
     }
     EpiArgs ge{};
@@ -2893,9 +2953,10 @@ static int power_sequence_check(int kmax, int alpha_max, int policy, int method,
 static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
                               rd_period_t *out, int32_t *diag);
 
-extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
-                                     int32_t *diag) {
+extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                                       int32_t *diag, double *seconds) {
   rd_enter();
+  const auto t0 = std::chrono::steady_clock::now();
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
   if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, 2 * m, out, diag)) return rc0;
   const int64_t N = count_words(m);
@@ -2904,7 +2965,18 @@ extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy,
   rd_chain *c = nullptr;
   int rc = rd_chain_create_ex(m, alpha_max, 0, N, method, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
-  return power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
+  const auto t1 = std::chrono::steady_clock::now();
+  rc = power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
+  if (seconds) {
+    seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+    seconds[1] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  }
+  return rc;
+}
+
+extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
+                                     int32_t *diag) {
+  return rd_power_sequence_timed(m, kmax, alpha_max, policy, method, out, diag, nullptr);
 }
 
 extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, int alpha_max, int policy,
@@ -2937,11 +3009,35 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
   int32_t *dstats = nullptr, *hstats = nullptr;
   std::vector<cudaEvent_t> ev(depth, nullptr);
   cudaError_t e;
-  if ((e = cudaMalloc((void **)&dstats, (size_t)slen * 4 * depth)) != cudaSuccess ||
-      (e = cudaMallocHost((void **)&hstats, (size_t)slen * 4 * depth)) != cudaSuccess) {
+  // the pinned stats mirror is kept per thread across calls (cudaMallocHost costs ~0.1-1 ms,
+  // as much as a whole small-order chain)
+  static thread_local int32_t *t_hstats = nullptr;
+  static thread_local size_t t_hwords = 0;
+  const size_t hwords = (size_t)slen * depth;
+  if (t_hwords < hwords) {
+    if (t_hstats) cudaFreeHost(t_hstats);
+    t_hstats = nullptr;
+    t_hwords = 0;
+    if ((e = cudaMallocHost((void **)&t_hstats, hwords * 4)) != cudaSuccess) {
+      t_hstats = nullptr;
+      rd_chain_destroy(c);
+      cudaStreamDestroy(st);
+      return fail(RD_ENOMEM, "rd_power_sequence: %s", cudaGetErrorString(e));
+    }
+    t_hwords = hwords;
+  }
+  hstats = t_hstats;
+  cudaMemPool_t pool = chain_pool(c->device);
+  if (pool) {
+    if (cudaMallocFromPoolAsync((void **)&dstats, (size_t)slen * 4 * depth, pool, st) != cudaSuccess) {
+      (void)cudaGetLastError();
+      dstats = nullptr;
+      pool = nullptr;
+    }
+  }
+  if (!dstats && (e = cudaMalloc((void **)&dstats, (size_t)slen * 4 * depth)) != cudaSuccess) {
     rd_chain_destroy(c);
     cudaStreamDestroy(st);
-    if (dstats) cudaFree(dstats);
     return fail(RD_ENOMEM, "rd_power_sequence: %s", cudaGetErrorString(e));
   }
   for (int q = 0; q < depth; ++q) cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
@@ -2983,8 +3079,7 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
   cudaStreamSynchronize(st);
   for (int q = 0; q < depth; ++q) cudaEventDestroy(ev[q]);
   int k_stop = std::min(k, kmax);
-  cudaFree(dstats);
-  cudaFreeHost(hstats);
+  if (pool) cudaFreeAsync(dstats, st); else cudaFree(dstats);
   rd_chain_destroy(c);
   cudaStreamDestroy(st);
   if (rc != RD_OK) return rc;
