@@ -517,9 +517,9 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                        "k_range": [2 + args.warmup, 1 + args.warmup + args.steps]},
             "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "Gop/s",
                          "frac": round(achieved / peak, 4), "traffic": TRAFFIC.get(m) if args.form == "replicated" else None,
-                         # compulsory DRAM bytes per launch: X, B, C (2N^2 B each at int16) + the
-                         # alpha_max earlier powers the fused periodicity test reads
-                         "algorithmic_bytes": int((3 + am) * 2 * N * N),
+                         # compulsory DRAM bytes per launch: B (2N^2 B at int16), the panel's X and
+                         # C, and the alpha_max earlier powers the fused periodicity test reads
+                         "algorithmic_bytes": int(2 * N * N + (2 + am) * 2 * (r1 - r0) * N),
                          "kernel": "minplus_gemm_kernel<RP,STATS,3> (peer B)" if args.form == "peer"
                                    else "minplus_gemm_kernel<PM,STATS,3>",
                          "peak_basis": "unit-count bound: 148 SMs x 192 (min,+)/clk/SM x 1965 MHz (alu 2 + fma 2 warp-instr/clk/SM, issue 4; "
