@@ -2951,7 +2951,8 @@ static int power_sequence_check(int kmax, int alpha_max, int policy, int method,
 }
 
 static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
-                              rd_period_t *out, int32_t *diag);
+                              rd_period_t *out, int32_t *diag,
+                              std::chrono::steady_clock::time_point *t_done = nullptr);
 
 extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
                                        int32_t *diag, double *seconds) {
@@ -2966,10 +2967,11 @@ extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int polic
   int rc = rd_chain_create_ex(m, alpha_max, 0, N, method, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
   const auto t1 = std::chrono::steady_clock::now();
-  rc = power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
-  if (seconds) {
+  auto t2 = t1;
+  rc = power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag, &t2);
+  if (seconds) {   // the chain ends when the decision is taken and the issued work is done
     seconds[0] = std::chrono::duration<double>(t1 - t0).count();
-    seconds[1] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    seconds[1] = std::chrono::duration<double>(t2 - t1).count();
   }
   return rc;
 }
@@ -2995,7 +2997,7 @@ extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, i
 
 // Algorithm 2's loop over a created chain (consumes c and st).
 static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
-                              rd_period_t *out, int32_t *diag) {
+                              rd_period_t *out, int32_t *diag, std::chrono::steady_clock::time_point *t_done) {
   NvtxRange nvtx_range("rd_power_sequence");
   const int64_t N = c->N;
   int rc = RD_OK;
@@ -3003,8 +3005,9 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
   // Speculative depth: up to `depth` power steps are enqueued ahead of the host decision,
   // each with its own stats slot and async D2H copy, so launch and sync latency overlap the
   // GEMMs of small orders.  Steps issued past the detecting power are discarded (their
-  // results are never read).  Large orders use depth 1: a step there is 10-300 ms.
-  const int depth = method == 1 ? 4 : (N >= 7000 ? 1 : (N >= 2000 ? 2 : 8));
+  // results are never read).  Large orders use depth 1 (dense) or 2 (structured): a step
+  // there is 4-300 ms and each speculative step past the decision is wasted work.
+  const int depth = method == 1 ? (N >= 7000 ? 2 : 4) : (N >= 7000 ? 1 : (N >= 2000 ? 2 : 8));
   const int slen = rd_stats_len(alpha_max);
   int32_t *dstats = nullptr, *hstats = nullptr;
   std::vector<cudaEvent_t> ev(depth, nullptr);
@@ -3077,6 +3080,7 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
     }
   }
   cudaStreamSynchronize(st);
+  if (t_done) *t_done = std::chrono::steady_clock::now();
   for (int q = 0; q < depth; ++q) cudaEventDestroy(ev[q]);
   int k_stop = std::min(k, kmax);
   if (pool) cudaFreeAsync(dstats, st); else cudaFree(dstats);
