@@ -147,6 +147,7 @@ def test_power_sequence_matches_oracle(m):
     got = rd.rd_power_sequence(m, 50)
     for key in ("found", "n0", "alpha", "beta", "k_stop"):
         assert got[key] == ref[key], (m, key)
+    assert got["t_build"] > 0 and got["t_chain"] > 0          # rd_power_sequence_timed
     assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
 
 
