@@ -2665,14 +2665,32 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
     c->k = knew;
     return RD_OK;
   }
-  // small grids (< 3 waves of 2 CTAs x 148 SMs) split K so the machine fills; the partial
-  // tiles are combined, stored and reduced by combine_pm_kernel
+  // Split K over nsplit CTAs per tile when that shortens the wave-quantised grid: the step
+  // takes ceil(ntiles * n / slots) waves of kstages / n pipeline stages each (slots = 2 CTAs x
+  // the SM count), plus, for n > 1, combine_pm_kernel's HBM passes: the n partial tiles, the
+  // stored power and the nprev earlier powers its stats read (~(n + 2 + nprev) slots at
+  // ~6 TB/s; one stage of a 128 x 128 tile is ~8.2 us at the measured mix rate with 2 CTAs
+  // per SM; a CTA's pipeline fill and epilogue cost ~2 stages).  A split must promise >= 3%;
+  // each keeps >= 2 stages.  Measured (tools/split_probe.py): m = 6 0.096 -> 0.053 ms, m = 8
+  // 8-rank panel 1.97 -> 1.59 ms, m = 7 and full m = 8 / m = 9 panels within 1% of no split.
   const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
   const int64_t kstages = (c->P / 2) / kBK2;
-  // aim for >= 4 waves of 2 x 148 CTAs; each split keeps >= 2 pipeline stages of k
-  int nsplit = (int)std::min<int64_t>(8, std::max<int64_t>(1, (1184 + ntiles - 1) / ntiles));
-  if (ntiles >= 888) nsplit = 1;
-  while (nsplit > 1 && kstages < 2 * nsplit) --nsplit;
+  int nsplit = 1;
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int64_t slots = 2 * (int64_t)sms;
+    const double t_stage = 8.2e-6, bw = 6.0e12, slot_bytes = 4.0 * (double)c->slot_words;
+    double best = 0.0, cost1 = 0.0;
+    for (int n = 1; n <= 8 && kstages >= 2 * n; ++n) {
+      const double waves = (double)((ntiles * n + slots - 1) / slots);
+      double cost = waves * ((double)kstages / n + 2.0);   // + pipeline fill / epilogue per CTA
+      if (n > 1) cost += (n + 2 + epi.nprev) * slot_bytes / bw / t_stage;
+      if (n == 1) cost1 = cost;
+      if (n == 1 || cost < best) { best = cost; nsplit = n; }
+    }
+    if (best > 0.97 * cost1) nsplit = 1;
+  }
   if (g_split_k_off) nsplit = 1;
   if (nsplit == 1) {
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
