@@ -222,9 +222,9 @@ typedef struct rd_chain rd_chain;
 
 /* Builds A(G) on the host, uploads it, packs the right operand once, places rows
  * [row_begin, row_end) of A^1 in ring slot 1.  alpha_max 1..32.  cuda_stream: all
- * work of this chain is enqueued on it (NULL = legacy default); buffers up to 256 MB come
- * from the library's stream-ordered pool on that stream, so the stream must outlive the
- * chain (rd_chain_destroy releases them on it). */
+ * work of this chain is enqueued on it (NULL = legacy default); its buffers come from the
+ * library's stream-ordered pool on that stream (up to 16 GB stay mapped between chains), so
+ * the stream must outlive the chain (rd_chain_destroy releases them on it). */
 int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
                     rd_chain **out);
 int rd_chain_destroy(rd_chain *c);

@@ -2111,12 +2111,14 @@ struct rd_chain {
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
 };
 
-// Device memory of chains.  cudaMalloc / cudaFree cost 0.05-20 ms each, depending on the
-// driver's state, and a small-order chain makes ten of them — more than its whole
-// computation (m = 5: 20 power steps in ~0.5 ms).  Buffers up to kPoolMax come from a
-// library-owned stream-ordered pool instead (µs after warm-up; up to 1 GB kept between
-// chains); larger ones (the m >= 9 rings) from cudaMalloc.
-constexpr size_t kPoolMax = (size_t)256 << 20;
+// Device memory of chains.  cudaMalloc / cudaFree cost 0.05-20 ms each for small buffers
+// and up to ~1 s to unmap a 10 GB ring, depending on the driver's state, while a small-order
+// chain computes in ~0.5 ms (m = 5).  Chain buffers come from a library-owned stream-ordered
+// pool instead (µs once warm); up to kPoolKeep bytes stay mapped between chains (an m = 9
+// dense chain's ring + packed operand is 11.7 GB), anything beyond is returned at the next
+// synchronisation.  cudaMalloc is the fallback when the pool cannot grow.
+constexpr size_t kPoolMax = ~(size_t)0;
+constexpr uint64_t kPoolKeep = (uint64_t)16 << 30;
 static cudaMemPool_t chain_pool(int dev) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
@@ -2132,7 +2134,7 @@ static cudaMemPool_t chain_pool(int dev) {
       pools[dev] = nullptr;
       return nullptr;
     }
-    uint64_t thr = (uint64_t)1 << 30;
+    uint64_t thr = kPoolKeep;
     cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
   }
   return pools[dev];
