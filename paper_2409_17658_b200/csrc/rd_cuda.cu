@@ -2116,9 +2116,10 @@ struct rd_chain {
 // chain computes in ~0.5 ms (m = 5).  Chain buffers come from a library-owned stream-ordered
 // pool instead (µs once warm); up to kPoolKeep bytes stay mapped between chains (an m = 9
 // dense chain's ring + packed operand is 11.7 GB), anything beyond is returned at the next
-// synchronisation.  cudaMalloc is the fallback when the pool cannot grow.
-constexpr size_t kPoolMax = ~(size_t)0;
+// synchronisation.  Buffers above kPoolMax (the m >= 10 rings: growing the pool by 92 GB took
+// 9 s against 0.5 s for cudaMalloc) and allocations the pool cannot serve use cudaMalloc.
 constexpr uint64_t kPoolKeep = (uint64_t)16 << 30;
+constexpr size_t kPoolMax = (size_t)kPoolKeep;
 static cudaMemPool_t chain_pool(int dev) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
