@@ -788,3 +788,17 @@ def test_minplus_mul32_ex_strided_guard(M, N, K):
     C = dC.cpu().numpy()
     assert (C[:, :N] == _oracle_mul32(np.ascontiguousarray(A[:, :K]), np.ascontiguousarray(B[:, :N]))).all()
     assert (C[:, N:] == -7).all()
+
+
+def test_minplus_mul32_large_sampled_rows():
+    # the 32-bit product at a bench-like size (N = 7411, uniform [0, 2^29), 1% inf): sampled
+    # output rows recomputed by the oracle through B's transpose
+    N = 7411
+    A = operand(N, N, 71, inf_frac=0.01, hi=2**29 - 1, inf=RINF32, dtype=np.int32)
+    B = operand(N, N, 72, inf_frac=0.01, hi=2**29 - 1, inf=RINF32, dtype=np.int32)
+    C = rd.rd_minplus_mul32(_gpu(A), _gpu(B)).cpu().numpy()
+    rows = sample_rows(N, 12, seed=73)
+    Ao = to_inf(A[rows], RINF32, OINF, np.int32)
+    BT = np.ascontiguousarray(to_inf(B, RINF32, OINF, np.int32).T)
+    want = to_inf(O.minplus_bt(Ao, BT), OINF, RINF32, np.int32)
+    assert (C[rows] == want).all()
