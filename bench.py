@@ -521,7 +521,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                          # C, and the alpha_max earlier powers the fused periodicity test reads
                          "algorithmic_bytes": int(2 * N * N + (2 + am) * 2 * (r1 - r0) * N),
                          "kernel": "minplus_gemm_kernel<RP,STATS,3> (peer B)" if args.form == "peer"
-                                   else "minplus_gemm_kernel<PM,STATS,3>",
+                                   else ("minplus_gemm_kernel<PM,STATS,3,TMA>" if (N + 127) // 128 * 64 // 32 >= 128
+                                         else "minplus_gemm_kernel<PM,STATS,3>"),
                          "peak_basis": "unit-count bound: 148 SMs x 192 (min,+)/clk/SM x 1965 MHz (alu 2 + fma 2 warp-instr/clk/SM, issue 4; "
                                        "best mix 1 VIADDMNMX.S16x2 : 1 [2 IMAD + 1 VIMNMX3.S16x2]; DESIGN.md 5)",
                          "dpx_issue_peak": round(dpx_peak, 1), "frac_of_dpx_issue_peak": round(achieved / dpx_peak, 4),

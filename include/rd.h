@@ -339,6 +339,14 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 
+/* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
+ * one thread streams each 64-k-pair stage of both operands (cp.async.bulk.tensor, completion
+ * counted on an mbarrier; the warps release stages on a second mbarrier); without, every
+ * thread issues cp.async and the CTA meets at __syncthreads.  mode 0 = cp.async always;
+ * 1 (default) = TMA for single-pass steps of >= 128 stages (the m >= 9 orders); 2 = TMA
+ * always.  Identical results.  RD_EINVAL outside 0..2. */
+int rd_set_gemm_tma(int mode);
+
 /* rd_set_split_k — process-wide switch (default on) of split-K in dense chain steps whose
  * grid is under 3 waves (2 CTAs x the SM count): the k-range is split over 2 or 4 CTAs per
  * tile and a combine kernel takes the min, stores the power and computes the stats.

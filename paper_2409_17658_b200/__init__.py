@@ -84,6 +84,8 @@ def lib():
         L.rd_set_gemm_variant.argtypes = [ci]
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
+        L.rd_set_gemm_tma.argtypes = [ci]
+        L.rd_set_gemm_tma.restype = ci
         L.rd_set_sparse_bytes.argtypes = [ci]
         L.rd_minplus_mul32.argtypes = [p, p, p, i64]
         L.rd_minplus_mul32_ex.argtypes = [p, i64, p, i64, p, i64, i64, i64, i64, p]
@@ -315,6 +317,14 @@ def rd_roman_cylinder(m: int, n: int) -> int:
 def rd_set_gemm_variant(dpx_cols: int):
     """Mainloop instruction mix (rd.h): dpx_cols in {0, 2, 3, 4, 8}."""
     _check(lib().rd_set_gemm_variant(dpx_cols))
+
+
+def rd_set_gemm_tma(mode):
+    """Mainloop loads of dense chain steps (rd.h rd_set_gemm_tma): 0 cp.async, 1 auto (default:
+    TMA for long single-pass steps), 2 TMA always; True = 2, False = 0."""
+    if isinstance(mode, bool):
+        mode = 2 if mode else 0
+    _check(lib().rd_set_gemm_tma(int(mode)))
 
 
 def rd_set_split_k(enable: bool):

@@ -17,6 +17,8 @@
 // The accumulators start at INF; min(lo, hi) in the epilogue finishes the k-reduction.
 // The GEMM writes its output C = A^{k+1} directly in the PM layout (pairs along j), so
 // the output of one power step is the left operand of the next one.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>   // header-only; ranges cost nothing without an attached tool
 
@@ -198,6 +200,46 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// mbarrier + TMA (cp.async.bulk.tensor) primitives for the TMA mainloop
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "RD_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra RD_WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// Tensor maps of a dense chain's operands for the TMA mainloop: X = the ring of PM slots
+// ({Mp, P/2, slots} u32, box 128 x 32 x 1), B = the packed operand ({P, P/2} u32, box 128 x 32).
+struct TmaOps {
+  CUtensorMap x, b;
+  int xslot;
+};
+
 // One CTA computes a 128 x 128 tile of C; 256 threads in a 16 x 16 grid, each thread an
 // 8 x 8 register micro-tile: rows {ty*4 + 0..3, 64 + ty*4 + 0..3}, columns
 // {tx*4 + 0..3, 64 + tx*4 + 0..3}.  Per k-pair a thread reads 4 x LDS.128 and issues 64
@@ -227,12 +269,19 @@ struct PeerB {
   int n;
 };
 
-template <int OUT, bool STATS, int DPXC>
+template <int OUT, bool STATS, int DPXC, bool TMA = false>
 __global__ void __launch_bounds__(kThreads, 2)
 minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
                     int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
-                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb) {
-  extern __shared__ __align__(16) uint32_t smem[];
+                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb,
+                    const __grid_constant__ TmaOps tma) {
+  extern __shared__ __align__(16) uint32_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  // TMA writes need an aligned destination: the TMA variant is launched with 1 KB extra
+  // dynamic shared memory and rounds its stage base up to 1 KB
+  uint32_t *smem = smem_raw;
+  if constexpr (TMA)
+    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 4u;
   const int tid = threadIdx.x;
   // a warp covers 4 (ty) x 8 (tx) threads of the 16 x 16 grid: its fragment loads touch 4 and 8
   // distinct 16-byte chunks (one shared-memory wavefront each)
@@ -285,19 +334,46 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   const int KBt = kpairs / kBK2;
   const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
   const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
+  // TMA mainloop: thread 0 issues two bulk-tensor copies per stage (32 KB, completion counted
+  // on full_bar[s]); every warp releases a consumed stage on empty_bar[s]; thread 0 refills
+  // it once all 8 warps have.  No per-thread copy instructions, no CTA-wide barrier.
+  auto tma_issue = [&](int s, int kb) {
+    uint32_t *sx = smem + s * kStageWords;
+    mbar_expect_tx(&full_bar[s], (uint32_t)(kStageWords * 4));
+    tma_load_3d(sx, &tma.x, &full_bar[s], (int)i0, (kb0 + kb) * kBK2, tma.xslot);
+    tma_load_2d(sx + kBK2 * kTile, &tma.b, &full_bar[s], (int)j0, (kb0 + kb) * kBK2);
+  };
+  if constexpr (TMA) {
+    if (tid == 0) {
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (s < KB) load_stage(s, kb0 + s);
-    cp_async_commit();
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&full_bar[s], 1);
+        mbar_init(&empty_bar[s], kThreads / 32);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int s = 0; s < kStages && s < KB; ++s) tma_issue(s, s);
+  } else {
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+      if (s < KB) load_stage(s, kb0 + s);
+      cp_async_commit();
+    }
   }
 
   for (int kb = 0; kb < KB; ++kb) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
-    {
-      int nk = kb + kStages - 1;
-      if (nk < KB) load_stage(nk % kStages, kb0 + nk);
-      cp_async_commit();
+    if constexpr (TMA) {
+      mbar_wait(&full_bar[kb % kStages], (uint32_t)((kb / kStages) & 1));
+    } else {
+      cp_async_wait<kStages - 2>();
+      __syncthreads();
+      {
+        int nk = kb + kStages - 1;
+        if (nk < KB) load_stage(nk % kStages, kb0 + nk);
+        cp_async_commit();
+      }
     }
     const uint32_t *sx = smem + (kb % kStages) * kStageWords;
     const uint32_t *sb = sx + kBK2 * kTile;
@@ -350,8 +426,17 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           }
       }
     }
+    if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages
+      const int s = kb % kStages;
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty_bar[s]);
+      if (tid == 0 && kb + kStages < KB) {
+        mbar_wait(&empty_bar[s], (uint32_t)((kb / kStages) & 1));
+        tma_issue(s, kb + kStages);
+      }
+    }
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
 
   // ---------------------------------------------------------------- epilogue --
   // v = min(lo, hi) per accumulator; pairs (c, c+1) packed (min_c | min_{c+1} << 16).
@@ -714,21 +799,25 @@ template <int DPXC>
 int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
                     int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st);
 
-template <int OUT, bool STATS, int DPXC>
+template <int OUT, bool STATS, int DPXC, bool TMA = false>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                  cudaStream_t st, int nsplit, const PeerB &pb) {
+                  cudaStream_t st, int nsplit, const PeerB &pb, const TmaOps *tma = nullptr) {
   static bool attr_set[64] = {};
   int dev = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC, TMA>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kSmemBytes + (TMA ? 1024 : 0))));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
-  minplus_gemm_kernel<OUT, STATS, DPXC><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads, kSmemBytes, st>>>(
-      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb);
+  TmaOps t{};
+  if (tma) t = *tma;
+  minplus_gemm_kernel<OUT, STATS, DPXC, TMA><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads,
+                                              kSmemBytes + (TMA ? 1024 : 0), st>>>(
+      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb, t);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
 }
@@ -736,8 +825,19 @@ int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t l
 template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                cudaStream_t st, int nsplit = 1) {
+                cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr) {
   const PeerB pb{};
+  if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
+#define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
+    switch (g_dpx_cols) {
+      case 0: return RD_LGT(0);
+      case 2: return RD_LGT(2);
+      case 3: return RD_LGT(3);
+      case 4: return RD_LGT(4);
+      default: return RD_LGT(8);
+    }
+#undef RD_LGT
+  }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
   switch (g_dpx_cols) {
     case 0: return RD_LG(0);
@@ -2108,6 +2208,8 @@ struct rd_chain {
   int nchunks = 0, Qc = 0;
   int64_t nnz = 0;
   std::vector<void *> pooled;   // buffers taken from the library's stream-ordered pool
+  TmaOps tma{};                 // dense chains: tensor maps of the ring and packed operand
+  bool tma_ready = false;
   uint32_t *slot(int k) const { return ring + (int64_t)(k % (alpha_max + 1)) * slot_words; }
 };
 
@@ -2501,6 +2603,55 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
+// rd_set_gemm_tma: 0 = cp.async mainloop always; 1 (default) = TMA mainloop for single-pass
+// steps of >= 128 pipeline stages (measured: m = 9 274.2 vs 277.0 ms; with fewer stages per
+// CTA — split-K, m <= 8 — the single-thread issue costs 3-8 %); 2 = TMA always.
+static int g_gemm_tma = 1;
+
+extern "C" int rd_set_gemm_tma(int mode) {
+  rd_enter();
+  if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_gemm_tma: mode must be 0, 1 or 2");
+  g_gemm_tma = mode;
+  return RD_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    (void)cudaGetLastError();
+  });
+  return fn;
+}
+
+// Tensor maps of a dense chain: the ring as {Mp, P/2, alpha_max+1} u32 and the packed operand
+// as {P, P/2} u32, boxes of 128 x 32 (one pipeline stage of one operand), no swizzle (the
+// shared-memory layout of the cp.async path).
+static int chain_tma_prepare(rd_chain *c) {
+  if (c->tma_ready) return RD_OK;
+  auto enc = tma_encode_fn();
+  if (!enc) return fail(RD_ECUDA, "rd_chain_step: cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t xd[3] = {(cuuint64_t)c->Mp, (cuuint64_t)(c->P / 2), (cuuint64_t)(c->alpha_max + 1)};
+  const cuuint64_t xs[2] = {(cuuint64_t)c->Mp * 4, (cuuint64_t)c->slot_words * 4};
+  const cuuint32_t box3[3] = {(cuuint32_t)kTile, (cuuint32_t)kBK2, 1}, es3[3] = {1, 1, 1};
+  CUresult r = enc(&c->tma.x, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, c->ring, xd, xs, box3, es3,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RD_ECUDA, "rd_chain_step: tensor map of the ring: CUresult %d", (int)r);
+  const cuuint64_t bd[2] = {(cuuint64_t)c->P, (cuuint64_t)(c->P / 2)};
+  const cuuint64_t bs[1] = {(cuuint64_t)c->P * 4};
+  const cuuint32_t box2[2] = {(cuuint32_t)kTile, (cuuint32_t)kBK2}, es2[2] = {1, 1};
+  r = enc(&c->tma.b, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, c->BP, bd, bs, box2, es2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RD_ECUDA, "rd_chain_step: tensor map of the packed operand: CUresult %d", (int)r);
+  c->tma_ready = true;
+  return RD_OK;
+}
 
 extern "C" int rd_set_sparse_bytes(int enable) {
   rd_enter();
@@ -2695,9 +2846,15 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
     if (best > 0.97 * cost1) nsplit = 1;
   }
   if (g_split_k_off) nsplit = 1;
+  const TmaOps *tma = nullptr;
+  if (g_gemm_tma == 2 || (g_gemm_tma == 1 && nsplit == 1 && kstages >= 128)) {
+    if (int rc = chain_tma_prepare(c)) return rc;
+    c->tma.xslot = c->k % (c->alpha_max + 1);
+    tma = &c->tma;
+  }
   if (nsplit == 1) {
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st);
+                                     c->N, c->Mp, c->P, epi, c->st, 1, tma);
     if (rc != RD_OK) return rc;
   } else {
     if (!c->ws || c->nsplit < nsplit) {
@@ -2709,7 +2866,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
     EpiArgs ge{};
     ge.split_stride = c->slot_words;
     int rc = launch_gemm<true, false>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->ws, c->Mp, c->Mr, c->N, c->Mp,
-                                      c->P, ge, c->st, nsplit);
+                                      c->P, ge, c->st, nsplit, tma);
     if (rc != RD_OK) return rc;
     int dev = c->device, sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

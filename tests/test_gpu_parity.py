@@ -802,3 +802,22 @@ def test_minplus_mul32_large_sampled_rows():
     BT = np.ascontiguousarray(to_inf(B, RINF32, OINF, np.int32).T)
     want = to_inf(O.minplus_bt(Ao, BT), OINF, RINF32, np.int32)
     assert (C[rows] == want).all()
+
+
+@pytest.mark.parametrize("m,r0,r1", [(6, 0, 848), (7, 0, 2507), (8, 1000, 2999)])
+def test_tma_mainloop_bit_identical(m, r0, r1):
+    # the TMA + mbarrier mainloop (forced on, incl. split-K steps) = the cp.async mainloop,
+    # powers and stats, for whole and partial panels
+    def run(mode):
+        rd.rd_set_gemm_tma(mode)
+        try:
+            ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+            st = [ch.step().cpu().numpy().copy() for _ in range(7)]
+            rows = ch.read_rows(ch.k)
+            ch.close()
+        finally:
+            rd.rd_set_gemm_tma(1)
+        return np.stack(st), rows
+    s0, x0 = run(0)
+    s2, x2 = run(2)
+    assert (s0 == s2).all() and (x0 == x2).all()
