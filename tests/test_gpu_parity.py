@@ -821,3 +821,24 @@ def test_tma_mainloop_bit_identical(m, r0, r1):
     s0, x0 = run(0)
     s2, x2 = run(2)
     assert (s0 == s2).all() and (x0 == x2).all()
+
+
+@pytest.mark.parametrize("m,method", [(8, 0), (8, 1), (9, 0), (9, 1)])
+def test_v24_checksums_full_size(m, method, golden):
+    # every entry of A^1..A^5 at the full m = 8 / m = 9 size, through word-order-invariant sums
+    # (#inf, sum of finite entries, sum of the finite diagonal) produced at survey time by an
+    # independent model (tests/golden/survey_checksums_v24.json)
+    want = golden("survey_checksums_v24.json")["checksums"][str(m)]
+    ch = rd.Chain(m, alpha_max=5, method=method)
+    for k in range(1, 6):
+        if k > 1:
+            ch.step()
+        if str(k) not in want:
+            continue
+        X = ch.read_rows(k)
+        fin = X < RINF
+        got = [int((~fin).sum()), int(X[fin].astype(np.int64).sum()),
+               int(np.diag(X)[np.diag(fin)].astype(np.int64).sum())]
+        assert got == want[str(k)], (m, method, k)
+        del X, fin
+    ch.close()
