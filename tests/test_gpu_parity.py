@@ -842,3 +842,12 @@ def test_v24_checksums_full_size(m, method, golden):
         assert got == want[str(k)], (m, method, k)
         del X, fin
     ch.close()
+
+
+def test_structured_chain_nnz_pins_m9_m10():
+    # the library's CSC of A(G) has the survey's independent arc counts: nnz = 2 656 733 at m = 9
+    # (V11) and 13 327 868 at m = 10 (V27); rows * nnz terms per structured step
+    for m, nnz in ((9, 2656733), (10, 13327868)):
+        ch = rd.Chain(m, alpha_max=5, row_begin=0, row_end=8, method=1)
+        assert ch.terms_per_step == 8 * nnz, m
+        ch.close()
