@@ -243,7 +243,10 @@ struct TmaOps {
 // One CTA computes a 128 x 128 tile of C; 256 threads in a 16 x 16 grid, each thread an
 // 8 x 8 register micro-tile: rows {ty*4 + 0..3, 64 + ty*4 + 0..3}, columns
 // {tx*4 + 0..3, 64 + tx*4 + 0..3}.  Per k-pair a thread reads 4 x LDS.128 and issues 64
-// VIADDMNMX.S16x2 (128 (min,+) terms).
+// VIADDMNMX.S16x2 (128 (min,+) terms).  Stages of 32 k-pairs of both operands (32 KB) flow
+// through a 3-deep shared-memory ring, filled either by every thread's cp.async (TMA =
+// false) or, TMA = true (kOutPM only), by one thread's two cp.async.bulk.tensor copies per
+// stage with mbarrier completion and per-warp release (DESIGN.md §5 "Mainloop loads").
 //   OUT = kOutPM : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
 //   OUT = kOutRow: C is row-major int16 with ldc, predicated to (M, N).
 //   OUT = kOutRP : C is RP u32 [M/2][ldc] (pairs along i: C[2p][j] | C[2p+1][j] << 16), and the
