@@ -2758,7 +2758,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
   chain_free(c, c->spread);
   for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
                   (void *)c->ent8})
-    if (p) cudaFree(p);
+    chain_free(c, p);
   delete c;
   return RD_OK;
 }
