@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 38589946000}   # profiles/r01q_gemm_ncu_summary.txt (TMA mainloop): 37.515 GB read + 1.075 GB write
+TRAFFIC = {9: 37751291136}   # profiles/r01r_gemm_ncu_summary.txt (TMA mainloop, final code): 36.676 GB read + 1.075 GB write
 
 
 def parse():
