@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--gops-m", type=int, nargs="*", default=[3, 4, 5, 6, 7, 8])
     p.add_argument("--invariance-m", type=int, default=8, help="order of the operand-invariance check (0: off)")
     p.add_argument("--ttp-structured-only-m", type=int, nargs="*", default=[10])
+    p.add_argument("--no-m11", action="store_true", help="skip the m = 11 structured chain run at >= 4 ranks")
     p.add_argument("--form", default="replicated", choices=["replicated", "allgather", "peer"],
                    help="replicated: A packed on every rank, row panels of A^(k-1) (x) A (default); "
                         "allgather: A^k = A (x) A^(k-1), A^(k-1) gathered over a P2P ring each step; "
@@ -184,7 +185,7 @@ def run_reference(args, rank, world):
     sample = f"{rows} sampled output rows of A^(k-1) (x) A(G) per step, m={args.m}, N={N}, dense i-j-k oracle"
     line = {
         "impl": "reference", "metric": "(min,+) Gop/s on A^(k-1) (x) A(G) at order N = C_m (power step with fused diag-min + periodicity test)",
-        "value": round(value, 3), "unit": "Gop/s", "n_gpus": args.gpus, "steps": args.steps,
+        "value": round(value, 3), "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "i32",
         "data": "synthetic A^k-like rows (seeded) x deterministic A(G)",
@@ -444,18 +445,24 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                                           "chain_gterms": round((rs["k_stop"] - 1) * NNZ.get(mm, 0) * nn
                                                                 / float(ts[1]) / 1e9, 1)}
 
-    # orders whose dense chain takes minutes: the structured chain only (NEXT-2/NEXT-3)
+    # orders whose dense chain takes minutes: the structured chain only (NEXT-2/NEXT-3).
+    # m = 11 (N = 191476, 73 GB per int16 power) from 4 ranks on: row panels of a ring of
+    # alpha_max + 1 = 6 powers (the paper's alpha <= 5), 110 GB per rank at 4 GPUs
+    structured_only = list(args.ttp_structured_only_m)
+    if world >= 4 and 11 not in structured_only and not args.no_m11:
+        structured_only.append(11)
     if not args.no_e2e:
-        for mm in args.ttp_structured_only_m:
+        for mm in structured_only:
             if world > 1:
                 dist.barrier()
-            rs = (rd.rd_power_sequence(mm, 50, am, method=1) if world == 1
-                  else rdist.power_sequence(mm, 50, am, method=1))
+            amm = min(am, 5) if mm >= 11 else am
+            rs = (rd.rd_power_sequence(mm, 50, amm, method=1) if world == 1
+                  else rdist.power_sequence(mm, 50, amm, method=1))
             ts = torch.tensor([rs["t_build"], rs["t_chain"]], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(ts, op=dist.ReduceOp.MAX)
             nn = rd.count_words(mm)
-            ttp[str(mm)] = {"k_stop": rs["k_stop"], "triple": [rs["n0"], rs["alpha"], rs["beta"]],
+            ttp[str(mm)] = {"k_stop": rs["k_stop"], "triple": [rs["n0"], rs["alpha"], rs["beta"]], "alpha_max": amm,
                             "structured": {"build_s": round(float(ts[0]), 4), "chain_s": round(float(ts[1]), 4),
                                            "total_s": round(float(ts[0] + ts[1]), 4),
                                            "terms_per_step": NNZ.get(mm, 0) * nn,
@@ -545,11 +552,48 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_command(argv, gpus: int, port: int):
+    """The command that runs this script as `gpus` ranks of one node (one process per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def self_launch(args, argv) -> int | None:
+    """`--gpus N > 1` without a launcher: re-run this script as N ranks under
+    torch.distributed.run and return its exit status (None: nothing to launch).  Ranks must
+    each have a GPU of their own unless the gloo test hook (RD_FORCE_DEVICE) is set."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl != "reference" and "RD_FORCE_DEVICE" not in os.environ:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible", file=sys.stderr)
+            return 2
+    import subprocess
+    return subprocess.call(launch_command(argv, args.gpus, _free_port()))
+
+
 def main():
     args = parse()
+    rc = self_launch(args, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)", file=sys.stderr)
+        sys.exit(2)
     # test hooks: several ranks on one GPU with host-side (gloo) collectives; never used for
     # a reported number (the line then says so in config.backend)
     if "RD_FORCE_DEVICE" in os.environ:

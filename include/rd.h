@@ -191,6 +191,13 @@ int rd_build_matrix_border(int16_t *A, int64_t *N_out);
  *   and cached per process.  Errors: RD_EINVAL, RD_NOTFOUND (no recurrence and n > 50). */
 int rd_roman_cylinder(int m, int64_t n, int64_t *gamma);
 
+/* rd_roman_cylinder_ex — rd_roman_cylinder with the power step chosen explicitly:
+ *   method 0 = the dense (min,+) GEMM chain (rd_power_sequence's north-star path),
+ *   method 1 = the structured step (finite terms of A only; rd_roman_cylinder's default).
+ * Both give the identical gamma (same powers); results are cached per (m, method).
+ * Errors: those of rd_roman_cylinder, RD_EINVAL for any other method. */
+int rd_roman_cylinder_ex(int m, int64_t n, int method, int64_t *gamma);
+
 /* ---------------------------------------------------------------------------
  * Closed form (NEXT-4): the unique solution of gamma(n + alpha) - gamma(n) = beta for
  * n >= n0 (Prop 8) with the boundary values diag[n0..n0+alpha-1]:
@@ -298,7 +305,7 @@ int rd_stats_decide(const int32_t *stats, int alpha_max, int k, int only_alpha, 
  * `world` owns rows R_r = [bounds[r], bounds[r+1]) of every power and the fixed left operand
  * A[R_r, :].  Each step's GEMM reads the right operand A^k straight from every rank's ring
  * slot (its own, and the peers' through CUDA IPC mappings, i.e. NVLink peer memory on a
- * multi-GPU node), 64 k-pairs per pipeline stage: no gather buffer, no copy kernel, and the
+ * multi-GPU node), 32 k-pairs (64 k) per pipeline stage: no gather buffer, no copy kernel, and the
  * transfer of power k overlaps the product of power k+1 tile by tile.
  *
  * Ordering contract (the caller's): every rank's step k must have completed before any rank
@@ -321,7 +328,10 @@ int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int64_t *slot_w
 /* This rank's ring as a device pointer of this process (for peers in the same process). */
 int rd_agchain_ring(const rd_agchain *c, const void **ring_dev, int64_t *slot_words);
 /* Registers rank s's ring: opened from its IPC handle (ipc_handle != NULL, another process),
- * or a device pointer valid in this process (ipc_handle == NULL).  s == own rank: no-op. */
+ * or a device pointer valid in this process (ipc_handle == NULL).  s == own rank: no-op.
+ * A device pointer on another GPU requires peer access from the chain's device: it is enabled
+ * here (already enabled is fine); RD_EINVAL if the two devices cannot be peers or the pointer
+ * is not device memory. */
 int rd_agchain_set_peer(rd_agchain *c, int s, const void *ipc_handle, const void *ring_dev, int64_t slot_words);
 /* Rows R_r of A^{k+1} into the ring with the fused stats of rd_chain_step (same layout,
  * MIN-reducible).  Requires every peer registered.  Asynchronous on the chain's stream. */
@@ -340,7 +350,7 @@ int64_t rd_agchain_order(const rd_agchain *c);
 int rd_set_gemm_variant(int dpx_cols);
 
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
- * one thread streams each 64-k-pair stage of both operands (cp.async.bulk.tensor, completion
+ * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
  * counted on an mbarrier; the warps release stages on a second mbarrier); without, every
  * thread issues cp.async and the CTA meets at __syncthreads.  mode 0 = cp.async always;
  * 1 (default) = TMA for single-pass steps of >= 128 stages (the m >= 9 orders); 2 = TMA

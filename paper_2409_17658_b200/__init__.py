@@ -59,6 +59,7 @@ def lib():
         L.rd_power_sequence.argtypes = [ci, ci, p, p]
         L.rd_power_sequence_ex.argtypes = [ci, ci, ci, ci, p, p]
         L.rd_roman_cylinder.argtypes = [ci, i64, p]
+        L.rd_roman_cylinder_ex.argtypes = [ci, i64, ci, p]
         L.rd_chain_create.argtypes = [ci, ci, i64, i64, p, p]
         L.rd_chain_create_ex.argtypes = [ci, ci, i64, i64, ci, p, p]
         L.rd_chain_terms_per_step.argtypes = [p]; L.rd_chain_terms_per_step.restype = ctypes.c_double
@@ -104,7 +105,7 @@ def lib():
                   "rd_agchain_step", "rd_agchain_read_rows"):
             getattr(L, f).restype = ci
         for f in ("rd_set_device", "rd_build_states", "rd_build_matrix", "rd_minplus_mul", "rd_minplus_mul_ex",
-                  "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_chain_create",
+                  "rd_power_sequence", "rd_power_sequence_ex", "rd_roman_cylinder", "rd_roman_cylinder_ex", "rd_chain_create",
                   "rd_chain_destroy", "rd_chain_current_k", "rd_stats_len", "rd_chain_step",
                   "rd_chain_read_rows", "rd_stats_decide", "rd_alu_probe", "rd_set_gemm_variant",
                   "rd_minplus_mul_acc", "rd_panel_stats", "rd_chain_create_ex", "rd_power_sequence_ex2", "rd_set_sparse_variant",
@@ -306,11 +307,15 @@ def rd_power_sequence_matrix(A: np.ndarray, kmax: int = 50, alpha_max: int = 10,
                 diag=[int(x) for x in diag], status=rc)
 
 
-def rd_roman_cylinder(m: int, n: int) -> int:
-    """gamma_R(P_m [] C_n)."""
+def rd_roman_cylinder(m: int, n: int, method: int | None = None) -> int:
+    """gamma_R(P_m [] C_n); method None = the library default (structured), 0 = dense GEMM
+    chain, 1 = structured step (rd_roman_cylinder_ex)."""
     _sync_device()
     g = ctypes.c_int64()
-    _check(lib().rd_roman_cylinder(m, n, ctypes.byref(g)))
+    if method is None:
+        _check(lib().rd_roman_cylinder(m, n, ctypes.byref(g)))
+    else:
+        _check(lib().rd_roman_cylinder_ex(m, n, method, ctypes.byref(g)))
     return g.value
 
 

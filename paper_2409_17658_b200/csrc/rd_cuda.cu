@@ -27,6 +27,8 @@
 #include <climits>
 #include <cstdio>
 #include <cstring>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -252,7 +254,7 @@ struct TmaOps {
 //   OUT = kOutRP : C is RP u32 [M/2][ldc] (pairs along i: C[2p][j] | C[2p+1][j] << 16), and the
 //                  right operand is read straight from the ranks' memory (PeerB): k-pairs
 //                  [t0[s], t0[s+1]) of B live at base[s] (the packed layout, pitch ldb), e.g.
-//                  peer GPUs' ring slots mapped over NVLink (CUDA IPC).  Each 64-k-pair stage
+//                  peer GPUs' ring slots mapped over NVLink (CUDA IPC).  Each stage (32 k-pairs)
 //                  lies inside one rank's range (ranges are whole 128-row tiles), so the
 //                  all-gather of B happens inside the mainloop's cp.async pipeline, tile by tile.
 //
@@ -901,34 +903,59 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 
 }  // namespace
 
-extern "C" int rd_set_gemm_variant(int dpx_cols) {
+extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   rd_enter();
   if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
     return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
   g_dpx_cols = dpx_cols;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_set_gemm_variant")
 
-extern "C" int rd_set_device(int device) {
+extern "C" int rd_set_device(int device) try {
   rd_enter();
   RD_CUDA_CHECK(cudaSetDevice(device));
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_set_device")
 
 // =========================================================== generic product ==
-// Keep stream-ordered workspace in the device's default pool across stream syncs (the
-// default release threshold of 0 would return ~2 GB to the driver after every call).
-static int retain_default_pool() {
-  static bool done[64] = {};
+// Library-owned stream-ordered pool (one per device; chains and the generic products' workspace).
+constexpr uint64_t kPoolKeep = (uint64_t)16 << 30;
+constexpr size_t kPoolMax = (size_t)kPoolKeep;
+static cudaMemPool_t chain_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      (void)cudaGetLastError();
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    uint64_t thr = kPoolKeep;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pools[dev];
+}
+
+// Stream-ordered workspace from the library's pool (the device's default pool and its release
+// threshold are left alone: other cudaMallocAsync users in the process keep their setting);
+// falls back to cudaMallocAsync on the default pool if the library pool cannot be created.
+static cudaError_t ws_malloc(void **p, size_t bytes, cudaStream_t st) {
+  *p = nullptr;
   int dev = 0;
-  RD_CUDA_CHECK(cudaGetDevice(&dev));
-  if (dev >= 0 && dev < 64 && done[dev]) return RD_OK;
-  cudaMemPool_t pool;
-  RD_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t thr = UINT64_MAX;
-  RD_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  if (dev >= 0 && dev < 64) done[dev] = true;
-  return RD_OK;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (cudaMemPool_t pool = chain_pool(dev)) {
+    if ((e = cudaMallocFromPoolAsync(p, bytes, pool, st)) == cudaSuccess) return e;
+    (void)cudaGetLastError();
+    *p = nullptr;
+  }
+  return cudaMallocAsync(p, bytes, st);
 }
 
 static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
@@ -942,11 +969,11 @@ static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int
   const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, 2 * kBK2);
   const int64_t kpairs = Kp / 2;
   uint32_t *XT = nullptr, *BP = nullptr;
-  if (int rc0 = retain_default_pool()) return rc0;
-  RD_CUDA_CHECK(cudaMallocAsync((void **)&XT, (size_t)(kpairs * Mp * 4), st));
-  cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(kpairs * Np * 4), st);
+  cudaError_t e = ws_malloc((void **)&XT, (size_t)(kpairs * Mp * 4), st);
+  if (e == cudaSuccess) e = ws_malloc((void **)&BP, (size_t)(kpairs * Np * 4), st);
   if (e != cudaSuccess) {
-    cudaFreeAsync(XT, st);
+    if (XT) cudaFreeAsync(XT, st);
+    (void)cudaGetLastError();
     return fail(RD_ENOMEM, "%s: workspace: %s", who, cudaGetErrorString(e));
   }
   int rc = pack_left(A, lda, M, K, 0, XT, Mp, kpairs, st);
@@ -960,14 +987,14 @@ static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int
 }
 
 extern "C" int rd_minplus_mul_ex(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
-                                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+                                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) try {
   return minplus_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, 0, "rd_minplus_mul_ex");
-}
+} RD_ABI_CATCH("rd_minplus_mul_ex")
 
 extern "C" int rd_minplus_mul_acc(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
-                                  int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+                                  int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) try {
   return minplus_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, 1, "rd_minplus_mul_acc");
-}
+} RD_ABI_CATCH("rd_minplus_mul_acc")
 
 static int minplus32_rowmajor(const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb, int32_t *C,
                               int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, const char *who) {
@@ -978,11 +1005,11 @@ static int minplus32_rowmajor(const int32_t *A, int64_t lda, const int32_t *B, i
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t Mp = round_up(M, kTile), Np = round_up(N, kTile), Kp = round_up(K, kBK2);
   int32_t *XT = nullptr, *BP = nullptr;
-  if (int rc0 = retain_default_pool()) return rc0;
-  RD_CUDA_CHECK(cudaMallocAsync((void **)&XT, (size_t)(Kp * Mp * 4), st));
-  cudaError_t e = cudaMallocAsync((void **)&BP, (size_t)(Kp * Np * 4), st);
+  cudaError_t e = ws_malloc((void **)&XT, (size_t)(Kp * Mp * 4), st);
+  if (e == cudaSuccess) e = ws_malloc((void **)&BP, (size_t)(Kp * Np * 4), st);
   if (e != cudaSuccess) {
-    cudaFreeAsync(XT, st);
+    if (XT) cudaFreeAsync(XT, st);
+    (void)cudaGetLastError();
     return fail(RD_ENOMEM, "%s: workspace: %s", who, cudaGetErrorString(e));
   }
   pack_t32_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((Mp + 31) / 32)), dim3(32, 8), 0, st>>>(
@@ -997,13 +1024,13 @@ static int minplus32_rowmajor(const int32_t *A, int64_t lda, const int32_t *B, i
 }
 
 extern "C" int rd_minplus_mul32_ex(const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb, int32_t *C,
-                                   int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) {
+                                   int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream) try {
   return minplus32_rowmajor(A, lda, B, ldb, C, ldc, M, N, K, cuda_stream, "rd_minplus_mul32_ex");
-}
+} RD_ABI_CATCH("rd_minplus_mul32_ex")
 
-extern "C" int rd_minplus_mul32(const int32_t *A, const int32_t *B, int32_t *C, int64_t N) {
+extern "C" int rd_minplus_mul32(const int32_t *A, const int32_t *B, int32_t *C, int64_t N) try {
   return minplus32_rowmajor(A, N, B, N, C, N, N, N, N, nullptr, "rd_minplus_mul32");
-}
+} RD_ABI_CATCH("rd_minplus_mul32")
 
 // ------------------------------------------------------- standalone stats --
 // Stats of a row-major int16 panel `cur` (rows x cols, ld) against up to kMaxAlpha
@@ -1099,7 +1126,7 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
 
 extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, int nprev, int64_t rows,
                               int64_t cols, int64_t ld, int64_t diag_row0, int alpha_max, int32_t *stats_dev,
-                              void *cuda_stream) {
+                              void *cuda_stream) try {
   rd_enter();
   if (!cur || !stats_dev || (nprev > 0 && !prev)) return fail(RD_EINVAL, "rd_panel_stats: NULL argument");
   if (alpha_max < 1 || alpha_max > kMaxAlpha || nprev < 0 || nprev > alpha_max)
@@ -1126,14 +1153,14 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
     RD_CUDA_CHECK(cudaGetLastError());
   }
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_panel_stats")
 
-extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N) {
+extern "C" int rd_minplus_mul(const int16_t *A, const int16_t *B, int16_t *C, int64_t N) try {
   if (!A || !B || !C) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: NULL pointer"); }
   if (N < 1) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: N must be >= 1"); }
   if (C == A || C == B) { rd_enter(); return fail(RD_EINVAL, "rd_minplus_mul: C aliases an input"); }
   return rd_minplus_mul_ex(A, N, B, N, C, N, N, N, N, nullptr);
-}
+} RD_ABI_CATCH("rd_minplus_mul")
 
 namespace {
 // ======================================================= structured step ==
@@ -1757,21 +1784,32 @@ __global__ void pack_rp_kernel(const int16_t *__restrict__ X, int64_t ld, int64_
   RP[p * ldr + j] = lo | (hi << 16);
 }
 
-// Dense-chain operands straight from a (single-chunk, general-format) CSC of A, thread per
-// column, into all-INF buffers: the packed right operand BP[t][j] = A[2t][j] | A[2t+1][j] << 16
-// and the PM panel XT[t][i] = A[r0+i][2t] | A[r0+i][2t+1] << 16 of rows [r0, r1).
+// Dense-chain operands straight from a general-format CSC of A (per q-chunk: entries hold
+// q - ch * Qc in 17 bits, so orders with N >= 2^17 take several chunks), thread per column,
+// into all-INF buffers: the packed right operand BP[t][j] = A[2t][j] | A[2t+1][j] << 16 and the
+// PM panel XT[t][i] = A[r0+i][2t] | A[r0+i][2t+1] << 16 of rows [r0, r1).
 __global__ void scatter_dense_operands_kernel(const int32_t *__restrict__ colptr, const uint32_t *__restrict__ ent,
-                                              int64_t N, uint32_t *__restrict__ BP, int64_t ldp,
-                                              uint32_t *__restrict__ XT, int64_t ldt, int64_t r0, int64_t r1) {
+                                              int64_t N, int nchunks, int Qc, uint32_t *__restrict__ BP,
+                                              int64_t ldp, uint32_t *__restrict__ XT, int64_t ldt, int64_t r0,
+                                              int64_t r1) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   uint16_t *hb = reinterpret_cast<uint16_t *>(BP), *hx = reinterpret_cast<uint16_t *>(XT);
-  for (int t = colptr[j]; t < colptr[j + 1]; ++t) {
-    const int64_t q = ent[t] & 0x1FFFFu;
-    const uint16_t w = (uint16_t)(ent[t] >> 17);
-    if (BP) hb[((q >> 1) * ldp + j) * 2 + (q & 1)] = w;
-    if (XT && q >= r0 && q < r1) hx[((j >> 1) * ldt + (q - r0)) * 2 + (j & 1)] = w;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int32_t *cp = colptr + (int64_t)ch * (N + 1);
+    for (int t = cp[j]; t < cp[j + 1]; ++t) {
+      const int64_t q = (int64_t)ch * Qc + (ent[t] & 0x1FFFFu);
+      const uint16_t w = (uint16_t)(ent[t] >> 17);
+      if (BP) hb[((q >> 1) * ldp + j) * 2 + (q & 1)] = w;
+      if (XT && q >= r0 && q < r1) hx[((j >> 1) * ldt + (q - r0)) * 2 + (j & 1)] = w;
+    }
   }
+}
+
+// q-chunking of a general-format CSC: entries store q - ch * Qc in 17 bits
+inline void csc_chunks_17bit(int64_t N, int *nchunks, int *Qc) {
+  *nchunks = (int)((N + (1 << 17) - 1) >> 17);
+  *Qc = (int)((N + *nchunks - 1) / *nchunks);
 }
 
 // A^1 rows [r0, r1) into an all-INF RP slot straight from the CSC (thread per column).
@@ -2223,29 +2261,6 @@ struct rd_chain {
 // dense chain's ring + packed operand is 11.7 GB), anything beyond is returned at the next
 // synchronisation.  Buffers above kPoolMax (the m >= 10 rings: growing the pool by 92 GB took
 // 9 s against 0.5 s for cudaMalloc) and allocations the pool cannot serve use cudaMalloc.
-constexpr uint64_t kPoolKeep = (uint64_t)16 << 30;
-constexpr size_t kPoolMax = (size_t)kPoolKeep;
-static cudaMemPool_t chain_pool(int dev) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!pools[dev]) {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
-      (void)cudaGetLastError();
-      pools[dev] = nullptr;
-      return nullptr;
-    }
-    uint64_t thr = kPoolKeep;
-    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  return pools[dev];
-}
-
 template <typename T>
 static cudaError_t chain_malloc(rd_chain *c, T **p, size_t bytes) {
   *p = nullptr;
@@ -2276,6 +2291,15 @@ static void chain_free(rd_chain *c, void *p) {
     cudaFree(p);
   }
 }
+
+// Runs f when the enclosing scope is left by an exception (not on normal returns).
+struct OnThrow {
+  std::function<void()> f;
+  int n0 = std::uncaught_exceptions();
+  ~OnThrow() {
+    if (std::uncaught_exceptions() > n0 && f) f();
+  }
+};
 
 // Creates a chain over the host matrix A (N x N int16 row-major, entries in [0, RD_INF]).
 // Ahost == nullptr (method 1 only): the CSC comes straight from the successor generator of
@@ -2331,7 +2355,24 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     delete c;
     return code;
   };
+  // a host allocation that throws (std::bad_alloc in the CSC / slab builds) releases the
+  // chain's device buffers on the way out; the C-ABI wrapper turns it into RD_ENOMEM
+  OnThrow on_throw{[&] { cleanup(0); }};
   cudaError_t e;
+  {
+    // device memory first, before any host build: the ring of alpha_max + 1 powers and (dense)
+    // the packed operand must fit in what the device has free
+    const double need = 4.0 * (double)((alpha_max + 1) * c->slot_words) +
+                        (method == 0 ? 2.0 * (double)c->P * (double)c->P : 0.0);
+    size_t free_b = 0, total_b = 0;
+    if ((e = cudaMemGetInfo(&free_b, &total_b)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return cleanup(fail(RD_ECUDA, "rd_chain_create: cudaMemGetInfo: %s", cudaGetErrorString(e)));
+    }
+    if (need > (double)free_b)
+      return cleanup(fail(RD_ENOMEM, "rd_chain_create: needs %.1f GB of device memory (ring%s), %.1f GB free",
+                          need / 1e9, method == 0 ? " + packed operand" : "", (double)free_b / 1e9));
+  }
   if (method == 1) {
     c->nchunks = (int)(((N + 1) * 8 + kSpSmemMax - 1) / kSpSmemMax);
     c->Qc = (int)((N + c->nchunks - 1) / c->nchunks);   // (Qc + 1) * 8 B of shared memory
@@ -2446,7 +2487,9 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     std::vector<int32_t> colptr;
     std::vector<uint32_t> ent;
     std::vector<int16_t> dg;
-    build_csc_direct(m, border, 1, (int)N, colptr, ent, dg);
+    int nch = 1, qc = (int)N;
+    csc_chunks_17bit(N, &nch, &qc);
+    build_csc_direct(m, border, nch, qc, colptr, ent, dg);
     for (int64_t p = c->r0; p < c->r1; ++p)
       if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
     int32_t *dcp = nullptr;
@@ -2463,7 +2506,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
     const int64_t nbp = c->P / 2 * c->P, nring = (alpha_max + 1) * c->slot_words;
     fill_u32_kernel<<<(unsigned)((nbp + 255) / 256), 256, 0, c->st>>>(c->BP, nbp, kInf2);
     fill_u32_kernel<<<(unsigned)((nring + 255) / 256), 256, 0, c->st>>>(c->ring, nring, kInf2);
-    scatter_dense_operands_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(dcp, dent, N, c->BP, c->P,
+    scatter_dense_operands_kernel<<<(unsigned)((N + 255) / 256), 256, 0, c->st>>>(dcp, dent, N, nch, qc, c->BP, c->P,
                                                                                   c->slot(1), c->Mp, c->r0, c->r1);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
@@ -2498,7 +2541,7 @@ static int chain_create_impl(const int16_t *Ahost, int64_t N, int m, int alpha_m
 }
 
 extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64_t row_end, int method,
-                                  void *cuda_stream, rd_chain **out) {
+                                  void *cuda_stream, rd_chain **out) try {
   rd_enter();
   if (!out) return fail(RD_EINVAL, "rd_chain_create: out is NULL");
   *out = nullptr;
@@ -2506,15 +2549,10 @@ extern "C" int rd_chain_create_ex(int m, int alpha_max, int64_t row_begin, int64
   if (m < 1 || m > 12 || (m == 12 && method != 1))
     return fail(RD_EINVAL, "rd_chain_create: m=%d out of range (m = 12: method 1 only)", m);
   const int64_t N = count_words(m);
-  // both methods: CSC from the successor generator, operands built on the device (the CSC
-  // entry holds q in 17 bits: m = 11 dense chains take the dense host matrix instead)
-  if (method == 1 || N < (1 << 17))
-    return chain_create_impl(nullptr, N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
-  std::vector<int16_t> A((size_t)(N * N));
-  int rc = build_matrix(m, A.data(), N);
-  if (rc != RD_OK) return rc;
-  return chain_create_impl(A.data(), N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
-}
+  // both methods: CSC from the successor generator (q-chunked where N >= 2^17), operands built
+  // on the device; no dense host matrix at any order
+  return chain_create_impl(nullptr, N, m, alpha_max, row_begin, row_end, method, cuda_stream, out);
+} RD_ABI_CATCH("rd_chain_create_ex")
 
 // Validates a caller's matrix: entries in [0, RD_INF] (> RD_INF is read as +inf);
 // returns the largest finite entry in *maxlab.
@@ -2530,7 +2568,7 @@ static int check_matrix(const int16_t *A, int64_t N, int32_t *maxlab, const char
 }
 
 extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max, int64_t row_begin,
-                                      int64_t row_end, int method, void *cuda_stream, rd_chain **out) {
+                                      int64_t row_end, int method, void *cuda_stream, rd_chain **out) try {
   rd_enter();
   int32_t mx = 0;
   if (int rc = check_matrix(A, N, &mx, "rd_chain_create_matrix")) return rc;
@@ -2538,12 +2576,12 @@ extern "C" int rd_chain_create_matrix(const int16_t *A, int64_t N, int alpha_max
   std::vector<int16_t> Ac(A, A + N * N);
   for (auto &x : Ac) x = std::min<int16_t>(x, RD_INF);
   return chain_create_impl(Ac.data(), N, 0, alpha_max, row_begin, row_end, method, cuda_stream, out);
-}
+} RD_ABI_CATCH("rd_chain_create_matrix")
 
 // Dense chain (method 0) over the packed operand of A(G) that another chain exported
 // (e.g. broadcast over NVLink from rank 0): no host build, the A^1 panel comes from BP.
 extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, int64_t row_end,
-                                      const uint32_t *bp_dev, int32_t diag1, void *cuda_stream, rd_chain **out) {
+                                      const uint32_t *bp_dev, int32_t diag1, void *cuda_stream, rd_chain **out) try {
   rd_enter();
   if (!out || !bp_dev) return fail(RD_EINVAL, "rd_chain_create_packed: NULL argument");
   *out = nullptr;
@@ -2578,7 +2616,7 @@ extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, i
   pm_from_bp_kernel<<<grid, 256, 0, c->st>>>(c->BP, c->P, c->Mr, c->r0, c->slot(1), c->Mp, c->P / 2);
   if (diag1 == INT32_MAX) {   // not supplied: the panel's self-loop labels from the packed operand
     int32_t *dd = nullptr;
-    if ((e = cudaMallocAsync((void **)&dd, 4, c->st)) == cudaSuccess) {
+    if ((e = ws_malloc((void **)&dd, 4, c->st)) == cudaSuccess) {
       int32_t init = INT32_MAX;
       cudaMemcpyAsync(dd, &init, 4, cudaMemcpyHostToDevice, c->st);
       diag_from_bp_kernel<<<(unsigned)((c->Mr + 255) / 256), 256, 0, c->st>>>(c->BP, c->P, c->r0, c->r1, dd);
@@ -2593,16 +2631,16 @@ extern "C" int rd_chain_create_packed(int m, int alpha_max, int64_t row_begin, i
   c->k = 1;
   *out = c;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_chain_create_packed")
 
-extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_dev, int64_t *words) {
+extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_dev, int64_t *words) try {
   rd_enter();
   if (!c || !bp_dev || !words) return fail(RD_EINVAL, "rd_chain_packed_operand: NULL argument");
   if (c->method != 0 || !c->BP) return fail(RD_EINVAL, "rd_chain_packed_operand: not a dense chain");
   *bp_dev = c->BP;
   *words = c->P / 2 * c->P;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_chain_packed_operand")
 
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
@@ -2611,12 +2649,12 @@ static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small 
 // CTA — split-K, m <= 8 — the single-thread issue costs 3-8 %); 2 = TMA always.
 static int g_gemm_tma = 1;
 
-extern "C" int rd_set_gemm_tma(int mode) {
+extern "C" int rd_set_gemm_tma(int mode) try {
   rd_enter();
   if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_gemm_tma: mode must be 0, 1 or 2");
   g_gemm_tma = mode;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_set_gemm_tma")
 
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -2656,17 +2694,17 @@ static int chain_tma_prepare(rd_chain *c) {
   return RD_OK;
 }
 
-extern "C" int rd_set_sparse_bytes(int enable) {
+extern "C" int rd_set_sparse_bytes(int enable) try {
   rd_enter();
   if (enable < 0 || enable > 2) return fail(RD_EINVAL, "rd_set_sparse_bytes: 0, 1 or 2");
   g_sparse_bytes = enable;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_set_sparse_bytes")
 
-extern "C" int rd_set_split_k(int enable) {
+extern "C" int rd_set_split_k(int enable) try {
   g_split_k_off = enable ? 0 : 1;
   return RD_OK;
-}   // rd_set_sparse_variant (default: measured best, 1024 threads)
+} RD_ABI_CATCH("rd_set_split_k")   // rd_set_sparse_variant (default: measured best, 1024 threads)
 
 template <int THREADS, int UNROLL, bool UNIFORM, bool STATS = true>
 static int launch_sparse_u(rd_chain *c, const SpArgs &sa, int knew, const EpiArgs &epi) {
@@ -2735,19 +2773,19 @@ static int step_slab(rd_chain *c, int knew, EpiArgs &epi) {
   return RD_OK;
 }
 
-extern "C" int rd_set_sparse_variant(int v) {
+extern "C" int rd_set_sparse_variant(int v) try {
   rd_enter();
   if (v < 0 || v > 3) return fail(RD_EINVAL, "rd_set_sparse_variant: 0..3");
   g_sparse_variant = v;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_set_sparse_variant")
 
 extern "C" int rd_chain_create(int m, int alpha_max, int64_t row_begin, int64_t row_end, void *cuda_stream,
-                               rd_chain **out) {
+                               rd_chain **out) try {
   return rd_chain_create_ex(m, alpha_max, row_begin, row_end, 0, cuda_stream, out);
-}
+} RD_ABI_CATCH("rd_chain_create")
 
-extern "C" int rd_chain_destroy(rd_chain *c) {
+extern "C" int rd_chain_destroy(rd_chain *c) try {
   if (!c) return RD_OK;
   chain_free(c, c->BP);
   chain_free(c, c->ring);
@@ -2761,7 +2799,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) {
     chain_free(c, p);
   delete c;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_chain_destroy")
 
 extern "C" int64_t rd_chain_order(const rd_chain *c) { return c ? c->N : -1; }
 extern "C" int rd_chain_current_k(const rd_chain *c) { return c ? c->k : -1; }
@@ -2771,7 +2809,7 @@ extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
   return c->method == 0 ? (double)c->Mr * (double)c->N * (double)c->N : (double)c->Mr * (double)c->nnz;
 }
 
-extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
+extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   rd_enter();
   NvtxRange nvtx_range(c && c->method == 1 ? "rd_chain_step structured" : "rd_chain_step");
   if (!c || !stats_dev) return fail(RD_EINVAL, "rd_chain_step: NULL argument");
@@ -2883,17 +2921,17 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) {
   }
   c->k = knew;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_chain_step")
 
-extern "C" int rd_panel_step(rd_chain *c, int32_t *stats_dev) { return rd_chain_step(c, stats_dev); }
+extern "C" int rd_panel_step(rd_chain *c, int32_t *stats_dev) try { return rd_chain_step(c, stats_dev); } RD_ABI_CATCH("rd_panel_step")
 
-extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
+extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) try {
   rd_enter();
   if (!c || !host_out) return fail(RD_EINVAL, "rd_chain_read_rows: NULL argument");
   if (k < 1 || k > c->k || k < c->k - c->alpha_max)
     return fail(RD_EINVAL, "rd_chain_read_rows: power %d not in the ring (current %d)", k, c->k);
   int16_t *d = nullptr;
-  RD_CUDA_CHECK(cudaMallocAsync((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
+  RD_CUDA_CHECK(ws_malloc((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
   dim3 grid((unsigned)((c->N + 255) / 256), (unsigned)c->Mr);
   if (c->method == 0)
     unpack_pm_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->Mp, c->Mr, c->N, d);
@@ -2904,7 +2942,7 @@ extern "C" int rd_chain_read_rows(rd_chain *c, int k, int16_t *host_out) {
   if (e != cudaSuccess) return fail(RD_ECUDA, "rd_chain_read_rows: %s", cudaGetErrorString(e));
   RD_CUDA_CHECK(cudaStreamSynchronize(c->st));
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_chain_read_rows")
 
 // ======================================================= peer all-gather chain ==
 // The north star's all-gather form with the gather fused into the product:
@@ -2930,7 +2968,7 @@ struct rd_agchain {
   uint32_t *slot(int kk) const { return ring + (int64_t)(kk % (alpha_max + 1)) * slot_words; }
 };
 
-extern "C" int rd_agchain_destroy(rd_agchain *c) {
+extern "C" int rd_agchain_destroy(rd_agchain *c) try {
   if (!c) return RD_OK;
   for (void *p : c->ipc_mapped)
     if (p) cudaIpcCloseMemHandle(p);
@@ -2938,10 +2976,10 @@ extern "C" int rd_agchain_destroy(rd_agchain *c) {
   if (c->ring) cudaFree(c->ring);
   delete c;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_destroy")
 
 extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, int world, int rank, void *cuda_stream,
-                                 rd_agchain **out) {
+                                 rd_agchain **out) try {
   rd_enter();
   NvtxRange nvtx_range("rd_agchain_create");
   if (!out || !bounds) return fail(RD_EINVAL, "rd_agchain_create: NULL argument");
@@ -2958,6 +2996,7 @@ extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, in
       return fail(RD_EINVAL, "rd_agchain_create: panel %d = [%lld, %lld) must be non-empty and start on a %d-row tile",
                   s, (long long)bounds[s], (long long)bounds[s + 1], kTile);
   rd_agchain *c = new rd_agchain;
+  OnThrow on_throw{[&] { rd_agchain_destroy(c); }};
   c->m = m; c->alpha_max = alpha_max; c->world = world; c->rank = rank; c->N = N;
   c->bounds.assign(bounds, bounds + world + 1);
   c->r0 = bounds[rank]; c->r1 = bounds[rank + 1]; c->Mr = c->r1 - c->r0;
@@ -2972,7 +3011,9 @@ extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, in
   std::vector<int32_t> colptr;
   std::vector<uint32_t> ent;
   std::vector<int16_t> dg;
-  build_csc_direct(m, false, 1, (int)N, colptr, ent, dg);
+  int nch = 1, qc = (int)N;
+  csc_chunks_17bit(N, &nch, &qc);   // m = 11: N = 191476 >= 2^17 takes two q-chunks
+  build_csc_direct(m, false, nch, qc, colptr, ent, dg);
   for (int64_t p = c->r0; p < c->r1; ++p)
     if (dg[p] < RD_INF) c->diag1 = std::min<int32_t>(c->diag1, dg[p]);
   int32_t *dcp = nullptr;
@@ -2993,8 +3034,8 @@ extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, in
   fill_u32_kernel<<<(unsigned)((nxl + 255) / 256), 256, 0, c->st>>>(c->XL, nxl, kInf2);
   fill_u32_kernel<<<(unsigned)((nring + 255) / 256), 256, 0, c->st>>>(c->ring, nring, kInf2);
   const unsigned g = (unsigned)((N + 255) / 256);
-  scatter_dense_operands_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, nullptr, 0, c->XL, c->Mp, c->r0, c->r1);
-  scatter_rp_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, 1, (int)N, c->r0, c->r1, c->slot(1), c->P, nullptr, nullptr);
+  scatter_dense_operands_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, nch, qc, nullptr, 0, c->XL, c->Mp, c->r0, c->r1);
+  scatter_rp_kernel<<<g, 256, 0, c->st>>>(dcp, dent, N, nch, qc, c->r0, c->r1, c->slot(1), c->P, nullptr, nullptr);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
   cudaFree(dcp);
@@ -3008,9 +3049,9 @@ extern "C" int rd_agchain_create(int m, int alpha_max, const int64_t *bounds, in
   c->k = 1;
   *out = c;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_create")
 
-extern "C" int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int64_t *slot_words) {
+extern "C" int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int64_t *slot_words) try {
   rd_enter();
   if (!c || !handle_out) return fail(RD_EINVAL, "rd_agchain_ipc_handle: NULL argument");
   static_assert(sizeof(cudaIpcMemHandle_t) == RD_IPC_HANDLE_BYTES, "IPC handle size");
@@ -3019,18 +3060,18 @@ extern "C" int rd_agchain_ipc_handle(const rd_agchain *c, void *handle_out, int6
   memcpy(handle_out, &h, sizeof h);
   if (slot_words) *slot_words = c->slot_words;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_ipc_handle")
 
-extern "C" int rd_agchain_ring(const rd_agchain *c, const void **ring_dev, int64_t *slot_words) {
+extern "C" int rd_agchain_ring(const rd_agchain *c, const void **ring_dev, int64_t *slot_words) try {
   rd_enter();
   if (!c || !ring_dev) return fail(RD_EINVAL, "rd_agchain_ring: NULL argument");
   *ring_dev = c->ring;
   if (slot_words) *slot_words = c->slot_words;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_ring")
 
 extern "C" int rd_agchain_set_peer(rd_agchain *c, int s, const void *ipc_handle, const void *ring_dev,
-                                   int64_t slot_words) {
+                                   int64_t slot_words) try {
   rd_enter();
   if (!c || s < 0 || s >= c->world) return fail(RD_EINVAL, "rd_agchain_set_peer: bad chain or rank");
   if (s == c->rank) return RD_OK;
@@ -3051,13 +3092,35 @@ extern "C" int rd_agchain_set_peer(rd_agchain *c, int s, const void *ipc_handle,
     c->peer_ring[s] = reinterpret_cast<const uint32_t *>(p);
   } else {
     if (!ring_dev) return fail(RD_EINVAL, "rd_agchain_set_peer: neither an IPC handle nor a device pointer");
+    // a ring on another GPU of this process is read by the GEMM directly: enable peer access
+    // from the chain's device (already enabled is fine), or refuse the pointer
+    cudaPointerAttributes pa{};
+    RD_CUDA_CHECK(cudaPointerGetAttributes(&pa, ring_dev));
+    if (pa.type != cudaMemoryTypeDevice)
+      return fail(RD_EINVAL, "rd_agchain_set_peer: rank %d's ring is not device memory", s);
+    if (pa.device != c->device) {
+      int ok = 0;
+      RD_CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, c->device, pa.device));
+      if (!ok)
+        return fail(RD_EINVAL, "rd_agchain_set_peer: device %d cannot access rank %d's ring on device %d", c->device,
+                    s, pa.device);
+      int cur = 0;
+      RD_CUDA_CHECK(cudaGetDevice(&cur));
+      RD_CUDA_CHECK(cudaSetDevice(c->device));
+      cudaError_t pe = cudaDeviceEnablePeerAccess(pa.device, 0);
+      cudaSetDevice(cur);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+      else if (pe != cudaSuccess)
+        return fail(RD_ECUDA, "rd_agchain_set_peer: enabling peer access to device %d: %s", pa.device,
+                    cudaGetErrorString(pe));
+    }
     c->peer_ring[s] = reinterpret_cast<const uint32_t *>(ring_dev);
   }
   c->peer_slot_words[s] = slot_words;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_set_peer")
 
-extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) {
+extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) try {
   rd_enter();
   NvtxRange nvtx_range("rd_agchain_step");
   if (!c || !stats_dev) return fail(RD_EINVAL, "rd_agchain_step: NULL argument");
@@ -3092,15 +3155,15 @@ extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) {
   if (rc != RD_OK) return rc;
   c->k = knew;
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_step")
 
-extern "C" int rd_agchain_read_rows(rd_agchain *c, int k, int16_t *host_out) {
+extern "C" int rd_agchain_read_rows(rd_agchain *c, int k, int16_t *host_out) try {
   rd_enter();
   if (!c || !host_out) return fail(RD_EINVAL, "rd_agchain_read_rows: NULL argument");
   if (k < 1 || k > c->k || k < c->k - c->alpha_max)
     return fail(RD_EINVAL, "rd_agchain_read_rows: power %d not in the ring (current %d)", k, c->k);
   int16_t *d = nullptr;
-  RD_CUDA_CHECK(cudaMallocAsync((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
+  RD_CUDA_CHECK(ws_malloc((void **)&d, (size_t)(c->Mr * c->N * 2), c->st));
   dim3 grid((unsigned)((c->N + 255) / 256), (unsigned)c->Mr);
   unpack_rp_kernel<<<grid, 256, 0, c->st>>>(c->slot(k), c->P, c->Mr, c->N, d, nullptr);
   cudaError_t e = cudaMemcpyAsync(host_out, d, (size_t)(c->Mr * c->N * 2), cudaMemcpyDeviceToHost, c->st);
@@ -3108,7 +3171,7 @@ extern "C" int rd_agchain_read_rows(rd_agchain *c, int k, int16_t *host_out) {
   if (e != cudaSuccess) return fail(RD_ECUDA, "rd_agchain_read_rows: %s", cudaGetErrorString(e));
   RD_CUDA_CHECK(cudaStreamSynchronize(c->st));
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_agchain_read_rows")
 
 extern "C" int32_t rd_agchain_diag1(const rd_agchain *c) { return c ? c->diag1 : INT32_MAX; }
 extern "C" int64_t rd_agchain_order(const rd_agchain *c) { return c ? c->N : -1; }
@@ -3136,7 +3199,7 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
                               std::chrono::steady_clock::time_point *t_done = nullptr);
 
 extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
-                                       int32_t *diag, double *seconds) {
+                                       int32_t *diag, double *seconds) try {
   rd_enter();
   const auto t0 = std::chrono::steady_clock::now();
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
@@ -3155,15 +3218,15 @@ extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int polic
     seconds[1] = std::chrono::duration<double>(t2 - t1).count();
   }
   return rc;
-}
+} RD_ABI_CATCH("rd_power_sequence_timed")
 
 extern "C" int rd_power_sequence_ex2(int m, int kmax, int alpha_max, int policy, int method, rd_period_t *out,
-                                     int32_t *diag) {
+                                     int32_t *diag) try {
   return rd_power_sequence_timed(m, kmax, alpha_max, policy, method, out, diag, nullptr);
-}
+} RD_ABI_CATCH("rd_power_sequence_ex2")
 
 extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, int alpha_max, int policy,
-                                        int method, rd_period_t *out, int32_t *diag) {
+                                        int method, rd_period_t *out, int32_t *diag) try {
   rd_enter();
   int32_t mx = 0;
   if (int rc0 = check_matrix(A, N, &mx, "rd_power_sequence_matrix")) return rc0;
@@ -3174,7 +3237,7 @@ extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, i
   int rc = rd_chain_create_matrix(A, N, alpha_max, 0, N, method, st, &c);
   if (rc != RD_OK) { cudaStreamDestroy(st); return rc; }
   return power_sequence_run(c, st, kmax, alpha_max, policy, method, out, diag);
-}
+} RD_ABI_CATCH("rd_power_sequence_matrix")
 
 // Algorithm 2's loop over a created chain (consumes c and st).
 static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_max, int policy, int method,
@@ -3277,13 +3340,13 @@ static int power_sequence_run(rd_chain *c, cudaStream_t st, int kmax, int alpha_
 }
 
 extern "C" int rd_power_sequence_ex(int m, int kmax, int alpha_max, int policy, rd_period_t *out,
-                                    int32_t *diag) {
+                                    int32_t *diag) try {
   return rd_power_sequence_ex2(m, kmax, alpha_max, policy, 0, out, diag);
-}
+} RD_ABI_CATCH("rd_power_sequence_ex")
 
-extern "C" int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag) {
+extern "C" int rd_power_sequence(int m, int kmax, rd_period_t *out, int32_t *diag) try {
   return rd_power_sequence_ex(m, kmax, 10, 0, out, diag);
-}
+} RD_ABI_CATCH("rd_power_sequence")
 
 // ================================================================ ALU probe ==
 namespace {
@@ -3385,7 +3448,7 @@ int probe_one(int sms, double *minplus_per_clk_sm, double *mhz, double *instr_pe
 }
 }  // namespace
 
-extern "C" int rd_alu_probe(double out[4]) {
+extern "C" int rd_alu_probe(double out[4]) try {
   rd_enter();
   if (!out) return fail(RD_EINVAL, "rd_alu_probe: NULL");
   int dev = 0, sms = 0;
@@ -3400,4 +3463,4 @@ extern "C" int rd_alu_probe(double out[4]) {
   out[2] = mp1;
   out[3] = 0.5 * (mhz0 + mhz1);
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_alu_probe")

@@ -10,6 +10,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -19,16 +21,33 @@ namespace rd {
 
 static thread_local std::string g_err;
 
-int fail(int code, const char *fmt, ...) {
+int fail(int code, const char *fmt, ...) noexcept {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  g_err = buf;
+  try {
+    g_err = buf;
+  } catch (...) {   // out of host memory for the message itself: keep the status
+  }
   return code;
 }
-void clear_error() { g_err.clear(); }
+void clear_error() noexcept { g_err.clear(); }
+
+int abi_exception(const char *who) noexcept {
+  try {
+    throw;
+  } catch (const std::bad_alloc &) {
+    return fail(RD_ENOMEM, "%s: host allocation failed (std::bad_alloc)", who);
+  } catch (const std::length_error &) {
+    return fail(RD_ENOMEM, "%s: host allocation too large (std::length_error)", who);
+  } catch (const std::exception &e) {
+    return fail(RD_EINVAL, "%s: internal error: %s", who, e.what());
+  } catch (...) {
+    return fail(RD_EINVAL, "%s: internal error (unknown exception)", who);
+  }
+}
 
 // Letters as digits: a=0 b=1 c=2 d=3.  Def 4: no ad, da, ab, ba, bb.
 static inline bool adjacent_ok(int x, int y) {
@@ -197,7 +216,7 @@ using namespace rd;
 
 extern "C" const char *rd_last_error(void) { return g_err.c_str(); }
 
-extern "C" int rd_build_states(int m, char *words, int64_t *N_out) {
+extern "C" int rd_build_states(int m, char *words, int64_t *N_out) try {
   clear_error();
   if (!N_out) return fail(RD_EINVAL, "rd_build_states: N_out is NULL");
   if (m < 1 || m > 12) return fail(RD_EINVAL, "rd_build_states: m=%d out of range 1..12", m);
@@ -207,9 +226,9 @@ extern "C" int rd_build_states(int m, char *words, int64_t *N_out) {
     for (size_t w = 0; w < codes.size(); ++w)
       for (int i = 0; i < m; ++i) words[w * m + i] = (char)('a' + ((codes[w] >> (2 * (m - 1 - i))) & 3));
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_build_states")
 
-extern "C" int rd_build_matrix(int m, int16_t *A, int64_t *N_out) {
+extern "C" int rd_build_matrix(int m, int16_t *A, int64_t *N_out) try {
   clear_error();
   if (!N_out) return fail(RD_EINVAL, "rd_build_matrix: N_out is NULL");
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_build_matrix: m=%d out of range 1..11", m);
@@ -217,16 +236,16 @@ extern "C" int rd_build_matrix(int m, int16_t *A, int64_t *N_out) {
   *N_out = N;
   if (!A) return RD_OK;
   return build_matrix(m, A, N);
-}
+} RD_ABI_CATCH("rd_build_matrix")
 
-extern "C" int rd_build_matrix_border(int16_t *A, int64_t *N_out) {
+extern "C" int rd_build_matrix_border(int16_t *A, int64_t *N_out) try {
   clear_error();
   if (!N_out) return fail(RD_EINVAL, "rd_build_matrix_border: N_out is NULL");
   const int64_t N = count_words(4);
   *N_out = N;
   if (!A) return RD_OK;
   return build_matrix_variant(4, A, N, true);
-}
+} RD_ABI_CATCH("rd_build_matrix_border")
 
 extern "C" int rd_stats_len(int alpha_max) { return 1 + 4 * alpha_max; }
 
@@ -259,29 +278,28 @@ struct Cached {
   std::vector<int32_t> diag;
 };
 std::mutex g_cache_mu;
-std::map<int, Cached> g_cache;
+std::map<std::pair<int, int>, Cached> g_cache;   // (m, method) -> chain result
 }  // namespace
 
-extern "C" int rd_roman_cylinder(int m, int64_t n, int64_t *gamma) {
+extern "C" int rd_roman_cylinder_ex(int m, int64_t n, int method, int64_t *gamma) try {
   clear_error();
   if (!gamma) return fail(RD_EINVAL, "rd_roman_cylinder: gamma is NULL");
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_roman_cylinder: m=%d out of range", m);
   if (n < 3) return fail(RD_EINVAL, "rd_roman_cylinder: n=%lld < 3 (P:21)", (long long)n);
+  if (method != 0 && method != 1) return fail(RD_EINVAL, "rd_roman_cylinder: method must be 0 (dense) or 1 (structured)");
   Cached c;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.find(m);
+    auto it = g_cache.find({m, method});
     if (it != g_cache.end()) c = it->second;
   }
   if (c.diag.empty()) {
     const int kmax = 50;
     c.diag.assign(kmax + 1, INT32_MAX);
-    // the structured step (method 1) evaluates the same product on the finite terms only:
-    // identical powers, ~12x faster at m = 9
-    int rc = rd_power_sequence_ex2(m, kmax, 10, 0, 1, &c.per, c.diag.data());
+    int rc = rd_power_sequence_ex2(m, kmax, 10, 0, method, &c.per, c.diag.data());
     if (rc < 0) return rc;
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    g_cache[m] = c;
+    g_cache[{m, method}] = c;
   }
   if (n <= c.per.k_stop) {
     *gamma = c.diag[n];
@@ -292,10 +310,14 @@ extern "C" int rd_roman_cylinder(int m, int64_t n, int64_t *gamma) {
   int64_t np = n0 + (n - n0) % a;  // n0 <= np < n0 + a <= k_stop
   *gamma = (int64_t)c.diag[np] + b * ((n - np) / a);
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_roman_cylinder_ex")
+
+// The structured step (method 1) evaluates the same product on the finite terms only:
+// identical powers, ~70x faster at m = 9.
+extern "C" int rd_roman_cylinder(int m, int64_t n, int64_t *gamma) try { return rd_roman_cylinder_ex(m, n, 1, gamma); } RD_ABI_CATCH("rd_roman_cylinder")
 
 // Closed form from the recurrence (Prop 8 + the finite-difference solution).
-extern "C" int rd_closed_form_from(const rd_period_t *per, const int32_t *diag, rd_formula_t *f, int32_t *small) {
+extern "C" int rd_closed_form_from(const rd_period_t *per, const int32_t *diag, rd_formula_t *f, int32_t *small) try {
   clear_error();
   if (!per || !diag || !f) return fail(RD_EINVAL, "rd_closed_form_from: NULL argument");
   if (!per->found) return fail(RD_EINVAL, "rd_closed_form_from: no recurrence");
@@ -320,9 +342,9 @@ extern "C" int rd_closed_form_from(const rd_period_t *per, const int32_t *diag, 
   if (small)
     for (int64_t n = 3; n < nv && n - 3 < 64; ++n) small[n - 3] = diag[n];
   return RD_OK;
-}
+} RD_ABI_CATCH("rd_closed_form_from")
 
-extern "C" int rd_closed_form(int m, rd_formula_t *f, int32_t *small) {
+extern "C" int rd_closed_form(int m, rd_formula_t *f, int32_t *small) try {
   clear_error();
   if (!f) return fail(RD_EINVAL, "rd_closed_form: f is NULL");
   int64_t g = 0;
@@ -331,7 +353,7 @@ extern "C" int rd_closed_form(int m, rd_formula_t *f, int32_t *small) {
   Cached c;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    c = g_cache[m];
+    c = g_cache[{m, 1}];
   }
   return rd_closed_form_from(&c.per, c.diag.data(), f, small);
-}
+} RD_ABI_CATCH("rd_closed_form")

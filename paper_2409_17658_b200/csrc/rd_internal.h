@@ -9,8 +9,16 @@
 namespace rd {
 
 // Records a thread-local message for rd_last_error() and returns `code`.
-int fail(int code, const char *fmt, ...);
-void clear_error();
+int fail(int code, const char *fmt, ...) noexcept;
+void clear_error() noexcept;
+
+// The C-ABI never lets an exception out (rd.h "Errors"): every entry point with an int status
+// is a function-try-block ending in RD_ABI_CATCH, which maps the in-flight exception to a
+// status: std::bad_alloc / std::length_error (a host allocation) -> RD_ENOMEM, anything
+// else -> RD_EINVAL with the exception's text.
+int abi_exception(const char *who) noexcept;
+#define RD_ABI_CATCH(who) \
+  catch (...) { return ::rd::abi_exception(who); }
 
 // Number of correct words of length m (Def 4); -1 if m is out of range.
 int64_t count_words(int m);

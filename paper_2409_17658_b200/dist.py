@@ -278,19 +278,23 @@ def power_sequence_allgather(m: int, kmax: int = 50, alpha_max: int = 10, policy
     on_gpu = acc is None
     device = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
     A_rows = torch.from_numpy(np.ascontiguousarray(A[r0:r1])).to(device)
-    d = np.diag(A)[r0:r1] if r1 > r0 else np.array([], dtype=A.dtype)
-    fin = d[d < RD_INF]
-    d1 = int(fin.min()) if fin.size else 2**31 - 1
-    if world > 1:
-        tt = torch.tensor([d1], dtype=torch.int64, device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MIN, group=group)
-        d1 = int(tt.item())
     if stats is None:
         from . import rd_panel_stats, rd_stats_len
         sbuf = torch.empty(rd_stats_len(alpha_max), dtype=torch.int32, device=device)
 
         def stats(cur, prevs):
             return rd_panel_stats(cur, prevs, r0, alpha_max, sbuf)
+    # diag[1] = min_p (A^1)_pp over this rank's rows (Cor 7 at k = 1): the stats kernel's
+    # diagonal min of the panel with no earlier power
+    d1 = 2**31 - 1
+    if r1 > r0:
+        d1 = int(stats(A_rows, []).cpu()[0])
+        if d1 >= RD_INF:
+            d1 = 2**31 - 1
+    if world > 1:
+        tt = torch.tensor([d1], dtype=torch.int64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MIN, group=group)
+        d1 = int(tt.item())
     ring = {1: A_rows.clone()}
     if on_gpu:
         torch.cuda.synchronize()

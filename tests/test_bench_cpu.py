@@ -26,6 +26,37 @@ def test_reference_arm_line():
 
 def test_reference_arm_nonzero_rank_is_silent():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--order-m", "5"],
-                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--order-m", "5",
+                        "--gpus", "2"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_world_must_match_gpus():
+    """A launcher that started a different number of ranks than --gpus is refused."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--order-m", "5",
+                        "--gpus", "4"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2 and "launcher started 2" in r.stderr
+
+
+def test_launch_command_shape():
+    sys.path.insert(0, ROOT)
+    import bench
+    cmd = bench.launch_command(["--gpus", "8", "--steps", "3"], 8, 29511)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and "--nnodes=1" in cmd and "127.0.0.1" in cmd
+    assert cmd[-3:] == ["8", "--steps", "3"] and cmd[-5].endswith("bench.py")
+
+
+def test_self_launch_reference_two_ranks():
+    """`bench.py --gpus 2` without torchrun starts two ranks itself: rank 0 prints one line with
+    n_gpus = 2, rank 1 exits 0 without work (the reference arm needs no GPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--order-m", "5",
+                        "--gpus", "2", "--steps", "2", "--warmup", "1", "--cpu-seconds", "0.2"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"

@@ -91,6 +91,25 @@ def test_bench_two_ranks_one_gpu_gloo():
     assert d["time_to_periodicity"]["5"]["triple"] == [16, 5, 12]
 
 
+def test_bench_self_launch_two_ranks():
+    # `bench.py --gpus 2` WITHOUT torchrun (the driver's plain invocation): bench.py starts the
+    # two ranks itself; the gloo hook puts both on cuda:0 (functional check, not a perf number)
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env.update(RD_DIST_BACKEND="gloo", RD_FORCE_DEVICE="0")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--order-m", "7", "--steps", "3",
+           "--warmup", "22", "--no-cpu-baseline", "--ttp-m", "5", "--ttp-structured-only-m", "--gops-m",
+           "--invariance-m", "0"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["backend"] == "gloo"
+    assert d["config"]["detected"] == [21, 5, 16]
+    assert d["e2e"]["triple"] == [21, 5, 16]
+    assert d["time_to_periodicity"]["5"]["triple"] == [16, 5, 12]
+
+
 PEER_WORKER = r'''
 import json, os, sys
 sys.path.insert(0, os.environ["ROOT"])

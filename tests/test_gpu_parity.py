@@ -505,10 +505,9 @@ def test_panel_sequential_driver_matches_oracle(m, rows, method):
 
 
 
-@pytest.mark.skipif(__import__("os").environ.get("RD_LONG") != "1", reason="~15 min of GPU; RD_LONG=1")
 def test_m11_panel_sequential_pins():
-    # m = 11 (N = 191476) on one GPU, panel by panel: Cor 12 (24n/5 for 5 | n) and
-    # the independent row DP X3 for n = 3..10
+    # m = 11 (N = 191476) on one GPU, panel by panel with the slab structured step (~50 s):
+    # Cor 12 (24n/5 for 5 | n) and the independent row DP X3 for n = 3..10
     from paper_2409_17658_b200 import dist as rdist
     got = rdist.power_sequence_panels(11, 45, alpha_max=5, panel_rows=57344, method=1)
     assert got["found"]
@@ -594,12 +593,68 @@ def test_every_power_sampled_rows_full_size(m, method):
     ch.close()
 
 
+@pytest.mark.parametrize("method", [0, 1])
+def test_m8_every_power_full_matrix(method):
+    """Alg 2 step 4 compares whole matrices: at m = 8 (N = 7411) every power A^k,
+    k = 1..26 (first detection, Table 2), equals the oracle's X4 chain entry for entry —
+    dense GEMM chain (method 0) and structured chain (method 1)."""
+    ch = rd.Chain(8, alpha_max=10, method=method)
+    for k, X in O.powers(8, 26):
+        if k > 1:
+            ch.step()
+        got = ch.read_rows(k)
+        assert (got == to_inf(X, OINF, RINF, np.int16)).all(), (method, k)
+    ch.close()
+
+
+def _digest16(X16):
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(X16.astype("<i2")).tobytes(), digest_size=8).hexdigest()
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_m9_every_power_full_matrix_hash(method, golden):
+    """m = 9 (N = 21909): every full power A^k, k = 1..27 (k* of Table 2), hashed (BLAKE2b-64 of
+    the row-major int16 matrix, inf = 0x3FFF) equals the digest of the oracle's X4 chain written
+    by tools/make_golden.py (oracle only) — plus its inf count and diagonal min."""
+    g = golden("m9_power_hashes.json")
+    assert g["N"] == 21909 and g["kmax"] == 27
+    ch = rd.Chain(9, alpha_max=2, method=method)
+    for k in range(1, 28):
+        if k > 1:
+            s = ch.step().cpu().numpy()
+            assert int(s[0]) == g["powers"][str(k)]["diag_min"], k
+        X = ch.read_rows(k)
+        want = g["powers"][str(k)]
+        assert int((X == RINF).sum()) == want["n_inf"], (method, k)
+        assert _digest16(X) == want["blake2b64"], (method, k)
+    ch.close()
+
+
+def test_border_n11_erratum_on_gpu(golden):
+    """P:664 claims 2 L_a(n) = n for 10 <= n <= 30; at n = 11 the library's border chain
+    (App. A matrix, dense and structured) gives the oracle row DP's value written by
+    tools/make_golden.py (12, R16)."""
+    want = golden("border_n11_rowdp.json")
+    assert want["n"] == 11 and want["value"] == 12
+    A = rd.rd_build_matrix_border()
+    for method in (0, 1):
+        got = rd.rd_power_sequence_matrix(A, 50, 10, 0, method)
+        assert got["diag"][11] == want["value"]
+        for n in range(10, 31):
+            if n != 11:
+                assert got["diag"][n] == n if n <= got["k_stop"] else True
+
+
 def test_device_allocation_failure_is_reported():
-    # a dense m = 11 chain with a 33-power ring needs ~2.4 TB: RD_ENOMEM, no crash, and the
-    # device stays usable
+    # a dense m = 11 chain with a 33-power ring needs ~2.4 TB: RD_ENOMEM from the device-memory
+    # check before any host build (fast), no crash, and the device stays usable
+    import time
+    t0 = time.perf_counter()
     with pytest.raises(rd.RDError) as e:
         rd.Chain(11, alpha_max=32)
-    assert e.value.status in (rd.RD_ENOMEM, rd.RD_EINVAL)
+    assert e.value.status == rd.RD_ENOMEM and "GB free" in str(e.value)
+    assert time.perf_counter() - t0 < 5.0
     with pytest.raises(rd.RDError) as e:
         rd.Chain(3, alpha_max=17, method=1)          # structured step: alpha_max <= 16
     assert e.value.status == rd.RD_EINVAL
@@ -851,3 +906,60 @@ def test_structured_chain_nnz_pins_m9_m10():
         ch = rd.Chain(m, alpha_max=5, row_begin=0, row_end=8, method=1)
         assert ch.terms_per_step == 8 * nnz, m
         ch.close()
+
+
+# ------------------------------------------- orders with N >= 2^17 (q-chunked CSC) --
+def _oracle_rows_a1(m, rows):
+    W = O.words(m)
+    out = np.full((len(rows), len(W)), rd.RD_INF, dtype=np.int16)
+    for r, q in enumerate(rows):
+        for p, wp in enumerate(W):
+            if O.can_follow(W[q], wp):
+                out[r, p] = O.label(wp)
+    return out
+
+
+def test_m11_operands_decode_rows_beyond_2_17():
+    """m = 11 (N = 191476 >= 2^17): the CSC entries hold q - ch * Qc in 17 bits, so the operand
+    scatter must decode per q-chunk; rows on both sides of 2^17 of the dense chain's A^1 panel
+    (scatter_dense_operands_kernel) and of the peer chain's A^1 slot (scatter_rp_kernel) equal
+    the oracle's can-follow rules and labels."""
+    N = rd.count_words(11)
+    assert N == 191476 > (1 << 17)
+    r0 = (1 << 17) - 64                     # a 128-row panel straddling q = 2^17
+    ch = rd.Chain(11, alpha_max=1, row_begin=r0, row_end=r0 + 128)
+    got = ch.read_rows(1)
+    ch.close()
+    sample = [0, 63, 64, 65, 127]
+    want = _oracle_rows_a1(11, [r0 + i for i in sample])
+    assert (got[sample] == want).all()
+    # the peer all-gather chain's own panel of A^1 (RP slot) for the rank holding rows >= 2^17
+    bounds = [min(N, b) for b in range(0, N + 12032, 12032)]
+    if bounds[-1] != N:
+        bounds.append(N)
+    rank = next(s for s in range(len(bounds) - 1) if bounds[s] <= 140000 < bounds[s + 1])
+    ag = rd.AgChain(11, bounds, rank, alpha_max=1)
+    rows = ag.read_rows(1)
+    ag.close()
+    pick = [140000 - bounds[rank], bounds[rank + 1] - 1 - bounds[rank]]
+    assert (rows[pick] == _oracle_rows_a1(11, [bounds[rank] + i for i in pick])).all()
+
+
+@pytest.mark.parametrize("m", [1, 3, 5, 7, 8])
+def test_roman_cylinder_ex_dense_equals_structured_and_formulas(m):
+    """rd_roman_cylinder_ex: the dense GEMM chain (method 0) and the structured chain (method 1)
+    give the same gamma; both equal the oracle chain's (Alg 1 / Prop 8) for n = 3..60."""
+    ref = O.power_chain(m, 50, 10, 0) if m <= 7 else None
+    for n in range(3, 61):
+        g0 = rd.rd_roman_cylinder(m, n, method=0)
+        g1 = rd.rd_roman_cylinder(m, n, method=1)
+        assert g0 == g1, (m, n)
+        if ref is not None:
+            assert g0 == O.gamma_from_chain(ref, n), (m, n)
+        elif m == 8:
+            c = (18 * n + 4) // 5
+            f8 = c if n % 5 == 0 else (c + 1 if (n % 5 in (2, 3, 4) or n == 6) else c + 2)
+            assert g0 == (13 if n == 3 else f8), n     # P:443-448 with the R10 erratum at n = 3
+    with pytest.raises(rd.RDError) as e:
+        rd.rd_roman_cylinder(m, 5, method=2)
+    assert e.value.status == rd.RD_EINVAL

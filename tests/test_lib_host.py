@@ -160,3 +160,57 @@ def test_closed_form_rejects_bad_input():
     bad["diag"][bad["k_stop"]] += 1
     with pytest.raises(rd.RDError):
         rd.rd_closed_form_from(bad)
+
+
+OOM_SCRIPT = r"""
+import ctypes, resource, sys
+sys.path.insert(0, sys.argv[1])
+import paper_2409_17658_b200 as rd
+L = rd.lib()
+n = ctypes.c_int64()
+assert L.rd_build_states(12, None, ctypes.byref(n)) == 0 and n.value == 566059
+
+def vmsize():
+    for line in open("/proc/self/status"):
+        if line.startswith("VmSize:"):
+            return int(line.split()[1]) * 1024
+
+resource.setrlimit(resource.RLIMIT_AS, (vmsize() + (256 << 10), resource.RLIM_INFINITY))
+rc = L.rd_build_states(12, None, ctypes.byref(n))
+resource.setrlimit(resource.RLIMIT_AS, (resource.RLIM_INFINITY, resource.RLIM_INFINITY))
+print("RC", rc, L.rd_last_error().decode())
+rc2 = L.rd_build_states(12, None, ctypes.byref(n))
+print("AFTER", rc2, n.value)
+"""
+
+
+def test_host_allocation_failure_is_enomem_not_abort(tmp_path):
+    """rd.h: the C-ABI never aborts or throws.  With the address space capped just above what the
+    process uses, the host word list of m = 12 (2.2 MB) cannot be allocated: the call returns
+    RD_ENOMEM with a message instead of letting std::bad_alloc terminate the process, and the
+    next call (limit lifted) succeeds."""
+    import subprocess
+    import sys
+    f = tmp_path / "oom.py"
+    f.write_text(OOM_SCRIPT)
+    r = subprocess.run([sys.executable, str(f), ROOT], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert f"RC {rd.RD_ENOMEM} rd_build_states: host allocation failed" in r.stdout
+    assert "AFTER 0 566059" in r.stdout
+
+
+def test_every_status_entry_is_a_function_try_block():
+    """Every C-ABI entry returning a status (int) in the library sources ends in RD_ABI_CATCH, so no
+    C++ exception crosses the ABI (rd.h "Errors")."""
+    import re
+    csrc = os.path.join(ROOT, "paper_2409_17658_b200", "csrc")
+    plain = {"rd_stats_len", "rd_stats_decide", "rd_chain_current_k"}   # no allocation, no status
+    for fn in ("rd_cuda.cu", "rd_host.cpp"):
+        src = open(os.path.join(csrc, fn)).read()
+        for mt in re.finditer(r'extern "C" int (rd_[a-z0-9_]+)\(', src):
+            name = mt.group(1)
+            if name in plain:
+                continue
+            body_start = src.index("{", mt.end())
+            assert src[mt.end():body_start].rstrip().endswith("try"), name
+            assert f'RD_ABI_CATCH("{name}")' in src, name

@@ -195,6 +195,28 @@ def test_erratum_witness_7_6(golden):
     assert f.shape == (7, 6)
     assert O.rdf_weight(f) == 20          # a valid RDF of weight 20 < formula 21
     assert O.gamma_rowdp(7, 6) == 20
+    # the checker rejects what is not an RDF (Def): every 0 needs a neighbour with 2
+    for r, c in zip(*np.nonzero(f == 2)):
+        g = f.copy()
+        g[r, c] = 0                        # drop one 2: some 0 (or this vertex) loses its 2-neighbour
+        assert O.rdf_weight(g) == -1, (r, c)
+    g = f.copy()
+    g[0, 0] = 3                            # values outside {0, 1, 2}
+    assert O.rdf_weight(g) == -1
+    g = f.copy()
+    g[g == 0] = 1                          # all-nonzero: valid, weight = sum of values
+    assert O.rdf_weight(g) == int(g.sum())
+    # domination wraps around the cycle (columns n-1 and 0 are adjacent) but not the path ends
+    h = np.zeros((1, 4), dtype=np.int32)
+    h[0, 0], h[0, 2] = 2, 0
+    h[0, 2] = 2
+    assert O.rdf_weight(h) == 4
+    h = np.zeros((2, 3), dtype=np.int32)
+    h[0, 0] = 2                            # (0,1) (0,2) via the cycle, (1,0) below; (1,1) undominated
+    assert O.rdf_weight(h) == -1
+    h[1, 1] = 1
+    h[1, 2] = 1
+    assert O.rdf_weight(h) == 4
 
 
 def test_erratum_8_3():
