@@ -85,6 +85,8 @@ def lib():
         L.rd_set_gemm_variant.argtypes = [ci]
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
+        L.rd_set_stream_k.argtypes = [ci]
+        L.rd_set_stream_k.restype = ci
         L.rd_set_gemm_tma.argtypes = [ci]
         L.rd_set_gemm_tma.restype = ci
         L.rd_set_sparse_bytes.argtypes = [ci]
@@ -335,6 +337,11 @@ def rd_set_gemm_tma(mode):
 def rd_set_split_k(enable: bool):
     """Split-K for small dense chain grids (default on; identical results)."""
     _check(lib().rd_set_split_k(1 if enable else 0))
+
+
+def rd_set_stream_k(mode: int):
+    """Stream-K remainder of dense chain steps (rd.h): 0 off, 1 model (default), 2 forced."""
+    _check(lib().rd_set_stream_k(int(mode)))
 
 
 def rd_set_sparse_bytes(mode):

@@ -14,8 +14,10 @@ LIB = os.path.join(PKG, "librd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES = ["rd_host.cpp", "rd_cuda.cu"]
-HEADERS = ["rd_internal.h", os.path.join(INCLUDE, "rd.h")]
+CUDA_UNITS = ["rd_cuda.cu", "rd_gemm_pm_stats.cu", "rd_gemm_pm_stats_tma.cu", "rd_gemm_pm_part.cu",
+              "rd_gemm_row_rp.cu", "rd_gemm32.cu", "rd_gemm_pm_sk.cu"]
+SOURCES = ["rd_host.cpp"] + CUDA_UNITS
+HEADERS = ["rd_internal.h", "rd_gemm.cuh", "rd_gemm_kernels.cuh", os.path.join(INCLUDE, "rd.h")]
 
 
 def _stale() -> bool:
@@ -27,29 +29,40 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles the host unit and the CUDA units in parallel (the GEMM instances live in
+    separate units), then links librd.so; ptxas -v output goes to build/ptxas.log."""
+    from concurrent.futures import ThreadPoolExecutor
     if not force and not _stale():
         return LIB
     bdir = os.path.join(PKG, "build")
     os.makedirs(bdir, exist_ok=True)
-    host_o = os.path.join(bdir, "rd_host.o")
-    cuda_o = os.path.join(bdir, "rd_cuda.o")
-    cmds = [
-        ["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-I", INCLUDE, "-c",
-         os.path.join(CSRC, "rd_host.cpp"), "-o", host_o],
-        [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "-Xptxas", "-v",
-         "-I", INCLUDE, "-c", os.path.join(CSRC, "rd_cuda.cu"), "-o", cuda_o],
-        [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", host_o, cuda_o, "-o", LIB + ".tmp",
-         "-lgomp", "-lpthread"],
-    ]
-    for c in cmds:
-        r = subprocess.run(c, capture_output=True, text=True)
+    objs = [os.path.join(bdir, os.path.splitext(u)[0] + ".o") for u in SOURCES]
+    cmds = [["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-I", INCLUDE, "-c",
+             os.path.join(CSRC, "rd_host.cpp"), "-o", objs[0]]]
+    for u, o in zip(CUDA_UNITS, objs[1:]):
+        cmds.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "-Xptxas", "-v",
+                     "-I", INCLUDE, "-c", os.path.join(CSRC, u), "-o", o])
+
+    def run(c):
+        return c, subprocess.run(c, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(run, cmds))
+    log = []
+    for c, r in results:
         if verbose or r.returncode != 0:
             sys.stderr.write(" ".join(c) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
-            raise RuntimeError(f"build failed: {' '.join(c[:2])}")
-        if "ptxas" in " ".join(r.stderr.splitlines()[:0]) or (c[0] == NVCC and "-c" in c):
-            with open(os.path.join(bdir, "ptxas.log"), "w") as f:
-                f.write(r.stderr)
+            raise RuntimeError(f"build failed: {' '.join(c[:2])} {c[-3]}")
+        if c[0] == NVCC:
+            log.append(f"==== {c[-3]}\n" + r.stderr)
+    with open(os.path.join(bdir, "ptxas.log"), "w") as f:
+        f.write("".join(log))
+    link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB + ".tmp", "-lgomp", "-lpthread"]
+    r = subprocess.run(link, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(link) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError("link failed")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

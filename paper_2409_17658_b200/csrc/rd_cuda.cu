@@ -34,8 +34,15 @@
 #include <vector>
 
 #include "rd_internal.h"
+#include "rd_gemm.cuh"
 
 using namespace rd;
+
+namespace rd {
+// row-tiles per rasterisation group; measured at m = 9 (ncu DRAM read per launch): 8 -> 37.7 GB,
+// 12 -> 41.3, 16 -> 47.4, 24 -> 68.5, 32 -> 85.8 GB, the same 276 ms (DESIGN.md §5)
+int g_raster_group = kGroup;
+}  // namespace rd
 
 // Scoped NVTX range (one per power step / chain build / power sequence)
 struct NvtxRange {
@@ -51,22 +58,7 @@ static inline void rd_enter() {
   (void)cudaGetLastError();
 }
 
-#define RD_CUDA_CHECK(expr)                                                                     \
-  do {                                                                                          \
-    cudaError_t e_ = (expr);                                                                    \
-    if (e_ != cudaSuccess) return fail(RD_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
-                                       __FILE__, __LINE__);                                     \
-  } while (0)
-
 namespace {
-
-constexpr uint32_t kInf2 = 0x3FFF3FFFu;
-constexpr int kThreads = 256;
-constexpr int kBK2 = 32;      // k-pairs per pipeline stage (64 k)
-constexpr int kStages = 3;
-constexpr int kGroup = 8;     // row-tiles per rasterisation group
-constexpr int kStageWords = 2 * kBK2 * kTile;   // u32 per stage (left + right tile)
-constexpr size_t kSmemBytes = (size_t)kStages * kStageWords * 4;   // 96 KB (2 CTAs/SM)
 
 // ------------------------------------------------------------------ packing --
 // Row-major int16 X (rows x cols, ld) -> PM u32 XT[cols_p/2][rows_p] (ld = rows_p).
@@ -160,428 +152,6 @@ __global__ void stats_init_kernel(int32_t *s, int alpha_max) {
   s[i] = (i == 0 || q == 0 || q == 1) ? INT_MAX : 0;
 }
 
-__device__ __forceinline__ void stats_pair(uint32_t o, uint32_t w, uint32_t &lo2, uint32_t &hi2, uint32_t &mis,
-                                           uint32_t &fin) {
-  const uint32_t eo = __vcmpeq2(o, kInf2), ew = __vcmpeq2(w, kInf2);
-  const uint32_t d = __vsub2(o, w);
-  if (!(eo | ew)) {            // both lanes finite in both powers (every entry from k = 4 on)
-    fin = 0xFFFFFFFFu;
-    lo2 = __vmins2(lo2, d);
-    hi2 = __vmaxs2(hi2, d);
-    return;
-  }
-  mis |= eo ^ ew;
-  const uint32_t fm = ~(eo | ew);
-  fin |= fm;
-  lo2 = __vmins2(lo2, (d & fm) | (0x7FFF7FFFu & ~fm));
-  hi2 = __vmaxs2(hi2, (d & fm) | (0x80008000u & ~fm));
-}
-// --------------------------------------------------------------------- GEMM --
-struct EpiArgs {
-  const uint32_t *prev[kMaxAlpha];  // PM slots of A^{k+1-a}, a = 1..nprev, same ld as C
-  int nprev;
-  int32_t *stats;          // MIN-reducible stats vector (nullable: no stats)
-  int64_t diag_row0;       // global row index of local row 0 (row panels)
-  int accumulate;          // row-major output only: C = min(C, X (x) B)
-  int64_t split_stride;    // split-K (gridDim.y > 1, PM output): u32 between the splits' partial tiles
-  const int *spread_in;    // structured step: 1 if some row of X has a finite spread > 254 (nullable)
-  int *spread_out;         // ... the same flag for the output, for the next step (nullable)
-};
-
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
-  return r;
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
-// mbarrier + TMA (cp.async.bulk.tensor) primitives for the TMA mainloop
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "RD_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra RD_WAIT_%=;\n}" ::"r"(
-          smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-// Tensor maps of a dense chain's operands for the TMA mainloop: X = the ring of PM slots
-// ({Mp, P/2, slots} u32, box 128 x 32 x 1), B = the packed operand ({P, P/2} u32, box 128 x 32).
-struct TmaOps {
-  CUtensorMap x, b;
-  int xslot;
-};
-
-// One CTA computes a 128 x 128 tile of C; 256 threads in a 16 x 16 grid, each thread an
-// 8 x 8 register micro-tile: rows {ty*4 + 0..3, 64 + ty*4 + 0..3}, columns
-// {tx*4 + 0..3, 64 + tx*4 + 0..3}.  Per k-pair a thread reads 4 x LDS.128 and issues 64
-// VIADDMNMX.S16x2 (128 (min,+) terms).  Stages of 32 k-pairs of both operands (32 KB) flow
-// through a 3-deep shared-memory ring, filled either by every thread's cp.async (TMA =
-// false) or, TMA = true (kOutPM only), by one thread's two cp.async.bulk.tensor copies per
-// stage with mbarrier completion and per-warp release (DESIGN.md §5 "Mainloop loads").
-//   OUT = kOutPM : C is PM u32 [N/2][ldc] (pairs along j), no predicates (padded).
-//   OUT = kOutRow: C is row-major int16 with ldc, predicated to (M, N).
-//   OUT = kOutRP : C is RP u32 [M/2][ldc] (pairs along i: C[2p][j] | C[2p+1][j] << 16), and the
-//                  right operand is read straight from the ranks' memory (PeerB): k-pairs
-//                  [t0[s], t0[s+1]) of B live at base[s] (the packed layout, pitch ldb), e.g.
-//                  peer GPUs' ring slots mapped over NVLink (CUDA IPC).  Each stage (32 k-pairs)
-//                  lies inside one rank's range (ranges are whole 128-row tiles), so the
-//                  all-gather of B happens inside the mainloop's cp.async pipeline, tile by tile.
-//
-// Two instruction forms share the mainloop: for accumulator columns
-// c < DPXC each k-pair costs one VIADDMNMX.S16x2 (alu pipe); for c >= DPXC two k-pairs
-// (t, t+1) cost two packed adds s = x + b on IMAD (fma pipe; exact: lane sums <= 0x7FFE
-// never carry) and one VIMNMX3.S16x2 (alu) folding both into the accumulator.  The mix
-// balances the alu pipe, the fma pipe and the issue slot.  `one` is a kernel argument
-// equal to 1, opaque to the compiler so that the add stays an IMAD.
-// Tiles are rasterised in groups of kGroup row-tiles so CTAs resident together share
-// right-operand panels in L2.
-constexpr int kOutRow = 0, kOutPM = 1, kOutRP = 2;
-constexpr int kMaxPeers = 16;
-struct PeerB {
-  const uint32_t *base[kMaxPeers];  // rank s: packed rows of B for k-pairs [t0[s], t0[s+1])
-  int32_t t0[kMaxPeers + 1];
-  int n;
-};
-
-template <int OUT, bool STATS, int DPXC, bool TMA = false>
-__global__ void __launch_bounds__(kThreads, 2)
-minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
-                    int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
-                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb,
-                    const __grid_constant__ TmaOps tma) {
-  extern __shared__ __align__(16) uint32_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
-  // TMA writes need an aligned destination: the TMA variant is launched with 1 KB extra
-  // dynamic shared memory and rounds its stage base up to 1 KB
-  uint32_t *smem = smem_raw;
-  if constexpr (TMA)
-    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 4u;
-  const int tid = threadIdx.x;
-  // a warp covers 4 (ty) x 8 (tx) threads of the 16 x 16 grid: its fragment loads touch 4 and 8
-  // distinct 16-byte chunks (one shared-memory wavefront each)
-  const int wq = tid >> 5, lq = tid & 31;
-  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
-  int64_t i0, j0;
-  {
-    const int bid = blockIdx.x;
-    const int per_group = kgroup * ntj;
-    const int g = bid / per_group, first = g * kgroup;
-    const int gsz = min(nti - first, kgroup);
-    const int w = bid - g * per_group;
-    i0 = (int64_t)(first + w % gsz) * kTile;
-    j0 = (int64_t)(w / gsz) * kTile;
-  }
-
-  // cp.async mapping: 512 16-byte chunks per operand tile (16 rows x 32 chunks)
-  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
-  const uint32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
-  const uint32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
-  const int64_t gx_step8 = 8 * ldx, gb_step8 = 8 * ldb;
-
-  auto load_stage = [&](int stage, int kb) {
-    uint32_t *sx = smem + stage * kStageWords;
-    uint32_t *sb = sx + kBK2 * kTile;
-    const int64_t ox = (int64_t)kb * kBK2 * ldx;
-    const uint32_t *gbk;
-    if constexpr (OUT == kOutRP) {   // the rank holding k-pairs [kb * kBK2, +kBK2)
-      const int tk = kb * kBK2;
-      int s = 0;
-      while (s + 1 < pb.n && tk >= pb.t0[s + 1]) ++s;
-      gbk = pb.base[s] + (int64_t)(tk - pb.t0[s] + ld_row) * ldb + j0 + ld_col;
-    } else {
-      gbk = gb + (int64_t)kb * kBK2 * ldb;
-    }
-#pragma unroll
-    for (int r = 0; r < kBK2; r += 8) {
-      cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
-      cp_async16(sb + (ld_row + r) * kTile + ld_col, gbk + (r / 8) * gb_step8);
-    }
-  };
-
-  uint32_t acc[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
-
-  // split-K (gridDim.y > 1): this CTA folds the k-stages [kb0, kb0 + KB) into a partial tile
-  const int KBt = kpairs / kBK2;
-  const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
-  const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
-  // TMA mainloop: thread 0 issues two bulk-tensor copies per stage (32 KB, completion counted
-  // on full_bar[s]); every warp releases a consumed stage on empty_bar[s]; thread 0 refills
-  // it once all 8 warps have.  No per-thread copy instructions, no CTA-wide barrier.
-  auto tma_issue = [&](int s, int kb) {
-    uint32_t *sx = smem + s * kStageWords;
-    mbar_expect_tx(&full_bar[s], (uint32_t)(kStageWords * 4));
-    tma_load_3d(sx, &tma.x, &full_bar[s], (int)i0, (kb0 + kb) * kBK2, tma.xslot);
-    tma_load_2d(sx + kBK2 * kTile, &tma.b, &full_bar[s], (int)j0, (kb0 + kb) * kBK2);
-  };
-  if constexpr (TMA) {
-    if (tid == 0) {
-#pragma unroll
-      for (int s = 0; s < kStages; ++s) {
-        mbar_init(&full_bar[s], 1);
-        mbar_init(&empty_bar[s], kThreads / 32);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int s = 0; s < kStages && s < KB; ++s) tma_issue(s, s);
-  } else {
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-      if (s < KB) load_stage(s, kb0 + s);
-      cp_async_commit();
-    }
-  }
-
-  for (int kb = 0; kb < KB; ++kb) {
-    if constexpr (TMA) {
-      mbar_wait(&full_bar[kb % kStages], (uint32_t)((kb / kStages) & 1));
-    } else {
-      cp_async_wait<kStages - 2>();
-      __syncthreads();
-      {
-        int nk = kb + kStages - 1;
-        if (nk < KB) load_stage(nk % kStages, kb0 + nk);
-        cp_async_commit();
-      }
-    }
-    const uint32_t *sx = smem + (kb % kStages) * kStageWords;
-    const uint32_t *sb = sx + kBK2 * kTile;
-    if (DPXC >= 8) {
-#pragma unroll
-      for (int t = 0; t < kBK2; ++t) {
-        const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
-        const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
-        const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
-        const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
-        const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-        const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < kBK2; t += 2) {
-        uint32_t x0[8], x1[8], b0[8], b1[8];
-        {
-          const uint4 p = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
-          const uint4 q = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
-          const uint4 u = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + ty * 4);
-          const uint4 v = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
-          x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
-          x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
-        }
-        {
-          const uint4 p = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
-          const uint4 q = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
-          const uint4 u = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + tx * 4);
-          const uint4 v = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
-          b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
-          b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            if (c < DPXC) {
-              acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
-              acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
-            } else {
-              const uint32_t s0 = x0[r] * one + b0[c];
-              const uint32_t s1 = x1[r] * one + b1[c];
-              acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
-            }
-          }
-      }
-    }
-    if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages
-      const int s = kb % kStages;
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&empty_bar[s]);
-      if (tid == 0 && kb + kStages < KB) {
-        mbar_wait(&empty_bar[s], (uint32_t)((kb / kStages) & 1));
-        tma_issue(s, kb + kStages);
-      }
-    }
-  }
-  if constexpr (!TMA) cp_async_wait<0>();
-
-  // ---------------------------------------------------------------- epilogue --
-  // v = min(lo, hi) per accumulator; pairs (c, c+1) packed (min_c | min_{c+1} << 16).
-  uint32_t out[8][4];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      uint32_t a0 = acc[r][2 * p], a1 = acc[r][2 * p + 1];
-      out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
-    }
-
-  // RP word (rows 2q', 2q'+1 of row group g; columns h*64 + tx*4 + e) from the folded pairs
-  auto rp_word = [&](int g, int q, int h, int e) -> uint32_t {
-    const uint32_t a = out[g * 4 + 2 * q][2 * h + (e >> 1)], b = out[g * 4 + 2 * q + 1][2 * h + (e >> 1)];
-    return prmt(a, b, (e & 1) ? 0x7632 : 0x5410);
-  };
-  if constexpr (OUT == kOutRP) {
-    uint32_t *C = reinterpret_cast<uint32_t *>(Cv);
-#pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
-          const uint4 v = make_uint4(rp_word(g, q, h, 0), rp_word(g, q, h, 1), rp_word(g, q, h, 2), rp_word(g, q, h, 3));
-          *reinterpret_cast<uint4 *>(C + pr * ldc + j0 + h * 64 + tx * 4) = v;
-        }
-  } else if constexpr (OUT == kOutPM) {
-    uint32_t *C = reinterpret_cast<uint32_t *>(Cv) + (int64_t)blockIdx.y * epi.split_stride;
-#pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        // column pair jp covers columns j0 + (p>>1)*64 + tx*4 + (p&1)*2 + {0,1}
-        int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-        uint4 v = make_uint4(out[g * 4 + 0][p], out[g * 4 + 1][p], out[g * 4 + 2][p], out[g * 4 + 3][p]);
-        *reinterpret_cast<uint4 *>(C + jp * ldc + i0 + g * 64 + ty * 4) = v;
-      }
-  } else {
-    int16_t *C = reinterpret_cast<int16_t *>(Cv);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
-      if (i >= M) continue;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2;
-        int v0 = (int)(out[r][p] & 0xFFFF), v1 = (int)(out[r][p] >> 16);
-        if (epi.accumulate) {
-          if (j < N) v0 = min(v0, min((int)C[i * ldc + j], (int)RD_INF));
-          if (j + 1 < N) v1 = min(v1, min((int)C[i * ldc + j + 1], (int)RD_INF));
-        }
-        if (j < N) C[i * ldc + j] = (int16_t)v0;
-        if (j + 1 < N) C[i * ldc + j + 1] = (int16_t)v1;
-      }
-    }
-  }
-
-  if (!STATS) return;
-
-  // ---- fused reductions over this tile (MIN-reducible; see rd.h rd_chain_step) ----
-  __shared__ int32_t red[kThreads / 32][1 + 4 * kMaxAlpha];
-  const int warp = tid >> 5, lane = tid & 31;
-
-  // diagonal min (Cor 7): global row diag_row0 + i == column j
-  int32_t dmin = INT_MAX;
-  {
-    const int64_t gi0 = epi.diag_row0 + i0;
-    if (gi0 < j0 + kTile && j0 < gi0 + kTile) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            int64_t gi = gi0 + (r >> 2) * 64 + ty * 4 + (r & 3);
-            int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2 + h;
-            int32_t v = (int32_t)((out[r][p] >> (16 * h)) & 0xFFFF);
-            if (gi == j && v < dmin) dmin = v;
-          }
-    }
-  }
-  dmin = __reduce_min_sync(0xffffffffu, dmin);
-  if (lane == 0) red[warp][0] = dmin;
-
-  // periodicity stats against A^{k+1-a}: same PM address in the previous slots
-  for (int a = 0; a < epi.nprev; ++a) {
-    const uint32_t *P = epi.prev[a];
-    uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
-    if constexpr (OUT == kOutRP) {
-#pragma unroll
-      for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
-            const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + pr * ldc + j0 + h * 64 + tx * 4));
-            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) stats_pair(rp_word(g, q, h, e), pw[e], lo2, hi2, mis, fin);
-          }
-    } else {
-#pragma unroll
-      for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-          uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
-          const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
-        }
-    }
-    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
-    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
-    if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
-    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
-    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
-    int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
-    int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
-    if (lane == 0) {
-      red[warp][1 + 4 * a + 0] = v0;
-      red[warp][1 + 4 * a + 1] = v1;
-      red[warp][1 + 4 * a + 2] = v2;
-      red[warp][1 + 4 * a + 3] = v3;
-    }
-  }
-  __syncthreads();
-  const int nval = 1 + 4 * epi.nprev;
-  for (int e = tid; e < nval; e += kThreads) {
-    int32_t v = red[0][e];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) v = min(v, red[w][e]);
-    atomicMin(epi.stats + e, v);
-  }
-}
-
 // Split-K combine for small grids: C = min over the nsplit partial PM tiles in W (HBM-bound,
 // 16-byte accesses), written into the chain's ring slot, with the diagonal min and the
 // periodicity stats of alphas [a0, a0 + 8) fused (pass a0 > 0 re-reads C instead of W).
@@ -656,23 +226,84 @@ __global__ void __launch_bounds__(256) combine_pm_kernel(const uint32_t *__restr
   }
 }
 
+// Stream-K combine: the remainder tiles [nfull, ntiles) of a step whose stream-K CTAs wrote
+// partial PM tiles (segment s at ws + s * stride): one CTA per tile takes the min over the
+// tile's segments, stores the power into the ring slot C and computes its diagonal min and the
+// periodicity stats of every alpha in one pass (the tile is held in registers; HBM/L2-bound).
+__global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restrict__ ws, int64_t stride,
+                                                         uint32_t *__restrict__ C, int64_t ldc, int nti, int ntj,
+                                                         int kgroup, int KBt, EpiArgs epi) {
+  __shared__ int32_t red[8][1 + 4 * kMaxAlpha];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = blockIdx.x;
+  const int64_t R = (int64_t)(nti * ntj - epi.sk_nfull) * KBt;
+  const int s0 = sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
+  const int nseg = sk_owner((int64_t)(r + 1) * KBt - 1, R, epi.sk_nsk) - s0 + 1;
+  int64_t i0, j0;
+  tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);
+  // the tile in PM: 64 k-pair rows (jp) of 128 u32 (i); thread: 8 uint4 at rows jr = w*8 + warp
+  uint4 o[8];
+  int32_t dmin = INT_MAX;
+  const int ic = lane * 4;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int jr = w * 8 + warp;
+    const int64_t e = (j0 / 2 + jr) * ldc + i0 + ic;
+    uint4 v = *reinterpret_cast<const uint4 *>(ws + e);
+    for (int sg = 1; sg < nseg; ++sg) {
+      const uint4 u = *reinterpret_cast<const uint4 *>(ws + (int64_t)sg * stride + e);
+      v.x = __vmins2(v.x, u.x); v.y = __vmins2(v.y, u.y); v.z = __vmins2(v.z, u.z); v.w = __vmins2(v.w, u.w);
+    }
+    *reinterpret_cast<uint4 *>(C + e) = v;
+    o[w] = v;
+    // diagonal (Cor 7): global row diag_row0 + i0 + ic + q meets column j0 + 2 jr + h
+    const uint32_t ow[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t gi = epi.diag_row0 + i0 + ic + q, j = j0 + 2 * jr;
+      if (gi == j) dmin = min(dmin, (int)(ow[q] & 0xFFFF));
+      if (gi == j + 1) dmin = min(dmin, (int)(ow[q] >> 16));
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+  for (int a = 0; a < epi.nprev; ++a) {
+    const uint32_t *P = epi.prev[a];
+    uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int jr = w * 8 + warp;
+      const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + (j0 / 2 + jr) * ldc + i0 + ic));
+      stats_pair(o[w].x, pv.x, lo2, hi2, mis, fin);
+      stats_pair(o[w].y, pv.y, lo2, hi2, mis, fin);
+      stats_pair(o[w].z, pv.z, lo2, hi2, mis, fin);
+      stats_pair(o[w].w, pv.w, lo2, hi2, mis, fin);
+    }
+    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
+    if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
+    const int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    const int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
+    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
+    if (lane == 0) {
+      red[warp][1 + 4 * a + 0] = v0;
+      red[warp][1 + 4 * a + 1] = v1;
+      red[warp][1 + 4 * a + 2] = v2;
+      red[warp][1 + 4 * a + 3] = v3;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 1 + 4 * epi.nprev; e += 256) {
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = min(v, red[w][e]);
+    atomicMin(epi.stats + e, v);
+  }
+}
+
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
 int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
-// row-tiles per rasterisation group; measured at m = 9 (ncu DRAM read per launch): 8 -> 37.7 GB,
-// 12 -> 41.3, 16 -> 47.4, 24 -> 68.5, 32 -> 85.8 GB, the same 276 ms (DESIGN.md §5)
-int g_raster_group = kGroup;
-
-// ----------------------------------------------------------- 32-bit GEMM --
-// The generic product for entries beyond the int16 headroom (the
-// `__viaddmin_s32` variant; rd.h rd_minplus_mul32).  Same CTA tile, thread tile, cp.async
-// pipeline and rasterisation as minplus_gemm_kernel, one int32 per k instead of a k-pair:
-//   XT[k][i] = X[i][k]  (left operand transposed, [Kp][Mp]),  BP[k][j] = B[k][j]  ([Kp][Np]),
-// both INF32-padded to the tile, entries clamped to [., RD_INF32] on packing.  Per k a thread
-// reads 4 x LDS.128 and updates 64 accumulators: columns c < DPXC with one VIADDMNMX (32-bit,
-// alu), the others two k at a time with two IMAD adds (fma; exact: sums <= 0x7FFFFFFE) and one
-// VIMNMX3 (alu).  RD_INF32 + anything >= RD_INF32, and accumulators start at RD_INF32, so
-// infinite results come out exactly RD_INF32 (finite sums >= RD_INF32 saturate to it).
-constexpr int32_t kInf32 = RD_INF32;
 
 __global__ void pack_t32_kernel(const int32_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
                                 int32_t *__restrict__ XT, int64_t ldt, int64_t kp) {
@@ -697,141 +328,25 @@ __global__ void pack_copy32_kernel(const int32_t *__restrict__ B, int64_t ld, in
   BP[k * ldp + j] = (j < N && k < K) ? min(B[k * ld + j], kInf32) : kInf32;
 }
 
-template <int DPXC>
-__global__ void __launch_bounds__(kThreads, 2)
-minplus_gemm32_kernel(const int32_t *__restrict__ XT, int64_t ldx, const int32_t *__restrict__ BP, int64_t ldb,
-                      int kp, int32_t *__restrict__ C, int64_t ldc, int64_t M, int64_t N, int nti, int ntj,
-                      int32_t one, int accumulate, int kgroup) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  const int tid = threadIdx.x;
-  const int wq = tid >> 5, lq = tid & 31;
-  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
-  int64_t i0, j0;
-  {
-    const int bid = blockIdx.x;
-    const int per_group = kgroup * ntj;
-    const int g = bid / per_group, first = g * kgroup;
-    const int gsz = min(nti - first, kgroup);
-    const int w = bid - g * per_group;
-    i0 = (int64_t)(first + w % gsz) * kTile;
-    j0 = (int64_t)(w / gsz) * kTile;
-  }
-  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
-  const int32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
-  const int32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
-  auto load_stage = [&](int stage, int kb) {
-    uint32_t *sx = smem + stage * kStageWords;
-    uint32_t *sb = sx + kBK2 * kTile;
-    const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
-#pragma unroll
-    for (int r = 0; r < kBK2; r += 8) {
-      cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * 8 * ldx);
-      cp_async16(sb + (ld_row + r) * kTile + ld_col, gb + ob + (r / 8) * 8 * ldb);
-    }
-  };
-  int32_t acc[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = kInf32;
-  const int KB = kp / kBK2;
-#pragma unroll
-  for (int st = 0; st < kStages - 1; ++st) {
-    if (st < KB) load_stage(st, st);
-    cp_async_commit();
-  }
-  for (int kb = 0; kb < KB; ++kb) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
-    {
-      const int nk = kb + kStages - 1;
-      if (nk < KB) load_stage(nk % kStages, nk);
-      cp_async_commit();
-    }
-    const int32_t *sx = reinterpret_cast<const int32_t *>(smem + (kb % kStages) * kStageWords);
-    const int32_t *sb = sx + kBK2 * kTile;
-#pragma unroll
-    for (int t = 0; t < kBK2; t += 2) {
-      int32_t x0[8], x1[8], b0[8], b1[8];
-      {
-        const int4 p = *reinterpret_cast<const int4 *>(sx + t * kTile + ty * 4);
-        const int4 q = *reinterpret_cast<const int4 *>(sx + t * kTile + 64 + ty * 4);
-        const int4 u = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + ty * 4);
-        const int4 v = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
-        x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
-        x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
-      }
-      {
-        const int4 p = *reinterpret_cast<const int4 *>(sb + t * kTile + tx * 4);
-        const int4 q = *reinterpret_cast<const int4 *>(sb + t * kTile + 64 + tx * 4);
-        const int4 u = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + tx * 4);
-        const int4 v = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
-        b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
-        b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < DPXC) {
-            acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
-            acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
-          } else {
-            const int32_t s0 = x0[r] * one + b0[c];
-            const int32_t s1 = x1[r] * one + b1[c];
-            acc[r][c] = __vimin3_s32(acc[r][c], s0, s1);
-          }
-        }
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
-    if (i >= M) continue;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int64_t j = j0 + (c >> 2) * 64 + tx * 4 + (c & 3);
-      if (j >= N) continue;
-      int32_t v = acc[r][c];
-      if (accumulate) v = min(v, min(C[i * ldc + j], kInf32));
-      C[i * ldc + j] = v;
-    }
-  }
-}
-
-template <int DPXC>
-int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
-                    int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st);
-
-template <int OUT, bool STATS, int DPXC, bool TMA = false>
-int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
-                  int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                  cudaStream_t st, int nsplit, const PeerB &pb, const TmaOps *tma = nullptr) {
-  static bool attr_set[64] = {};
-  int dev = 0;
-  RD_CUDA_CHECK(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC, TMA>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kSmemBytes + (TMA ? 1024 : 0))));
-    if (dev >= 0 && dev < 64) attr_set[dev] = true;
-  }
-  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
-  TmaOps t{};
-  if (tma) t = *tma;
-  minplus_gemm_kernel<OUT, STATS, DPXC, TMA><<<dim3((unsigned)(nti * ntj), (unsigned)nsplit), kThreads,
-                                              kSmemBytes + (TMA ? 1024 : 0), st>>>(
-      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb, t);
-  RD_CUDA_CHECK(cudaGetLastError());
-  return RD_OK;
-}
 
 template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
                 cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr) {
   const PeerB pb{};
+  if (OUT_PM && STATS && epi.sk_nsk > 0) {   // stream-K step (rd_set_stream_k)
+#define RD_LGS(D, T) launch_gemm_v<kOutPM, true, D, T, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, 1, pb, tma)
+#define RD_LGS2(D) return tma ? RD_LGS(D, true) : RD_LGS(D, false)
+    switch (g_dpx_cols) {
+      case 0: RD_LGS2(0);
+      case 2: RD_LGS2(2);
+      case 3: RD_LGS2(3);
+      case 4: RD_LGS2(4);
+      default: RD_LGS2(8);
+    }
+#undef RD_LGS2
+#undef RD_LGS
+  }
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
     switch (g_dpx_cols) {
@@ -852,24 +367,6 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
     default: return RD_LG(8);
   }
 #undef RD_LG
-}
-
-template <int DPXC>
-int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
-                    int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
-  static bool attr_set[64] = {};
-  int dev = 0;
-  RD_CUDA_CHECK(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm32_kernel<DPXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemBytes));
-    if (dev >= 0 && dev < 64) attr_set[dev] = true;
-  }
-  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
-  minplus_gemm32_kernel<DPXC><<<(unsigned)(nti * ntj), kThreads, kSmemBytes, st>>>(
-      XT, ldx, BP, ldb, (int)kp, C, ldc, M, N, nti, ntj, 1, accumulate, g_raster_group);
-  RD_CUDA_CHECK(cudaGetLastError());
-  return RD_OK;
 }
 
 int launch_gemm32(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
@@ -2644,6 +2141,15 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
+// rd_set_stream_k: 0 off, 1 (default) by the wave model, 2 whenever the last wave is partial
+static int g_stream_k = 1;
+
+extern "C" int rd_set_stream_k(int mode) try {
+  rd_enter();
+  if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_stream_k: mode must be 0, 1 or 2");
+  g_stream_k = mode;
+  return RD_OK;
+} RD_ABI_CATCH("rd_set_stream_k")
 // rd_set_gemm_tma: 0 = cp.async mainloop always; 1 (default) = TMA mainloop for single-pass
 // steps of >= 128 pipeline stages (measured: m = 9 274.2 vs 277.0 ms; with fewer stages per
 // CTA — split-K, m <= 8 — the single-thread issue costs 3-8 %); 2 = TMA always.
@@ -2868,32 +2374,75 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   // per SM; a CTA's pipeline fill and epilogue cost ~2 stages).  A split must promise >= 3%;
   // each keeps >= 2 stages.  Measured (tools/split_probe.py): m = 6 0.096 -> 0.053 ms, m = 8
   // 8-rank panel 1.97 -> 1.59 ms, m = 7 and full m = 8 / m = 9 panels within 1% of no split.
+  //
+  // Stream-K remainder (g_stream_k): the whole waves of tiles run as usual and the tiles of the
+  // last, partial wave are spread evenly over every CTA slot — each slot gets an equal range
+  // of their k-stages (crossing tile boundaries), writes partial tiles, and combine_sk_kernel
+  // folds them and computes their stats.  Its cost: the whole waves + ceil(R / nsk) stages +
+  // ~2 stages per segment + the combine's passes over the remainder tiles.  The model picks
+  // the cheapest of {plain, split-K, stream-K} (>= 3% better than plain).  A lone CTA on an SM
+  // (a partial wave of <= sms CTAs) runs ~1.35x faster than one of two, which the plain cost
+  // of a short last wave includes.
   const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
   const int64_t kstages = (c->P / 2) / kBK2;
-  int nsplit = 1;
+  int nsplit = 1, sk_nfull = 0, sk_nsk = 0;
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const int64_t slots = 2 * (int64_t)sms;
     const double t_stage = 8.2e-6, bw = 6.0e12, slot_bytes = 4.0 * (double)c->slot_words;
-    double best = 0.0, cost1 = 0.0;
-    for (int n = 1; n <= 8 && kstages >= 2 * n; ++n) {
+    const double tile_bytes = 4.0 * kTile * kTile / 2;
+    const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
+    const double lone = 0.74;
+    double cost1 = (double)full_waves * ((double)kstages + 2.0) +
+                   (rem == 0 ? 0.0 : (rem <= sms ? lone : 1.0) * ((double)kstages + 2.0));
+    double best = cost1;
+    for (int n = 2; n <= 8 && kstages >= 2 * n; ++n) {
       const double waves = (double)((ntiles * n + slots - 1) / slots);
       double cost = waves * ((double)kstages / n + 2.0);   // + pipeline fill / epilogue per CTA
-      if (n > 1) cost += (n + 2 + epi.nprev) * slot_bytes / bw / t_stage;
-      if (n == 1) cost1 = cost;
-      if (n == 1 || cost < best) { best = cost; nsplit = n; }
+      cost += (n + 2 + epi.nprev) * slot_bytes / bw / t_stage;
+      if (cost < best) { best = cost; nsplit = n; }
     }
-    if (best > 0.97 * cost1) nsplit = 1;
+    if (g_split_k_off) { nsplit = 1; best = cost1; }
+    if (g_stream_k && rem > 0) {
+      const int64_t R = rem * kstages;
+      const int nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, R / 4));   // >= 4 stages each
+      const double per = (double)((R + nsk - 1) / nsk);
+      const double segs = std::min(3.0, 1.0 + per / (double)kstages + 1.0);
+      double cost = (double)full_waves * ((double)kstages + 2.0) + per + 2.0 * segs;
+      cost += (double)rem * tile_bytes * (segs + 2 + epi.nprev) / bw / t_stage;
+      if (g_stream_k == 2 || cost < best) { best = cost; nsplit = 1; sk_nfull = (int)(full_waves * slots); sk_nsk = nsk; }
+    }
+    if (best > 0.97 * cost1 && g_stream_k != 2) { nsplit = 1; sk_nsk = 0; sk_nfull = 0; }
   }
-  if (g_split_k_off) nsplit = 1;
   const TmaOps *tma = nullptr;
   if (g_gemm_tma == 2 || (g_gemm_tma == 1 && nsplit == 1 && kstages >= 128)) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
     tma = &c->tma;
   }
-  if (nsplit == 1) {
+  if (sk_nsk > 0) {
+    const int64_t R = (ntiles - sk_nfull) * kstages;
+    const int64_t per_min = R / sk_nsk;
+    const int maxseg = (int)((kstages + per_min - 1) / std::max<int64_t>(1, per_min)) + 1;
+    if (!c->ws || c->nsplit < maxseg) {
+      chain_free(c, c->ws);
+      c->ws = nullptr;
+      RD_CUDA_CHECK(chain_malloc(c, &c->ws, (size_t)maxseg * c->slot_words * 4));
+      c->nsplit = maxseg;
+    }
+    epi.sk_nfull = sk_nfull;
+    epi.sk_nsk = sk_nsk;
+    epi.sk_ws = c->ws;
+    epi.sk_stride = c->slot_words;
+    int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
+                                     c->N, c->Mp, c->P, epi, c->st, 1, tma);
+    if (rc != RD_OK) return rc;
+    combine_sk_kernel<<<(unsigned)(ntiles - sk_nfull), 256, 0, c->st>>>(
+        c->ws, c->slot_words, c->slot(knew), c->Mp, (int)(c->Mp / kTile), (int)(c->P / kTile), g_raster_group,
+        (int)kstages, epi);
+    RD_CUDA_CHECK(cudaGetLastError());
+  } else if (nsplit == 1) {
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
                                      c->N, c->Mp, c->P, epi, c->st, 1, tma);
     if (rc != RD_OK) return rc;

@@ -1,0 +1,523 @@
+// Kernel templates of the (min,+) GEMM and their launchers; included only by the
+// instantiation units rd_gemm_*.cu (compiled in parallel).  See rd_gemm.cuh.
+#pragma once
+#include "rd_gemm.cuh"
+
+namespace rd {
+
+template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false>
+__global__ void __launch_bounds__(kThreads, 2)
+minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
+                    int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
+                    int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb,
+                    const __grid_constant__ TmaOps tma) {
+  extern __shared__ __align__(16) uint32_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  // TMA writes need an aligned destination: the TMA variant is launched with 1 KB extra
+  // dynamic shared memory and rounds its stage base up to 1 KB
+  uint32_t *smem = smem_raw;
+  if constexpr (TMA)
+    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 4u;
+  const int tid = threadIdx.x;
+  // a warp covers 4 (ty) x 8 (tx) threads of the 16 x 16 grid: its fragment loads touch 4 and 8
+  // distinct 16-byte chunks (one shared-memory wavefront each)
+  const int wq = tid >> 5, lq = tid & 31;
+  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
+  const int KBt = kpairs / kBK2;
+
+  // cp.async mapping: 512 16-byte chunks per operand tile (16 rows x 32 chunks)
+  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
+  const int64_t gx_step8 = 8 * ldx, gb_step8 = 8 * ldb;
+
+  uint32_t acc[8][8];
+  // TMA: thread 0 issues two bulk-tensor copies per stage (32 KB, completion counted on
+  // full_bar[s]); every warp releases a consumed stage on empty_bar[s]; thread 0 refills it
+  // once all 8 warps have.  No per-thread copy instructions, no CTA-wide barrier.  Stages are
+  // numbered by a running count `it` over the CTA's segments (stream-K CTAs run several), so
+  // slot = it mod kStages and the barrier phases continue across segments.
+  if constexpr (TMA) {
+    if (tid == 0) {
+#pragma unroll
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&full_bar[s], 1);
+        mbar_init(&empty_bar[s], kThreads / 32);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+
+  // acc = min over k-stages [kb0, kb0 + KB) of the tile at (i0, j0); it0 = stages this CTA
+  // consumed before (TMA slot / phase numbering)
+  auto mainloop = [&](int64_t i0, int64_t j0, int kb0, int KB, uint32_t it0) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
+    const uint32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
+    const uint32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
+    auto load_stage = [&](int stage, int kb) {
+      uint32_t *sx = smem + stage * kStageWords;
+      uint32_t *sb = sx + kBK2 * kTile;
+      const int64_t ox = (int64_t)kb * kBK2 * ldx;
+      const uint32_t *gbk;
+      if constexpr (OUT == kOutRP) {   // the rank holding k-pairs [kb * kBK2, +kBK2)
+        const int tk = kb * kBK2;
+        int s = 0;
+        while (s + 1 < pb.n && tk >= pb.t0[s + 1]) ++s;
+        gbk = pb.base[s] + (int64_t)(tk - pb.t0[s] + ld_row) * ldb + j0 + ld_col;
+      } else {
+        gbk = gb + (int64_t)kb * kBK2 * ldb;
+      }
+#pragma unroll
+      for (int r = 0; r < kBK2; r += 8) {
+        cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
+        cp_async16(sb + (ld_row + r) * kTile + ld_col, gbk + (r / 8) * gb_step8);
+      }
+    };
+    auto tma_issue = [&](int s, int kb) {
+      uint32_t *sx = smem + s * kStageWords;
+      mbar_expect_tx(&full_bar[s], (uint32_t)(kStageWords * 4));
+      tma_load_3d(sx, &tma.x, &full_bar[s], (int)i0, (kb0 + kb) * kBK2, tma.xslot);
+      tma_load_2d(sx + kBK2 * kTile, &tma.b, &full_bar[s], (int)j0, (kb0 + kb) * kBK2);
+    };
+    if constexpr (TMA) {
+      if (tid == 0)
+        for (int s = 0; s < kStages && s < KB; ++s) {
+          const uint32_t g = it0 + s;
+          if (g >= (uint32_t)kStages) mbar_wait(&empty_bar[g % kStages], ((g / kStages) - 1) & 1);
+          tma_issue(g % kStages, s);
+        }
+    } else {
+#pragma unroll
+      for (int s = 0; s < kStages - 1; ++s) {
+        if (s < KB) load_stage(s, kb0 + s);
+        cp_async_commit();
+      }
+    }
+
+    for (int kb = 0; kb < KB; ++kb) {
+      const uint32_t g = it0 + kb;
+      const int slot = TMA ? (int)(g % kStages) : kb % kStages;
+      if constexpr (TMA) {
+        mbar_wait(&full_bar[slot], (g / kStages) & 1);
+      } else {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        {
+          int nk = kb + kStages - 1;
+          if (nk < KB) load_stage(nk % kStages, kb0 + nk);
+          cp_async_commit();
+        }
+      }
+      const uint32_t *sx = smem + slot * kStageWords;
+      const uint32_t *sb = sx + kBK2 * kTile;
+      if (DPXC >= 8) {
+#pragma unroll
+        for (int t = 0; t < kBK2; ++t) {
+          const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
+          const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
+          const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
+          const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
+          const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+          const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < kBK2; t += 2) {
+          uint32_t x0[8], x1[8], b0[8], b1[8];
+          {
+            const uint4 p = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
+            const uint4 q = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
+            const uint4 u = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + ty * 4);
+            const uint4 v = *reinterpret_cast<const uint4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
+            x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
+            x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
+          }
+          {
+            const uint4 p = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
+            const uint4 q = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
+            const uint4 u = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + tx * 4);
+            const uint4 v = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
+            b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
+            b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
+          }
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              if (c < DPXC) {
+                acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+                acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+              } else {
+                const uint32_t s0 = x0[r] * one + b0[c];
+                const uint32_t s1 = x1[r] * one + b1[c];
+                acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
+              }
+            }
+        }
+      }
+      if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty_bar[slot]);
+        if (tid == 0 && kb + kStages < KB) {
+          mbar_wait(&empty_bar[slot], (g / kStages) & 1);
+          tma_issue(slot, kb + kStages);
+        }
+      }
+    }
+    if constexpr (!TMA) cp_async_wait<0>();
+  };
+
+  // ---------------------------------------------------------------- epilogue --
+  // v = min(lo, hi) per accumulator; pairs (c, c+1) packed (min_c | min_{c+1} << 16).
+  uint32_t out[8][4];
+  auto fold = [&]() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        uint32_t a0 = acc[r][2 * p], a1 = acc[r][2 * p + 1];
+        out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
+      }
+  };
+  // PM store of the folded tile at (i0, j0) into C (pitch ldc)
+  auto store_pm = [&](uint32_t *C, int64_t i0, int64_t j0) {
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        // column pair jp covers columns j0 + (p>>1)*64 + tx*4 + (p&1)*2 + {0,1}
+        int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+        uint4 v = make_uint4(out[g * 4 + 0][p], out[g * 4 + 1][p], out[g * 4 + 2][p], out[g * 4 + 3][p]);
+        *reinterpret_cast<uint4 *>(C + jp * ldc + i0 + g * 64 + ty * 4) = v;
+      }
+  };
+
+  int64_t i0, j0;
+  if constexpr (SK && OUT == kOutPM) {
+    if ((int)blockIdx.x >= epi.sk_nfull) {
+      // stream-K CTA: its share of the remainder's k-stage iterations, one partial tile per
+      // segment (a segment = the part of the range inside one tile)
+      const int c = (int)blockIdx.x - epi.sk_nfull;
+      const int64_t R = (int64_t)(nti * ntj - epi.sk_nfull) * KBt;
+      const int64_t e0 = sk_begin(c, R, epi.sk_nsk), e1 = sk_begin(c + 1, R, epi.sk_nsk);
+      uint32_t it = 0;
+      for (int64_t e = e0; e < e1;) {
+        const int r = (int)(e / KBt);
+        const int kb0 = (int)(e - (int64_t)r * KBt);
+        const int KB = (int)((e1 - e) < (int64_t)(KBt - kb0) ? (e1 - e) : (int64_t)(KBt - kb0));
+        const int seg = c - sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
+        tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);
+        if (it > 0 && !TMA) __syncthreads();   // every warp is done with the previous segment's stages
+        mainloop(i0, j0, kb0, KB, it);
+        fold();
+        store_pm(epi.sk_ws + (int64_t)seg * epi.sk_stride, i0, j0);
+        it += (uint32_t)KB;
+        e += KB;
+      }
+      return;
+    }
+  }
+  // classic CTA: one whole tile (or, split-K, the k-range blockIdx.y of gridDim.y)
+  tile_origin((int)blockIdx.x, nti, ntj, kgroup, i0, j0);
+  {
+    const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
+    const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
+    mainloop(i0, j0, kb0, KB, 0);
+  }
+  fold();
+
+  // RP word (rows 2q', 2q'+1 of row group g; columns h*64 + tx*4 + e) from the folded pairs
+  auto rp_word = [&](int g, int q, int h, int e) -> uint32_t {
+    const uint32_t a = out[g * 4 + 2 * q][2 * h + (e >> 1)], b = out[g * 4 + 2 * q + 1][2 * h + (e >> 1)];
+    return prmt(a, b, (e & 1) ? 0x7632 : 0x5410);
+  };
+  if constexpr (OUT == kOutRP) {
+    uint32_t *C = reinterpret_cast<uint32_t *>(Cv);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
+          const uint4 v = make_uint4(rp_word(g, q, h, 0), rp_word(g, q, h, 1), rp_word(g, q, h, 2), rp_word(g, q, h, 3));
+          *reinterpret_cast<uint4 *>(C + pr * ldc + j0 + h * 64 + tx * 4) = v;
+        }
+  } else if constexpr (OUT == kOutPM) {
+    store_pm(reinterpret_cast<uint32_t *>(Cv) + (int64_t)blockIdx.y * epi.split_stride, i0, j0);
+  } else {
+    int16_t *C = reinterpret_cast<int16_t *>(Cv);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+      if (i >= M) continue;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2;
+        int v0 = (int)(out[r][p] & 0xFFFF), v1 = (int)(out[r][p] >> 16);
+        if (epi.accumulate) {
+          if (j < N) v0 = min(v0, min((int)C[i * ldc + j], (int)RD_INF));
+          if (j + 1 < N) v1 = min(v1, min((int)C[i * ldc + j + 1], (int)RD_INF));
+        }
+        if (j < N) C[i * ldc + j] = (int16_t)v0;
+        if (j + 1 < N) C[i * ldc + j + 1] = (int16_t)v1;
+      }
+    }
+  }
+
+  if (!STATS) return;
+
+  // ---- fused reductions over this tile (MIN-reducible; see rd.h rd_chain_step) ----
+  __shared__ int32_t red[kThreads / 32][1 + 4 * kMaxAlpha];
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // diagonal min (Cor 7): global row diag_row0 + i == column j
+  int32_t dmin = INT_MAX;
+  {
+    const int64_t gi0 = epi.diag_row0 + i0;
+    if (gi0 < j0 + kTile && j0 < gi0 + kTile) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int64_t gi = gi0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+            int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2 + h;
+            int32_t v = (int32_t)((out[r][p] >> (16 * h)) & 0xFFFF);
+            if (gi == j && v < dmin) dmin = v;
+          }
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+
+  // periodicity stats against A^{k+1-a}: same PM address in the previous slots
+  for (int a = 0; a < epi.nprev; ++a) {
+    const uint32_t *P = epi.prev[a];
+    uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
+    if constexpr (OUT == kOutRP) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t pr = ((i0 + g * 64 + ty * 4) >> 1) + q;
+            const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + pr * ldc + j0 + h * 64 + tx * 4));
+            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) stats_pair(rp_word(g, q, h, e), pw[e], lo2, hi2, mis, fin);
+          }
+    } else {
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+          uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
+          const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
+        }
+    }
+    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
+    if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
+    int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
+    int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
+    int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
+    int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
+    if (lane == 0) {
+      red[warp][1 + 4 * a + 0] = v0;
+      red[warp][1 + 4 * a + 1] = v1;
+      red[warp][1 + 4 * a + 2] = v2;
+      red[warp][1 + 4 * a + 3] = v3;
+    }
+  }
+  __syncthreads();
+  const int nval = 1 + 4 * epi.nprev;
+  for (int e = tid; e < nval; e += kThreads) {
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) v = min(v, red[w][e]);
+    atomicMin(epi.stats + e, v);
+  }
+}
+
+// ----------------------------------------------------------- 32-bit GEMM --
+// The generic product for entries beyond the int16 headroom (the
+// `__viaddmin_s32` variant; rd.h rd_minplus_mul32).  Same CTA tile, thread tile, cp.async
+// pipeline and rasterisation as minplus_gemm_kernel, one int32 per k instead of a k-pair:
+//   XT[k][i] = X[i][k]  (left operand transposed, [Kp][Mp]),  BP[k][j] = B[k][j]  ([Kp][Np]),
+// both INF32-padded to the tile, entries clamped to [., RD_INF32] on packing.  Per k a thread
+// reads 4 x LDS.128 and updates 64 accumulators: columns c < DPXC with one VIADDMNMX (32-bit,
+// alu), the others two k at a time with two IMAD adds (fma; exact: sums <= 0x7FFFFFFE) and one
+// VIMNMX3 (alu).  RD_INF32 + anything >= RD_INF32, and accumulators start at RD_INF32, so
+// infinite results come out exactly RD_INF32 (finite sums >= RD_INF32 saturate to it).
+
+template <int DPXC>
+__global__ void __launch_bounds__(kThreads, 2)
+minplus_gemm32_kernel(const int32_t *__restrict__ XT, int64_t ldx, const int32_t *__restrict__ BP, int64_t ldb,
+                      int kp, int32_t *__restrict__ C, int64_t ldc, int64_t M, int64_t N, int nti, int ntj,
+                      int32_t one, int accumulate, int kgroup) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int tid = threadIdx.x;
+  const int wq = tid >> 5, lq = tid & 31;
+  const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
+  int64_t i0, j0;
+  {
+    const int bid = blockIdx.x;
+    const int per_group = kgroup * ntj;
+    const int g = bid / per_group, first = g * kgroup;
+    const int gsz = min(nti - first, kgroup);
+    const int w = bid - g * per_group;
+    i0 = (int64_t)(first + w % gsz) * kTile;
+    j0 = (int64_t)(w / gsz) * kTile;
+  }
+  const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
+  const int32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
+  const int32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
+  auto load_stage = [&](int stage, int kb) {
+    uint32_t *sx = smem + stage * kStageWords;
+    uint32_t *sb = sx + kBK2 * kTile;
+    const int64_t ox = (int64_t)kb * kBK2 * ldx, ob = (int64_t)kb * kBK2 * ldb;
+#pragma unroll
+    for (int r = 0; r < kBK2; r += 8) {
+      cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * 8 * ldx);
+      cp_async16(sb + (ld_row + r) * kTile + ld_col, gb + ob + (r / 8) * 8 * ldb);
+    }
+  };
+  int32_t acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = kInf32;
+  const int KB = kp / kBK2;
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (st < KB) load_stage(st, st);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < KB; ++kb) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + kStages - 1;
+      if (nk < KB) load_stage(nk % kStages, nk);
+      cp_async_commit();
+    }
+    const int32_t *sx = reinterpret_cast<const int32_t *>(smem + (kb % kStages) * kStageWords);
+    const int32_t *sb = sx + kBK2 * kTile;
+#pragma unroll
+    for (int t = 0; t < kBK2; t += 2) {
+      int32_t x0[8], x1[8], b0[8], b1[8];
+      {
+        const int4 p = *reinterpret_cast<const int4 *>(sx + t * kTile + ty * 4);
+        const int4 q = *reinterpret_cast<const int4 *>(sx + t * kTile + 64 + ty * 4);
+        const int4 u = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + ty * 4);
+        const int4 v = *reinterpret_cast<const int4 *>(sx + (t + 1) * kTile + 64 + ty * 4);
+        x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
+        x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
+      }
+      {
+        const int4 p = *reinterpret_cast<const int4 *>(sb + t * kTile + tx * 4);
+        const int4 q = *reinterpret_cast<const int4 *>(sb + t * kTile + 64 + tx * 4);
+        const int4 u = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + tx * 4);
+        const int4 v = *reinterpret_cast<const int4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
+        b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
+        b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < DPXC) {
+            acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
+            acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
+          } else {
+            const int32_t s0 = x0[r] * one + b0[c];
+            const int32_t s1 = x1[r] * one + b1[c];
+            acc[r][c] = __vimin3_s32(acc[r][c], s0, s1);
+          }
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
+    if (i >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int64_t j = j0 + (c >> 2) * 64 + tx * 4 + (c & 3);
+      if (j >= N) continue;
+      int32_t v = acc[r][c];
+      if (accumulate) v = min(v, min(C[i * ldc + j], kInf32));
+      C[i * ldc + j] = v;
+    }
+  }
+}
+
+template <int OUT, bool STATS, int DPXC, bool TMA, bool SK>
+int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
+                  int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
+                  cudaStream_t st, int nsplit, const PeerB &pb, const TmaOps *tma) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kSmemBytes + (TMA ? 1024 : 0))));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
+  TmaOps t{};
+  if (tma) t = *tma;
+  // stream-K steps: sk_nfull whole-tile CTAs, then sk_nsk CTAs sharing the remaining tiles
+  const unsigned gx = SK ? (unsigned)(epi.sk_nfull + epi.sk_nsk) : (unsigned)(nti * ntj);
+  minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK><<<dim3(gx, (unsigned)nsplit), kThreads,
+                                              kSmemBytes + (TMA ? 1024 : 0), st>>>(
+      XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb, t);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+template <int DPXC>
+int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm32_kernel<DPXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemBytes));
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
+  minplus_gemm32_kernel<DPXC><<<(unsigned)(nti * ntj), kThreads, kSmemBytes, st>>>(
+      XT, ldx, BP, ldb, (int)kp, C, ldc, M, N, nti, ntj, 1, accumulate, g_raster_group);
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
+
+}  // namespace rd
+
+// Explicit instantiation of one launcher: RD_INST_GEMM(OUT, STATS, DPXC, TMA)
+#define RD_INST_GEMM(OUT, STATS, D, TMA, ...)                                                              \
+  template int rd::launch_gemm_v<OUT, STATS, D, TMA, ##__VA_ARGS__>(const uint32_t *, int64_t, const uint32_t *, int64_t,  \
+                                                     int64_t, void *, int64_t, int64_t, int64_t, int64_t,  \
+                                                     int64_t, const rd::EpiArgs &, cudaStream_t, int,      \
+                                                     const rd::PeerB &, const rd::TmaOps *);
+#define RD_INST_GEMM_ALL(OUT, STATS, TMA, ...)                                                               \
+  RD_INST_GEMM(OUT, STATS, 0, TMA, ##__VA_ARGS__) RD_INST_GEMM(OUT, STATS, 2, TMA, ##__VA_ARGS__)             \
+  RD_INST_GEMM(OUT, STATS, 3, TMA, ##__VA_ARGS__) RD_INST_GEMM(OUT, STATS, 4, TMA, ##__VA_ARGS__)             \
+  RD_INST_GEMM(OUT, STATS, 8, TMA, ##__VA_ARGS__)

@@ -1,0 +1,6 @@
+// Explicit instances of the (min,+) GEMM launchers (rd_gemm_kernels.cuh); one unit per
+// group so that the build compiles them in parallel.
+#include "rd_gemm_kernels.cuh"
+
+RD_INST_GEMM_ALL(rd::kOutRow, false, false)
+RD_INST_GEMM_ALL(rd::kOutRP, true, false)

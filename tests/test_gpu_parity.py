@@ -478,6 +478,7 @@ def test_chain_from_packed_operand_equals_built_chain():
 @pytest.mark.parametrize("m,r0,r1", [(6, 0, 848), (7, 0, 2507), (8, 0, 1024), (8, 3712, 4736)])
 def test_split_k_equals_single_pass(m, r0, r1):
     outs = []
+    rd.rd_set_stream_k(0)
     for on in (True, False):
         rd.rd_set_split_k(on)
         try:
@@ -487,9 +488,42 @@ def test_split_k_equals_single_pass(m, r0, r1):
             ch.close()
         finally:
             rd.rd_set_split_k(True)
+            rd.rd_set_stream_k(1)
     for a, b in zip(outs[0][0], outs[1][0]):
         assert (a == b).all()
     assert (outs[0][1] == outs[1][1]).all()
+
+
+@pytest.mark.parametrize("m,r0,r1", [(3, 0, 33), (5, 0, 287), (6, 0, 848), (7, 0, 2507), (7, 128, 1000),
+                                     (8, 3712, 4736)])
+def test_stream_k_equals_oracle_and_single_pass(m, r0, r1):
+    """Stream-K remainder (rd_set_stream_k(2): forced whenever the last wave is partial): every
+    power and every stats vector equal the plain one-tile-per-CTA step, and the powers equal the
+    oracle's on the full matrix for m <= 7."""
+    outs = []
+    rd.rd_set_split_k(False)
+    try:
+        for mode in (2, 0):
+            rd.rd_set_stream_k(mode)
+            ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+            st, rows = [], {}
+            for k in range(2, 13):
+                st.append(ch.step().cpu().numpy())
+                if k in (2, 5, 12):
+                    rows[k] = ch.read_rows(k)
+            outs.append((st, rows))
+            ch.close()
+    finally:
+        rd.rd_set_stream_k(1)
+        rd.rd_set_split_k(True)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert (a == b).all()
+    for k in outs[0][1]:
+        assert (outs[0][1][k] == outs[1][1][k]).all(), k
+    if m <= 7:
+        P = {k: X for k, X in O.powers(m, 12) if k in (2, 5, 12)}
+        for k, X in P.items():
+            assert (outs[0][1][k] == to_inf(X[r0:r1], OINF, RINF, np.int16)).all(), k
 
 
 
