@@ -371,6 +371,13 @@ int rd_set_split_k(int enable);
  * 2 = whenever the last wave is partial (tests).  Identical results.  RD_EINVAL outside 0..2. */
 int rd_set_stream_k(int mode);
 
+/* rd_set_small_chain — process-wide switch (default 1): the dense Algorithm 2 of orders with
+ * N <= 1024 (m <= 6; rd_power_sequence*, rd_power_sequence_matrix, method 0) runs as ONE
+ * device-resident cooperative kernel — product tiles, fused diag/periodicity stats, a grid
+ * barrier and the decision per power on the device — instead of one host round trip per
+ * power (DESIGN.md §5 "Small orders").  0 = the host-driven chain.  Identical results. */
+int rd_set_small_chain(int enable);
+
 /* rd_set_sparse_bytes — process-wide choice of the structured step's kernel for chains
  * created afterwards over column-uniform labels:
  *   2 (default) slab layout: columns of the powers stored in in-degree order, one warp lane

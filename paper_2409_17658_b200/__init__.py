@@ -86,6 +86,8 @@ def lib():
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_stream_k.argtypes = [ci]
+        L.rd_set_small_chain.argtypes = [ci]
+        L.rd_set_small_chain.restype = ci
         L.rd_set_stream_k.restype = ci
         L.rd_set_gemm_tma.argtypes = [ci]
         L.rd_set_gemm_tma.restype = ci
@@ -342,6 +344,11 @@ def rd_set_split_k(enable: bool):
 def rd_set_stream_k(mode: int):
     """Stream-K remainder of dense chain steps (rd.h): 0 off, 1 model (default), 2 forced."""
     _check(lib().rd_set_stream_k(int(mode)))
+
+
+def rd_set_small_chain(enable: bool):
+    """Small orders' dense Algorithm 2 as one device-resident kernel (rd.h; default on)."""
+    _check(lib().rd_set_small_chain(1 if enable else 0))
 
 
 def rd_set_sparse_bytes(mode):

@@ -416,9 +416,10 @@ extern "C" int rd_set_device(int device) try {
 
 // =========================================================== generic product ==
 // Library-owned stream-ordered pool (one per device; chains and the generic products' workspace).
+namespace rd {
 constexpr uint64_t kPoolKeep = (uint64_t)16 << 30;
 constexpr size_t kPoolMax = (size_t)kPoolKeep;
-static cudaMemPool_t chain_pool(int dev) {
+cudaMemPool_t chain_pool(int dev) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
@@ -442,7 +443,7 @@ static cudaMemPool_t chain_pool(int dev) {
 // Stream-ordered workspace from the library's pool (the device's default pool and its release
 // threshold are left alone: other cudaMallocAsync users in the process keep their setting);
 // falls back to cudaMallocAsync on the default pool if the library pool cannot be created.
-static cudaError_t ws_malloc(void **p, size_t bytes, cudaStream_t st) {
+cudaError_t ws_malloc(void **p, size_t bytes, cudaStream_t st) {
   *p = nullptr;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -454,6 +455,7 @@ static cudaError_t ws_malloc(void **p, size_t bytes, cudaStream_t st) {
   }
   return cudaMallocAsync(p, bytes, st);
 }
+}  // namespace rd
 
 static int minplus_rowmajor(const int16_t *A, int64_t lda, const int16_t *B, int64_t ldb, int16_t *C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, void *cuda_stream, int accumulate,
@@ -2143,6 +2145,14 @@ static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
 // rd_set_stream_k: 0 off, 1 (default) by the wave model, 2 whenever the last wave is partial
 static int g_stream_k = 1;
+// rd_set_small_chain: dense Algorithm 2 of orders N <= kSmallMaxN as one device-resident kernel
+static int g_small_chain = 1;
+
+extern "C" int rd_set_small_chain(int enable) try {
+  rd_enter();
+  g_small_chain = enable ? 1 : 0;
+  return RD_OK;
+} RD_ABI_CATCH("rd_set_small_chain")
 
 extern "C" int rd_set_stream_k(int mode) try {
   rd_enter();
@@ -2754,6 +2764,18 @@ extern "C" int rd_power_sequence_timed(int m, int kmax, int alpha_max, int polic
   if (m < 1 || m > 11) return fail(RD_EINVAL, "rd_power_sequence: m=%d out of range", m);
   if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, 2 * m, out, diag)) return rc0;
   const int64_t N = count_words(m);
+  if (method == 0 && g_small_chain && N <= kSmallMaxN) {
+    // small orders: the whole chain as one device-resident kernel (rd_small.cu)
+    std::vector<int16_t> A((size_t)(N * N));
+    if (int rc0 = build_matrix(m, A.data(), N)) return rc0;
+    double tb = 0.0, tc = 0.0;
+    const int rc = small_power_sequence(A.data(), N, kmax, alpha_max, policy, out, diag, &tb, &tc);
+    if (seconds) {
+      seconds[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - tc;
+      seconds[1] = tc;
+    }
+    return rc;
+  }
   cudaStream_t st;
   RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   rd_chain *c = nullptr;
@@ -2780,6 +2802,11 @@ extern "C" int rd_power_sequence_matrix(const int16_t *A, int64_t N, int kmax, i
   int32_t mx = 0;
   if (int rc0 = check_matrix(A, N, &mx, "rd_power_sequence_matrix")) return rc0;
   if (int rc0 = power_sequence_check(kmax, alpha_max, policy, method, mx, out, diag)) return rc0;
+  if (method == 0 && g_small_chain && N <= kSmallMaxN) {
+    std::vector<int16_t> Ac(A, A + N * N);
+    for (auto &x : Ac) x = std::min<int16_t>(x, RD_INF);
+    return small_power_sequence(Ac.data(), N, kmax, alpha_max, policy, out, diag, nullptr, nullptr);
+  }
   cudaStream_t st;
   RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   rd_chain *c = nullptr;

@@ -175,6 +175,16 @@ struct PeerB {
 };
 
 
+// Stream-ordered device workspace from the library's pool (rd_cuda.cu).
+cudaMemPool_t chain_pool(int dev);
+cudaError_t ws_malloc(void **p, size_t bytes, cudaStream_t st);
+
+// Small orders (rd_small.cu): Algorithm 2 as one device-resident cooperative kernel for the
+// host matrix A (N x N int16, entries in [0, RD_INF]); times in seconds (nullable).
+constexpr int kSmallMaxN = 1024;
+int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_max, int policy, rd_period_t *out,
+                         int32_t *diag, double *t_build, double *t_chain);
+
 // Launchers of the GEMM instances (defined in rd_gemm_kernels.cuh, instantiated in rd_gemm_*.cu).
 template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,

@@ -997,3 +997,46 @@ def test_roman_cylinder_ex_dense_equals_structured_and_formulas(m):
     with pytest.raises(rd.RDError) as e:
         rd.rd_roman_cylinder(m, 5, method=2)
     assert e.value.status == rd.RD_EINVAL
+
+
+# ------------------------------------------- small orders: device-resident chain --
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6])
+def test_small_chain_kernel_equals_host_chain_and_oracle(m):
+    """The device-resident Algorithm 2 (rd_set_small_chain(1), one cooperative kernel with the
+    decision on the device) equals the host-driven chain and the oracle: triple,
+    k_stop and every diag, under both search policies (R6), several alpha_max, and a
+    kmax too small to detect (RD_NOTFOUND)."""
+    for policy in (0, 1):
+        for am in (5, 10):
+            ref = O.power_chain(m, 50, am, policy)
+            got = {}
+            for small in (True, False):
+                rd.rd_set_small_chain(small)
+                try:
+                    got[small] = rd.rd_power_sequence(m, 50, am, policy)
+                finally:
+                    rd.rd_set_small_chain(True)
+            for g in got.values():
+                assert (g["found"], g["n0"], g["alpha"], g["beta"], g["k_stop"]) == (
+                    ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"]), (m, policy, am)
+                assert g["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+    kmax = 6
+    ref = O.power_chain(m, kmax, 10, 0)
+    g = rd.rd_power_sequence(m, kmax, 10, 0)
+    assert g["found"] == ref["found"] and g["k_stop"] == ref["k_stop"]
+    assert g["diag"][1:kmax + 1] == ref["diag"][1:kmax + 1]
+    if not ref["found"]:
+        assert g["status"] == rd.RD_NOTFOUND
+
+
+@pytest.mark.parametrize("N,seed", [(1, 1), (7, 2), (64, 3), (65, 4), (500, 5), (1024, 6)])
+def test_small_chain_kernel_generic_matrices(N, seed):
+    """Caller matrices up to N = 1024 through the device-resident chain (rd_power_sequence_matrix,
+    method 0) equal the oracle's Algorithm 2 on the same matrix, including tile-ragged N."""
+    A16 = sparse_like(N, 6, seed=seed)
+    A32 = to_inf(A16, RINF, OINF, np.int32)
+    ref = O.power_chain_matrix(A32, 30, 6, 0)
+    got = rd.rd_power_sequence_matrix(A16, 30, 6, 0, 0)
+    assert (got["found"], got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (
+        ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"])
+    assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
