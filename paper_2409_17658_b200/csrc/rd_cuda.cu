@@ -540,81 +540,82 @@ struct PanelStatsArgs {
   int nprev;
 };
 
-// One pass handles alphas [a0, a0 + 8): warp w of a block owns alpha a0 + w (warps beyond
-// the pass's alphas only read), lane l a 16-byte column chunk; a block sweeps (row,
-// 256-column block) items, so the current power's segment is read once from HBM and
-// re-served from L1 to the block's eight warps.  Per lane the state is one alpha's packed
-// (lo, hi, mis, fin): few registers, many loads in flight.
+// Single pass over every alpha in [a0, a0 + NA): a thread holds one 16-byte chunk of the
+// current power (8 entries) in registers, loads the same chunk of each earlier power once and
+// folds it into that alpha's packed (lo, -hi, mis, fin) registers; the block reduces at the
+// end.  HBM bytes (1 + nprev) * 2 * rows * cols, each read exactly once.
+template <int NA>
 __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
                                                           int64_t cols, int64_t ld, int64_t diag_row0,
                                                           PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
-  __shared__ int32_t red[8][1 + 4 * 8];
+  __shared__ int32_t red[8][1 + 4 * NA];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int na = min(8, pa.nprev - a0);
-  const bool mine = warp < na;
-  const int16_t *P = mine ? pa.prev[a0 + warp] : cur;
+  const int na = min(NA, pa.nprev - a0);
   int32_t dmin = INT_MAX;
-  uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
-  const bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(P) & 15) == 0);
-  const int64_t nb = (cols + 255) / 256;
-  const int64_t items = rows * nb;
-  for (int64_t v = blockIdx.x; v < items; v += gridDim.x) {
-    const int64_t i = v / nb, j = (v - i * nb) * 256 + lane * 8;
-    if (j >= cols) continue;
-    const int64_t off = i * ld + j;
-    uint32_t o[4], w[4];
+  uint32_t lo2[NA], hi2[NA], mis[NA], fin[NA];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
+  for (int a = 0; a < na; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a0 + a]) & 15) == 0);
+  const int64_t cpr = (cols + 7) / 8, total = rows * cpr;
+  auto load8 = [&](const int16_t *base, int64_t off, int64_t j, uint32_t (&w)[4]) {
     if (vec && j + 8 <= cols) {
-      const uint4 x = *reinterpret_cast<const uint4 *>(cur + off);
-      o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
-      if (mine) {
-        const uint4 y = *reinterpret_cast<const uint4 *>(P + off);
-        w[0] = y.x; w[1] = y.y; w[2] = y.z; w[3] = y.w;
-      }
+      const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(base + off));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool in0 = j + 2 * q < cols, in1 = j + 2 * q + 1 < cols;
-        o[q] = (in0 ? (uint16_t)cur[off + 2 * q] : (uint16_t)RD_INF) |
-               ((uint32_t)(in1 ? (uint16_t)cur[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
-        if (mine)
-          w[q] = (in0 ? (uint16_t)P[off + 2 * q] : (uint16_t)RD_INF) |
-                 ((uint32_t)(in1 ? (uint16_t)P[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
+        w[q] = (in0 ? (uint16_t)base[off + 2 * q] : (uint16_t)RD_INF) |
+               ((uint32_t)(in1 ? (uint16_t)base[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q], kInf2);
-    if (a0 == 0 && warp == 0) {
+    for (int q = 0; q < 4; ++q) w[q] = __vminu2(w[q], kInf2);   // entries above RD_INF read as +inf
+  };
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = v / cpr, j = (v - i * cpr) * 8;
+    const int64_t off = i * ld + j;
+    uint32_t o[4];
+    load8(cur, off, j, o);
+    if (a0 == 0) {   // diagonal (Cor 7): global row diag_row0 + i meets column j .. j + 7
       const int64_t gi = diag_row0 + i;
       if (gi >= j && gi < j + 8) {
         const int t = (int)(gi - j);
         dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
       }
     }
-    if (mine) {
+    uint32_t w[NA][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q], kInf2), lo2, hi2, mis, fin);
-    }
+    for (int a = 0; a < NA; ++a)
+      if (a < na) load8(pa.prev[a0 + a], off, j, w[a]);
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+      if (a < na) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) stats_pair(o[q], w[a][q], lo2[a], hi2[a], mis[a], fin[a]);
+      }
   }
   dmin = __reduce_min_sync(0xffffffffu, dmin);
-  {
-    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
-    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
-    if (!fin) { lo = INT_MAX; hi = INT_MIN + 1; }
-    const int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
-    const int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
-    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
-    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
+  if (lane == 0) red[warp][0] = dmin;
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    if (a >= na) break;
+    int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
+    if (!(fin[a] & 0xFFFF) && !(fin[a] >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
+    const int32_t v0 = __reduce_min_sync(0xffffffffu, lo), v1 = __reduce_min_sync(0xffffffffu, -hi);
+    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis[a] ? -1 : 0);
+    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin[a] ? -1 : 0);
     if (lane == 0) {
-      if (warp == 0) red[0][0] = dmin;
-      if (mine) {
-        red[0][1 + 4 * warp] = v0; red[0][2 + 4 * warp] = v1; red[0][3 + 4 * warp] = v2; red[0][4 + 4 * warp] = v3;
-      }
+      red[warp][1 + 4 * a] = v0; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
     }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 1 + 4 * na; e += blockDim.x) {
-    const int32_t v = red[0][e];
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w2 = 1; w2 < 8; ++w2) v = min(v, red[w2][e]);
     if (e == 0) {
       if (a0 == 0) atomicMin(stats, v);
     } else {
@@ -644,11 +645,17 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // blocks sweep (row, 256-column block) items; 8 resident blocks per SM
-  const int64_t items = rows * ((cols + 255) / 256);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * 8));
-  for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 8) {
-    panel_stats_kernel<<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+  // one thread per 16-byte chunk of the panel, grid-strided; every alpha of a pass in one sweep
+  const int64_t chunks = rows * ((cols + 7) / 8);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms * 4));
+  for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 16) {
+    const int na = nprev - a0;
+    if (na <= 4)
+      panel_stats_kernel<4><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    else if (na <= 8)
+      panel_stats_kernel<8><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    else
+      panel_stats_kernel<16><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
     RD_CUDA_CHECK(cudaGetLastError());
   }
   return RD_OK;

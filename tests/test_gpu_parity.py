@@ -297,6 +297,53 @@ def test_panel_stats_against_oracle_shift():
     assert s2[3] == -1 and s2[4] == -1          # mismatch seen, finite pairs seen
 
 
+def _stats_reference(X, prevs, diag_row0):
+    """The MIN-reducible stats vector (rd.h rd_chain_step) of X against prevs, by definition."""
+    X = X.astype(np.int64)
+    s = [2**31 - 1]
+    d = [X[i, diag_row0 + i] for i in range(X.shape[0]) if 0 <= diag_row0 + i < X.shape[1]]
+    if d:
+        s[0] = int(min(d))
+    for P in prevs:
+        P = P.astype(np.int64)
+        fx, fp = X < RINF, P < RINF
+        both = fx & fp
+        if both.any():
+            diff = X[both] - P[both]
+            s += [int(diff.min()), -int(diff.max())]
+        else:
+            s += [2**31 - 1, 2**31 - 1]
+        s += [-1 if (fx != fp).any() else 0, -1 if both.any() else 0]
+    return np.array(s, dtype=np.int64)
+
+
+@pytest.mark.parametrize("rows,cols,ld,nprev", [(300, 287, 287, 20), (64, 1000, 1008, 10), (5, 13, 13, 3),
+                                                (257, 2048, 2048, 16), (33, 100, 100, 0)])
+def test_panel_stats_one_pass_every_entry(rows, cols, ld, nprev):
+    """rd_panel_stats (one pass over every alpha, 16 per pass; vector and ragged scalar paths)
+    equals the stats vector's definition entry by entry, with inf entries in both powers."""
+    rng = np.random.default_rng(rows + cols + nprev)
+    am = max(1, nprev)
+    base = rng.integers(50, 90, size=(rows, ld)).astype(np.int16)
+    X = base.copy()
+    X[rng.random((rows, ld)) < 0.01] = RINF
+    prevs = []
+    for a in range(nprev):
+        Pa = (base - (a % 3 == 0) * (2 * a)).astype(np.int16)     # some alphas uniform, some not
+        if a % 4 == 1:
+            Pa = Pa + rng.integers(0, 2, size=Pa.shape).astype(np.int16)
+        Pa[rng.random((rows, ld)) < (0.0 if a % 2 else 0.01)] = RINF
+        if a % 5 == 0:
+            Pa[X == RINF] = RINF                                    # identical inf pattern
+        prevs.append(Pa)
+    dX = _gpu(X)
+    s = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device="cuda")
+    view = lambda T: T.view(-1)[: (rows - 1) * ld + cols].as_strided((rows, cols), (ld, 1))
+    got = rd.rd_panel_stats(view(dX), [view(_gpu(P)) for P in prevs], 7, am, s).cpu().numpy().astype(np.int64)
+    want = _stats_reference(X[:, :cols], [P[:, :cols] for P in prevs], 7)
+    assert (got[:len(want)] == want).all(), (got[:len(want)], want)
+
+
 @pytest.mark.parametrize("m", [3, 5, 7])
 def test_power_sequence_allgather_single_rank(m):
     from paper_2409_17658_b200 import dist as rdist

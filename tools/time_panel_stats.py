@@ -22,4 +22,4 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
 by = 11 * 2 * N * N
-print(f"panel_stats N={N} alpha=10: {ms:.3f} ms per call (2 passes), {by / ms / 1e6:.1f} GB/s algorithmic")
+print(f"panel_stats N={N} alpha=10: {ms:.3f} ms per call (one pass), {by / ms / 1e6:.1f} GB/s algorithmic")
