@@ -363,12 +363,14 @@ int rd_set_gemm_tma(int mode);
  * Identical results.  Always RD_OK. */
 int rd_set_split_k(int enable);
 
-/* rd_set_stream_k — process-wide choice (default 1) for dense chain steps whose last wave of
+/* rd_set_stream_k — process-wide choice for dense chain steps whose last wave of
  * tiles is partial (DESIGN.md §5 "Wave quantisation"): the whole waves run one tile per CTA
  * and the remaining tiles' k-stages are split evenly over every CTA slot (contiguous ranges
  * that cross tile boundaries, "stream-K"); a combine kernel folds the partial tiles, stores
- * them and computes their stats.  mode 0 = never, 1 = when the wave model predicts >= 3%,
- * 2 = whenever the last wave is partial (tests).  Identical results.  RD_EINVAL outside 0..2. */
+ * them and computes their stats.  mode 0 (default) = never, 1 = when the wave model predicts
+ * >= 3%, 2 = whenever the last wave is partial (tests).  Identical results.  Measured slower
+ * than the plain / split-K steps on every shape tried, hence off by default.
+ * RD_EINVAL outside 0..2. */
 int rd_set_stream_k(int mode);
 
 /* rd_set_small_chain — process-wide switch (default 1): the dense Algorithm 2 of orders with

@@ -544,19 +544,23 @@ struct PanelStatsArgs {
 // current power (8 entries) in registers, loads the same chunk of each earlier power once and
 // folds it into that alpha's packed (lo, -hi, mis, fin) registers; the block reduces at the
 // end.  HBM bytes (1 + nprev) * 2 * rows * cols, each read exactly once.
+// NA = the number of alphas of this pass exactly (0: diagonal only), so every load is
+// unconditional and all 1 + NA chunks of a thread are in flight together.
 template <int NA>
 __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restrict__ cur, int64_t rows,
                                                           int64_t cols, int64_t ld, int64_t diag_row0,
                                                           PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
-  __shared__ int32_t red[8][1 + 4 * NA];
+  constexpr int NR = NA > 0 ? NA : 1;
+  __shared__ int32_t red[8][1 + 4 * NR];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int na = min(NA, pa.nprev - a0);
+  constexpr int na = NA;
   int32_t dmin = INT_MAX;
-  uint32_t lo2[NA], hi2[NA], mis[NA], fin[NA];
+  uint32_t lo2[NR], hi2[NR], mis[NR], fin[NR];
 #pragma unroll
-  for (int a = 0; a < NA; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  for (int a = 0; a < NR; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
   bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
-  for (int a = 0; a < na; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a0 + a]) & 15) == 0);
+#pragma unroll
+  for (int a = 0; a < NA; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a0 + a]) & 15) == 0);
   const int64_t cpr = (cols + 7) / 8, total = rows * cpr;
   auto load8 = [&](const int16_t *base, int64_t off, int64_t j, uint32_t (&w)[4]) {
     if (vec && j + 8 <= cols) {
@@ -585,22 +589,18 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
         dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
       }
     }
-    uint32_t w[NA][4];
+    uint32_t w[NR][4];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) load8(pa.prev[a0 + a], off, j, w[a]);
 #pragma unroll
     for (int a = 0; a < NA; ++a)
-      if (a < na) load8(pa.prev[a0 + a], off, j, w[a]);
 #pragma unroll
-    for (int a = 0; a < NA; ++a)
-      if (a < na) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) stats_pair(o[q], w[a][q], lo2[a], hi2[a], mis[a], fin[a]);
-      }
+      for (int q = 0; q < 4; ++q) stats_pair(o[q], w[a][q], lo2[a], hi2[a], mis[a], fin[a]);
   }
   dmin = __reduce_min_sync(0xffffffffu, dmin);
   if (lane == 0) red[warp][0] = dmin;
 #pragma unroll
   for (int a = 0; a < NA; ++a) {
-    if (a >= na) break;
     int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
     int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
     if (!(fin[a] & 0xFFFF) && !(fin[a] >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
@@ -649,13 +649,14 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   const int64_t chunks = rows * ((cols + 7) / 8);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms * 4));
   for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 16) {
-    const int na = nprev - a0;
-    if (na <= 4)
-      panel_stats_kernel<4><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
-    else if (na <= 8)
-      panel_stats_kernel<8><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
-    else
-      panel_stats_kernel<16><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev);
+    const int na = std::min(16, nprev - a0);
+    switch (na) {
+#define RD_PS(K) \
+  case K: panel_stats_kernel<K><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev); break;
+      RD_PS(0) RD_PS(1) RD_PS(2) RD_PS(3) RD_PS(4) RD_PS(5) RD_PS(6) RD_PS(7) RD_PS(8)
+      RD_PS(9) RD_PS(10) RD_PS(11) RD_PS(12) RD_PS(13) RD_PS(14) RD_PS(15) RD_PS(16)
+#undef RD_PS
+    }
     RD_CUDA_CHECK(cudaGetLastError());
   }
   return RD_OK;
@@ -2150,8 +2151,8 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
-// rd_set_stream_k: 0 off, 1 (default) by the wave model, 2 whenever the last wave is partial
-static int g_stream_k = 1;
+// rd_set_stream_k: 0 (default) off, 1 by the wave model, 2 whenever the last wave is partial
+static int g_stream_k = 0;
 // rd_set_small_chain: dense Algorithm 2 of orders N <= kSmallMaxN as one device-resident kernel
 static int g_small_chain = 1;
 

@@ -86,7 +86,7 @@ __device__ __forceinline__ bool decide(const int32_t *s, int alpha_max, int k, i
   return false;
 }
 
-__global__ void __launch_bounds__(kSThreads) small_chain_kernel(SmallArgs sa) {
+__global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa) {
   __shared__ __align__(16) uint32_t sX[2][kST][kSKC];   // [row][k-pair]
   __shared__ __align__(16) uint32_t sB[2][kSKC][kST];   // [k-pair][column]
   __shared__ int32_t red[kSThreads / 32][1 + 4 * kMaxAlpha];
@@ -99,35 +99,44 @@ __global__ void __launch_bounds__(kSThreads) small_chain_kernel(SmallArgs sa) {
   auto slot = [&](int k) { return sa.ring + (int64_t)(k % (am + 1)) * slot_elems; };
 
   // ---- prologue: pack A, A^1 into its slot, INF elsewhere, neutral stats for every power
+  // (sizes fit 32-bit indices: P <= 1024, (alpha_max + 1) P^2 <= 34.6e6)
   {
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + tid;
-    for (int64_t e = t0; e < P2 * P; e += nth) {
-      const int64_t t = e / P, j = e - t * P;
+    const int nth = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + tid;
+    const int n = (int)N, p = (int)P, p2 = (int)P2, se = (int)slot_elems;
+    for (int e = t0; e < p2 * p; e += nth) {
+      const int t = e / p, j = e - t * p;
       uint32_t lo = RD_INF, hi = RD_INF;
-      if (j < N) {
-        if (2 * t < N) lo = (uint32_t)min((int)sa.A[2 * t * N + j], (int)RD_INF);
-        if (2 * t + 1 < N) hi = (uint32_t)min((int)sa.A[(2 * t + 1) * N + j], (int)RD_INF);
+      if (j < n) {
+        if (2 * t < n) lo = (uint32_t)min((int)sa.A[2 * t * n + j], (int)RD_INF);
+        if (2 * t + 1 < n) hi = (uint32_t)min((int)sa.A[(2 * t + 1) * n + j], (int)RD_INF);
       }
       sa.BP[e] = lo | (hi << 16);
     }
-    for (int64_t e = t0; e < (int64_t)(am + 1) * slot_elems; e += nth) {
-      const int64_t s = e / slot_elems, r = e - s * slot_elems, i = r / P, j = r - i * P;
-      int16_t v = RD_INF;
-      if (s == 1 % (am + 1) && i < N && j < N) v = (int16_t)min((int)sa.A[i * N + j], (int)RD_INF);
-      sa.ring[e] = v;
+    const int s1 = 1 % (am + 1);
+    uint32_t *ring32 = reinterpret_cast<uint32_t *>(sa.ring);
+    for (int e = t0; e < (am + 1) * se / 2; e += nth) {
+      const int s = (2 * e) / se, r = 2 * e - s * se, i = r / p, j = r - i * p;   // j even
+      uint32_t v = kInf2;
+      if (s == s1 && i < n) {
+        const uint32_t lo = j < n ? (uint32_t)min((int)sa.A[i * n + j], (int)RD_INF) : RD_INF;
+        const uint32_t hi = j + 1 < n ? (uint32_t)min((int)sa.A[i * n + j + 1], (int)RD_INF) : RD_INF;
+        v = lo | (hi << 16);
+      }
+      ring32[e] = v;
     }
-    for (int64_t e = t0; e < (int64_t)(sa.kmax + 1) * slen; e += nth) {
-      const int q = (int)(e % slen);
+    for (int e = t0; e < (sa.kmax + 1) * slen; e += nth) {
+      const int q = e % slen;
       sa.stats[e] = (q == 0 || (q - 1) % 4 < 2) ? INT_MAX : 0;
     }
-    if (blockIdx.x == 0 && tid == 0) {
-      sa.result[0] = 0; sa.result[1] = 0; sa.result[2] = 0; sa.result[3] = 0; sa.result[4] = 0;
+    if (blockIdx.x == 0 && warp == 0) {
+      if (tid == 0) { sa.result[0] = 0; sa.result[1] = 0; sa.result[2] = 0; sa.result[3] = 0; sa.result[4] = 0; }
       int32_t d1 = INT_MAX;
-      for (int64_t p = 0; p < N; ++p) {
-        const int v = sa.A[p * N + p];
+      for (int q = lane; q < n; q += 32) {
+        const int v = sa.A[q * n + q];
         if (v < RD_INF) d1 = min(d1, v);
       }
-      sa.result[5] = d1;
+      d1 = __reduce_min_sync(0xffffffffu, d1);
+      if (lane == 0) sa.result[5] = d1;
     }
   }
   grid_barrier(sa.bar, gen);
@@ -206,26 +215,45 @@ __global__ void __launch_bounds__(kSThreads) small_chain_kernel(SmallArgs sa) {
           const uint32_t a0 = acc[r][2 * p], a1 = acc[r][2 * p + 1];
           out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
         }
+      // the tile goes to its ring slot and, as words, to shared memory (the chunk buffers are
+      // free after the k loop's last barrier) for the periodicity stats below
+      uint32_t(*sC)[kST / 2] = reinterpret_cast<uint32_t(*)[kST / 2]>(&sX[0][0][0]);
       int32_t dmin = INT_MAX;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int64_t i = i0 + ty * 4 + r, j = j0 + tx * 4;
         *reinterpret_cast<uint2 *>(C + i * P + j) = make_uint2(out[r][0], out[r][1]);
+        *reinterpret_cast<uint2 *>(&sC[ty * 4 + r][tx * 2]) = make_uint2(out[r][0], out[r][1]);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           if (i == j + c) dmin = min(dmin, (int)((out[r][c >> 1] >> (16 * (c & 1))) & 0xFFFF));
       }
       dmin = __reduce_min_sync(0xffffffffu, dmin);
       if (lane == 0) red[warp][0] = dmin;
-      for (int a = 1; a <= nprev; ++a) {
+      __syncthreads();
+      // periodicity stats: warp w takes alpha = 1 + w, 1 + w + 8, ...; a lane compares 16
+      // 16-byte chunks of the tile (from shared memory) with the same chunks of A^{k-alpha},
+      // all 16 loads in flight at once
+      for (int a = 1 + warp; a <= nprev; a += kSThreads / 32) {
         const int16_t *Pv = slot(k - a);
         uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int64_t i = i0 + ty * 4 + r, j = j0 + tx * 4;
-          const uint2 pv = __ldcg(reinterpret_cast<const uint2 *>(Pv + i * P + j));
-          stats_pair(out[r][0], pv.x, lo2, hi2, mis, fin);
-          stats_pair(out[r][1], pv.y, lo2, hi2, mis, fin);
+        for (int h = 0; h < 2; ++h) {
+          uint4 pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = lane + 32 * (8 * h + u), row = q >> 3, c8 = q & 7;
+            pv[u] = __ldcg(reinterpret_cast<const uint4 *>(Pv + (i0 + row) * P + j0 + c8 * 8));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = lane + 32 * (8 * h + u), row = q >> 3, c8 = q & 7;
+            const uint4 cv = *reinterpret_cast<const uint4 *>(&sC[row][c8 * 4]);
+            stats_pair(cv.x, pv[u].x, lo2, hi2, mis, fin);
+            stats_pair(cv.y, pv[u].y, lo2, hi2, mis, fin);
+            stats_pair(cv.z, pv[u].z, lo2, hi2, mis, fin);
+            stats_pair(cv.w, pv[u].w, lo2, hi2, mis, fin);
+          }
         }
         int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
         int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
@@ -234,15 +262,15 @@ __global__ void __launch_bounds__(kSThreads) small_chain_kernel(SmallArgs sa) {
         const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
         const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
         if (lane == 0) {
-          red[warp][4 * a - 3] = v0; red[warp][4 * a - 2] = v1; red[warp][4 * a - 1] = v2; red[warp][4 * a] = v3;
+          atomicMin(st + 4 * a - 3, v0); atomicMin(st + 4 * a - 2, v1);
+          atomicMin(st + 4 * a - 1, v2); atomicMin(st + 4 * a, v3);
         }
       }
-      __syncthreads();
-      for (int e = tid; e < 1 + 4 * nprev; e += kSThreads) {
-        int32_t v = red[0][e];
+      if (tid == 0) {
+        int32_t v = red[0][0];
 #pragma unroll
-        for (int w = 1; w < kSThreads / 32; ++w) v = min(v, red[w][e]);
-        atomicMin(st + e, v);
+        for (int w = 1; w < kSThreads / 32; ++w) v = min(v, red[w][0]);
+        atomicMin(st, v);
       }
       __syncthreads();
     }

@@ -535,7 +535,7 @@ def test_split_k_equals_single_pass(m, r0, r1):
             ch.close()
         finally:
             rd.rd_set_split_k(True)
-            rd.rd_set_stream_k(1)
+            rd.rd_set_stream_k(0)
     for a, b in zip(outs[0][0], outs[1][0]):
         assert (a == b).all()
     assert (outs[0][1] == outs[1][1]).all()
@@ -561,7 +561,7 @@ def test_stream_k_equals_oracle_and_single_pass(m, r0, r1):
             outs.append((st, rows))
             ch.close()
     finally:
-        rd.rd_set_stream_k(1)
+        rd.rd_set_stream_k(0)
         rd.rd_set_split_k(True)
     for a, b in zip(outs[0][0], outs[1][0]):
         assert (a == b).all()
