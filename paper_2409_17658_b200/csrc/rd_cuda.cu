@@ -558,30 +558,43 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
   uint32_t lo2[NR], hi2[NR], mis[NR], fin[NR];
 #pragma unroll
   for (int a = 0; a < NR; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  // the earlier powers' base pointers in registers (not re-read from the parameter block)
+  const int16_t *pp[NR];
   bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
 #pragma unroll
-  for (int a = 0; a < NA; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a0 + a]) & 15) == 0);
+  for (int a = 0; a < NA; ++a) {
+    pp[a] = pa.prev[a0 + a];
+    vec = vec && ((reinterpret_cast<uintptr_t>(pp[a]) & 15) == 0);
+  }
   const int64_t cpr = (cols + 7) / 8, total = rows * cpr;
-  auto load8 = [&](const int16_t *base, int64_t off, int64_t j, uint32_t (&w)[4]) {
-    if (vec && j + 8 <= cols) {
-      const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(base + off));
-      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-    } else {
+  auto scalar8 = [&](const int16_t *base, int64_t off, int64_t j, uint32_t (&w)[4]) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool in0 = j + 2 * q < cols, in1 = j + 2 * q + 1 < cols;
-        w[q] = (in0 ? (uint16_t)base[off + 2 * q] : (uint16_t)RD_INF) |
-               ((uint32_t)(in1 ? (uint16_t)base[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
-      }
+    for (int q = 0; q < 4; ++q) {
+      const bool in0 = j + 2 * q < cols, in1 = j + 2 * q + 1 < cols;
+      w[q] = (in0 ? (uint16_t)base[off + 2 * q] : (uint16_t)RD_INF) |
+             ((uint32_t)(in1 ? (uint16_t)base[off + 2 * q + 1] : (uint16_t)RD_INF) << 16);
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w[q] = __vminu2(w[q], kInf2);   // entries above RD_INF read as +inf
   };
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = v / cpr, j = (v - i * cpr) * 8;
     const int64_t off = i * ld + j;
-    uint32_t o[4];
-    load8(cur, off, j, o);
+    uint32_t o[4], w[NR][4];
+    if (vec && j + 8 <= cols) {
+      // fast path: all 1 + NA 16-byte loads issued before any is used
+      const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(cur + off));
+      uint4 y[NR];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) y[a] = __ldcs(reinterpret_cast<const uint4 *>(pp[a] + off));
+      o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) { w[a][0] = y[a].x; w[a][1] = y[a].y; w[a][2] = y[a].z; w[a][3] = y[a].w; }
+    } else {
+      scalar8(cur, off, j, o);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) scalar8(pp[a], off, j, w[a]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q], kInf2);   // entries above RD_INF read as +inf
     if (a0 == 0) {   // diagonal (Cor 7): global row diag_row0 + i meets column j .. j + 7
       const int64_t gi = diag_row0 + i;
       if (gi >= j && gi < j + 8) {
@@ -589,13 +602,10 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
         dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
       }
     }
-    uint32_t w[NR][4];
-#pragma unroll
-    for (int a = 0; a < NA; ++a) load8(pa.prev[a0 + a], off, j, w[a]);
 #pragma unroll
     for (int a = 0; a < NA; ++a)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) stats_pair(o[q], w[a][q], lo2[a], hi2[a], mis[a], fin[a]);
+      for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[a][q], kInf2), lo2[a], hi2[a], mis[a], fin[a]);
   }
   dmin = __reduce_min_sync(0xffffffffu, dmin);
   if (lane == 0) red[warp][0] = dmin;

@@ -388,52 +388,90 @@ def power_sequence_peer(m: int, kmax: int = 50, alpha_max: int = 10, policy: int
     return dec.result(t_build=t1 - t0, t_chain=t2 - t1)
 
 
-# ----------------------------------------------------- panel-sequential (one GPU) --
+# ------------------------------------------- panel-sequential (one GPU or several ranks) --
 def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int | None = None, method: int = 1,
-                          policy: int = 0, progress=None, early_stop: bool = True):
+                          policy: int = 0, progress=None, early_stop: bool = True, group=None,
+                          chain_factory=None):
     """Algorithm 2 for orders whose ring of powers does not fit one GPU (m = 11: 73 GB per
     int16 power).  Rows of A^{k+1} depend only on the same rows of A^k, so the chain
     runs panel by panel, each panel's per-power stats vector is kept, and the decision (first
     k with a uniform alpha, Alg 2 step 4) is taken on the MIN-combined stats afterwards — the
     same decision the row-panel driver takes across ranks.
 
-    early_stop: the first panel runs to its own first detection plus a margin (4 powers, or
-    alpha_max under policy 1) and the other panels to the same power; combining panels can only
-    delay a detection (MIN of the stats never creates uniformity), so if the combined decision
-    is not reached there, everything is recomputed to kmax.  Returns the dict of
-    power_sequence plus per-panel timings."""
+    Under torch.distributed (group), rank r runs panels r, r + world, ... of the same split;
+    the per-power stats arrays are MIN-reduced over the ranks (one all_reduce of
+    (kend - 1) x (1 + 4 alpha_max) int32 at the end) before the shared decision.
+
+    early_stop: each rank's first panel runs to its own first detection plus a margin (4
+    powers, or alpha_max under policy 1); the ranks agree on the largest such power (MAX
+    all_reduce) and every panel runs to it.  Combining panels can only delay a detection (MIN
+    of the stats never creates uniformity), so if the combined decision is not reached there,
+    everything is recomputed to kmax.  Returns the dict of power_sequence plus per-panel
+    timings (this rank's panels).
+
+    chain_factory(m, alpha_max, r0, r1) -> object with step() (stats tensor), diag1, close()
+    (default: paper_2409_17658_b200.Chain with `method`; CPU tests pass an oracle panel)."""
     import time
 
     import torch
+    import torch.distributed as dist
 
-    from . import Chain, RD_INF, count_words, rd_stats_decide
+    from . import count_words, rd_stats_decide
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
     N = count_words(m)
     if panel_rows is None:
         panel_rows = N
     panel_rows = max(TILE, (panel_rows + TILE - 1) // TILE * TILE)
     bounds = [(r0, min(N, r0 + panel_rows)) for r0 in range(0, N, panel_rows)]
+    mine = bounds[rank::world]
     margin = alpha_max if policy == 1 else 4
+    on_gpu = chain_factory is None and torch.cuda.is_available()
+    device = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    if chain_factory is None:
+        from . import Chain
 
-    def run(r0, r1, kstop, stop_on_detect):
+        def chain_factory(m_, am_, a_, b_):
+            return Chain(m_, alpha_max=am_, row_begin=a_, row_end=b_, method=method)
+
+    def sync():
+        if on_gpu:
+            torch.cuda.synchronize()
+
+    def start(r0, r1):
         t0 = time.perf_counter()
-        ch = Chain(m, alpha_max=alpha_max, row_begin=r0, row_end=r1, method=method)
-        torch.cuda.synchronize()
-        tb = time.perf_counter() - t0
-        rows, k_end, seen = [], kstop, False
-        for k in range(2, kstop + 1):
-            rows.append(ch.step().clone())
-            if stop_on_detect and not seen and rd_stats_decide(rows[-1].cpu().numpy(), alpha_max, k):
-                seen, k_end = True, min(kstop, k + margin)
-            if k >= k_end:
-                break
-        st = torch.stack(rows).cpu().numpy()
-        d1 = ch.diag1
-        ch.close()
-        t = {"rows": [r0, r1], "k_end": k_end, "build_s": round(tb, 3),
-             "chain_s": round(time.perf_counter() - t0 - tb, 3)}
+        ch = chain_factory(m, alpha_max, r0, r1)
+        sync()
+        return {"ch": ch, "rows": [], "k": 1, "r": (r0, r1), "t0": t0, "tb": time.perf_counter() - t0}
+
+    def advance(pn, k_to, stop_on_detect):
+        seen = False
+        while pn["k"] < k_to:
+            k = pn["k"] + 1
+            pn["rows"].append(pn["ch"].step().clone())
+            pn["k"] = k
+            if stop_on_detect and not seen and rd_stats_decide(pn["rows"][-1].cpu().numpy(), alpha_max, k):
+                seen, k_to = True, min(k_to, k + margin)
+        return pn["k"]
+
+    def finish(pn, timings):
+        st = torch.stack(pn["rows"]).cpu().numpy()
+        d1 = pn["ch"].diag1
+        pn["ch"].close()
+        sync()
+        t = {"rows": list(pn["r"]), "k_end": pn["k"], "build_s": round(pn["tb"], 3),
+             "chain_s": round(time.perf_counter() - pn["t0"] - pn["tb"], 3)}
+        timings.append(t)
         if progress:
             progress(t)
-        return st, d1, t
+        return st, d1
+
+    def allreduce(x, op):
+        if world == 1:
+            return x
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).to(device)
+        dist.all_reduce(t, op=op, group=group)
+        return t.cpu().numpy()
 
     def decide(combined, kend, diag1):
         dec = Decider(alpha_max, policy, kmax, diag1)
@@ -442,17 +480,23 @@ def power_sequence_panels(m: int, kmax: int, alpha_max: int = 5, panel_rows: int
                 break
         return dec
 
+    slen = 1 + 4 * alpha_max
     for attempt in (0, 1):
-        timings, combined, diag1 = [], None, 2**31 - 1
-        kend = kmax
-        for idx, (r0, r1) in enumerate(bounds):
-            st, d1, t = run(r0, r1, kend, early_stop and attempt == 0 and idx == 0)
-            if idx == 0:
-                kend = t["k_end"]
-            timings.append(t)
-            diag1 = min(diag1, d1)
-            combined = st if combined is None else np.minimum(combined, st[:combined.shape[0]])
-        dec = decide(combined, kend, diag1)
+        timings, diag1 = [], 2**31 - 1
+        stop = early_stop and attempt == 0
+        first = start(*mine[0]) if mine else None
+        k_local = advance(first, kmax, stop) if first else 0
+        kend = int(allreduce(np.array([k_local]), dist.ReduceOp.MAX if world > 1 else None)[0])
+        combined = np.tile(neutral_stats(alpha_max).astype(np.int64), (kend - 1, 1))
+        for idx, (r0, r1) in enumerate(mine):
+            pn = first if idx == 0 else start(r0, r1)
+            advance(pn, kend, False)
+            st, d1 = finish(pn, timings)
+            diag1 = min(diag1, int(d1))
+            combined = np.minimum(combined, st[:kend - 1].astype(np.int64))
+        combined = allreduce(combined.reshape(-1), dist.ReduceOp.MIN if world > 1 else None).reshape(kend - 1, slen)
+        diag1 = int(allreduce(np.array([diag1]), dist.ReduceOp.MIN if world > 1 else None)[0])
+        dec = decide(combined.astype(np.int32), kend, diag1)
         if dec.complete or kend >= kmax:
             break
     return dec.result(panels=timings)

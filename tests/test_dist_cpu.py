@@ -53,6 +53,11 @@ class OraclePanel:
         self.k = k
         return torch.from_numpy(s)
 
+    @property
+    def diag1(self):
+        d = [int(self.A[i, i]) for i in range(self.r0, self.r1) if self.A[i, i] != OINF]
+        return min(d) if d else 2**31 - 1
+
     def close(self):
         pass
 
@@ -303,3 +308,40 @@ def test_gloo_peer_allgather_chain(world, m):
         assert (res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (ref["n0"], ref["alpha"], ref["beta"],
                                                                          ref["k_stop"])
         assert res["diag"][1:res["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+# --------------------------------------------- panel-sequential driver over ranks --
+def _panels_worker(rank, world, port, m, panel_rows, policy, alpha_max, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = rdist.power_sequence_panels(m, 40, alpha_max, panel_rows=panel_rows, policy=policy,
+                                          chain_factory=lambda m_, am_, a, b: OraclePanel(m_, am_, a, b))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,rows,policy", [(2, 5, 128, 0), (3, 5, 128, 1), (2, 4, 128, 0)])
+def test_gloo_panels_over_ranks_equals_single_process(world, m, rows, policy):
+    """power_sequence_panels across ranks (rank r runs panels r, r + world, ...; stats arrays
+    MIN-reduced; one shared decision) equals the oracle's Algorithm 2, also when a rank holds
+    no panel (m = 4: one 128-row panel for 2 ranks) and under the paper-compatible policy."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    am = 5
+    ps = [ctx.Process(target=_panels_worker, args=(r, world, port, m, rows, policy, am, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = O.power_chain(m, 40, am, policy)
+    for r in range(world):
+        res = out[r]
+        assert (res["found"], res["n0"], res["alpha"], res["beta"], res["k_stop"]) == (
+            ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"]), (r, res["k_stop"])
+        assert res["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
