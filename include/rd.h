@@ -349,6 +349,12 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 
+/* rd_set_gemm_tile — process-wide tile width of the dense chain step's GEMM when it runs the
+ * cp.async mainloop (DESIGN.md §5 "Wave quantisation"): 128 (128 x 128 tiles, 8 x 8 per thread,
+ * 2 CTAs/SM) or 64 (128 x 64 tiles, 8 x 4 per thread, 3 CTAs/SM: twice the tiles, a finer last
+ * wave).  Identical results.  RD_EINVAL otherwise. */
+int rd_set_gemm_tile(int tn);
+
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
  * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
  * counted on an mbarrier; the warps release stages on a second mbarrier); without, every

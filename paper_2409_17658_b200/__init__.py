@@ -86,6 +86,8 @@ def lib():
         L.rd_set_sparse_variant.argtypes = [ci]
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_stream_k.argtypes = [ci]
+        L.rd_set_gemm_tile.argtypes = [ci]
+        L.rd_set_gemm_tile.restype = ci
         L.rd_set_small_chain.argtypes = [ci]
         L.rd_set_small_chain.restype = ci
         L.rd_set_stream_k.restype = ci
@@ -344,6 +346,11 @@ def rd_set_split_k(enable: bool):
 def rd_set_stream_k(mode: int):
     """Stream-K remainder of dense chain steps (rd.h): 0 off, 1 model (default), 2 forced."""
     _check(lib().rd_set_stream_k(int(mode)))
+
+
+def rd_set_gemm_tile(tn: int):
+    """Tile width of cp.async dense chain steps (rd.h): 128 (default) or 64."""
+    _check(lib().rd_set_gemm_tile(int(tn)))
 
 
 def rd_set_small_chain(enable: bool):

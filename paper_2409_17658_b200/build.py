@@ -15,7 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CUDA_UNITS = ["rd_cuda.cu", "rd_gemm_pm_stats.cu", "rd_gemm_pm_stats_tma.cu", "rd_gemm_pm_part.cu",
-              "rd_gemm_row_rp.cu", "rd_gemm32.cu", "rd_gemm_pm_sk.cu", "rd_small.cu"]
+              "rd_gemm_row_rp.cu", "rd_gemm32.cu", "rd_gemm_pm_sk.cu", "rd_small.cu",
+              "rd_gemm_pm64.cu"]
 SOURCES = ["rd_host.cpp"] + CUDA_UNITS
 HEADERS = ["rd_internal.h", "rd_gemm.cuh", "rd_gemm_kernels.cuh", os.path.join(INCLUDE, "rd.h")]
 

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restr
 }
 
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
+int g_gemm_tile = 128;    // rd_set_gemm_tile: tile width of chain steps without TMA (128 or 64)
 int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
 
 __global__ void pack_t32_kernel(const int32_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
@@ -358,6 +359,17 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
     }
 #undef RD_LGT
   }
+  if (OUT_PM && g_gemm_tile == 64) {   // 128 x 64 tiles, 3 CTAs per SM (rd_set_gemm_tile)
+#define RD_LG64(D) launch_gemm_v<kOutPM, STATS, D, false, false, 64>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
+    switch (g_dpx_cols) {
+      case 0: return RD_LG64(0);
+      case 2: return RD_LG64(2);
+      case 3: return RD_LG64(3);
+      case 4: return RD_LG64(4);
+      default: return RD_LG64(8);
+    }
+#undef RD_LG64
+  }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
   switch (g_dpx_cols) {
     case 0: return RD_LG(0);
@@ -407,6 +419,13 @@ extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   g_dpx_cols = dpx_cols;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")
+
+extern "C" int rd_set_gemm_tile(int tn) try {
+  rd_enter();
+  if (tn != 64 && tn != 128) return fail(RD_EINVAL, "rd_set_gemm_tile: tile width must be 64 or 128");
+  g_gemm_tile = tn;
+  return RD_OK;
+} RD_ABI_CATCH("rd_set_gemm_tile")
 
 extern "C" int rd_set_device(int device) try {
   rd_enter();

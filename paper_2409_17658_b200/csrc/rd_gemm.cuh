@@ -186,7 +186,7 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
                          int32_t *diag, double *t_build, double *t_chain);
 
 // Launchers of the GEMM instances (defined in rd_gemm_kernels.cuh, instantiated in rd_gemm_*.cu).
-template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false>
+template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false, int TN = 128>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
                   cudaStream_t st, int nsplit, const PeerB &pb, const TmaOps *tma = nullptr);

@@ -5,8 +5,12 @@
 
 namespace rd {
 
-template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false>
-__global__ void __launch_bounds__(kThreads, 2)
+// TN = tile width (columns of C): 128 (thread tile 8 x 8, 2 CTAs/SM) or 64 (8 x 4, 3 CTAs/SM,
+// twice the tiles for the same work: finer wave quantisation).  Accumulator (r, c) of a
+// thread uses the DPX form when (r * NC + c) mod 8 < DPXC (TN = 128: c < DPXC), so both widths
+// keep the DPXC / 8 instruction mix.
+template <int OUT, bool STATS, int DPXC, bool TMA = false, bool SK = false, int TN = 128>
+__global__ void __launch_bounds__(kThreads, TN == 128 ? 2 : 3)
 minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t *__restrict__ BP,
                     int64_t ldb, int kpairs, void *__restrict__ Cv, int64_t ldc, int64_t M, int64_t N,
                     int nti, int ntj, uint32_t one, EpiArgs epi, int kgroup, PeerB pb,
@@ -24,12 +28,18 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   const int wq = tid >> 5, lq = tid & 31;
   const int ty = 4 * (wq >> 1) + (lq >> 3), tx = 8 * (wq & 1) + (lq & 7);
   const int KBt = kpairs / kBK2;
+  constexpr int NC = TN / 16;                   // accumulator columns per thread (8 or 4)
+  constexpr int SW = kBK2 * (kTile + TN);       // u32 per pipeline stage (left + right tile)
+  static_assert(TN == 128 || (TN == 64 && OUT == kOutPM && !TMA && !SK), "TN = 64: PM output, cp.async");
 
-  // cp.async mapping: 512 16-byte chunks per operand tile (16 rows x 32 chunks)
+  // cp.async mapping: the left tile is 32 k-pair rows x 32 chunks of 16 B (8 rows per pass),
+  // the right tile 32 rows x TN / 4 chunks (1024 / TN rows per pass)
   const int ld_row = tid >> 5, ld_col = (tid & 31) * 4;
-  const int64_t gx_step8 = 8 * ldx, gb_step8 = 8 * ldb;
+  constexpr int BCH = TN / 4, BRP = kThreads / BCH;
+  const int ldb_row = tid / BCH, ldb_col = (tid % BCH) * 4;
+  const int64_t gx_step8 = 8 * ldx;
 
-  uint32_t acc[8][8];
+  uint32_t acc[8][NC];
   // TMA: thread 0 issues two bulk-tensor copies per stage (32 KB, completion counted on
   // full_bar[s]); every warp releases a consumed stage on empty_bar[s]; thread 0 refills it
   // once all 8 warps have.  No per-thread copy instructions, no CTA-wide barrier.  Stages are
@@ -53,11 +63,11 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[r][c] = kInf2;
+      for (int c = 0; c < NC; ++c) acc[r][c] = kInf2;
     const uint32_t *gx = XT + (int64_t)ld_row * ldx + i0 + ld_col;
-    const uint32_t *gb = BP + (int64_t)ld_row * ldb + j0 + ld_col;
+    const uint32_t *gb = BP + (int64_t)ldb_row * ldb + j0 + ldb_col;
     auto load_stage = [&](int stage, int kb) {
-      uint32_t *sx = smem + stage * kStageWords;
+      uint32_t *sx = smem + stage * SW;
       uint32_t *sb = sx + kBK2 * kTile;
       const int64_t ox = (int64_t)kb * kBK2 * ldx;
       const uint32_t *gbk;
@@ -65,19 +75,18 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
         const int tk = kb * kBK2;
         int s = 0;
         while (s + 1 < pb.n && tk >= pb.t0[s + 1]) ++s;
-        gbk = pb.base[s] + (int64_t)(tk - pb.t0[s] + ld_row) * ldb + j0 + ld_col;
+        gbk = pb.base[s] + (int64_t)(tk - pb.t0[s] + ldb_row) * ldb + j0 + ldb_col;
       } else {
         gbk = gb + (int64_t)kb * kBK2 * ldb;
       }
 #pragma unroll
-      for (int r = 0; r < kBK2; r += 8) {
-        cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
-        cp_async16(sb + (ld_row + r) * kTile + ld_col, gbk + (r / 8) * gb_step8);
-      }
+      for (int r = 0; r < kBK2; r += 8) cp_async16(sx + (ld_row + r) * kTile + ld_col, gx + ox + (r / 8) * gx_step8);
+#pragma unroll
+      for (int r = 0; r < kBK2; r += BRP) cp_async16(sb + (ldb_row + r) * TN + ldb_col, gbk + (int64_t)r * ldb);
     };
     auto tma_issue = [&](int s, int kb) {
-      uint32_t *sx = smem + s * kStageWords;
-      mbar_expect_tx(&full_bar[s], (uint32_t)(kStageWords * 4));
+      uint32_t *sx = smem + s * SW;
+      mbar_expect_tx(&full_bar[s], (uint32_t)(SW * 4));
       tma_load_3d(sx, &tma.x, &full_bar[s], (int)i0, (kb0 + kb) * kBK2, tma.xslot);
       tma_load_2d(sx + kBK2 * kTile, &tma.b, &full_bar[s], (int)j0, (kb0 + kb) * kBK2);
     };
@@ -110,26 +119,29 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           cp_async_commit();
         }
       }
-      const uint32_t *sx = smem + slot * kStageWords;
+      const uint32_t *sx = smem + slot * SW;
       const uint32_t *sb = sx + kBK2 * kTile;
       if (DPXC >= 8) {
 #pragma unroll
         for (int t = 0; t < kBK2; ++t) {
           const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
           const uint4 xb = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
-          const uint4 ba = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
-          const uint4 bb = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
           const uint32_t x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-          const uint32_t b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+          uint32_t b[NC];
+#pragma unroll
+          for (int h = 0; h < NC / 4; ++h) {
+            const uint4 bv = *reinterpret_cast<const uint4 *>(sb + t * TN + h * 64 + tx * 4);
+            b[4 * h] = bv.x; b[4 * h + 1] = bv.y; b[4 * h + 2] = bv.z; b[4 * h + 3] = bv.w;
+          }
 #pragma unroll
           for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
+            for (int c = 0; c < NC; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
         }
       } else {
 #pragma unroll
         for (int t = 0; t < kBK2; t += 2) {
-          uint32_t x0[8], x1[8], b0[8], b1[8];
+          uint32_t x0[8], x1[8], b0[NC], b1[NC];
           {
             const uint4 p = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
             const uint4 q = *reinterpret_cast<const uint4 *>(sx + t * kTile + 64 + ty * 4);
@@ -138,19 +150,18 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             x0[0] = p.x; x0[1] = p.y; x0[2] = p.z; x0[3] = p.w; x0[4] = q.x; x0[5] = q.y; x0[6] = q.z; x0[7] = q.w;
             x1[0] = u.x; x1[1] = u.y; x1[2] = u.z; x1[3] = u.w; x1[4] = v.x; x1[5] = v.y; x1[6] = v.z; x1[7] = v.w;
           }
-          {
-            const uint4 p = *reinterpret_cast<const uint4 *>(sb + t * kTile + tx * 4);
-            const uint4 q = *reinterpret_cast<const uint4 *>(sb + t * kTile + 64 + tx * 4);
-            const uint4 u = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + tx * 4);
-            const uint4 v = *reinterpret_cast<const uint4 *>(sb + (t + 1) * kTile + 64 + tx * 4);
-            b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
-            b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
+#pragma unroll
+          for (int h = 0; h < NC / 4; ++h) {
+            const uint4 p = *reinterpret_cast<const uint4 *>(sb + t * TN + h * 64 + tx * 4);
+            const uint4 u = *reinterpret_cast<const uint4 *>(sb + (t + 1) * TN + h * 64 + tx * 4);
+            b0[4 * h] = p.x; b0[4 * h + 1] = p.y; b0[4 * h + 2] = p.z; b0[4 * h + 3] = p.w;
+            b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
 #pragma unroll
           for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              if (c < DPXC) {
+            for (int c = 0; c < NC; ++c) {
+              if ((r * NC + c) % 8 < DPXC) {
                 acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
                 acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
               } else {
@@ -175,12 +186,12 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 
   // ---------------------------------------------------------------- epilogue --
   // v = min(lo, hi) per accumulator; pairs (c, c+1) packed (min_c | min_{c+1} << 16).
-  uint32_t out[8][4];
+  uint32_t out[8][NC / 2];
   auto fold = [&]() {
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
+      for (int p = 0; p < NC / 2; ++p) {
         uint32_t a0 = acc[r][2 * p], a1 = acc[r][2 * p + 1];
         out[r][p] = __vmins2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
       }
@@ -190,7 +201,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
+      for (int p = 0; p < NC / 2; ++p) {
         // column pair jp covers columns j0 + (p>>1)*64 + tx*4 + (p&1)*2 + {0,1}
         int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
         uint4 v = make_uint4(out[g * 4 + 0][p], out[g * 4 + 1][p], out[g * 4 + 2][p], out[g * 4 + 3][p]);
@@ -212,7 +223,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
         const int kb0 = (int)(e - (int64_t)r * KBt);
         const int KB = (int)((e1 - e) < (int64_t)(KBt - kb0) ? (e1 - e) : (int64_t)(KBt - kb0));
         const int seg = c - sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
-        tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);
+        tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);   // SK: TN = 128
         if (it > 0 && !TMA) __syncthreads();   // every warp is done with the previous segment's stages
         mainloop(i0, j0, kb0, KB, it);
         fold();
@@ -225,6 +236,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   }
   // classic CTA: one whole tile (or, split-K, the k-range blockIdx.y of gridDim.y)
   tile_origin((int)blockIdx.x, nti, ntj, kgroup, i0, j0);
+  if constexpr (TN != kTile) j0 = j0 / kTile * TN;
   {
     const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
     const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
@@ -258,7 +270,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       int64_t i = i0 + (r >> 2) * 64 + ty * 4 + (r & 3);
       if (i >= M) continue;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
+      for (int p = 0; p < NC / 2; ++p) {
         int64_t j = j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2;
         int v0 = (int)(out[r][p] & 0xFFFF), v1 = (int)(out[r][p] >> 16);
         if (epi.accumulate) {
@@ -281,11 +293,11 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   int32_t dmin = INT_MAX;
   {
     const int64_t gi0 = epi.diag_row0 + i0;
-    if (gi0 < j0 + kTile && j0 < gi0 + kTile) {
+    if (gi0 < j0 + TN && j0 < gi0 + kTile) {
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+        for (int p = 0; p < NC / 2; ++p)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             int64_t gi = gi0 + (r >> 2) * 64 + ty * 4 + (r & 3);
@@ -319,7 +331,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
       for (int g = 0; g < 2; ++g)
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < NC / 2; ++p) {
           int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
           uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + jp * ldc + i0 + g * 64 + ty * 4));
           const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
@@ -465,26 +477,25 @@ minplus_gemm32_kernel(const int32_t *__restrict__ XT, int64_t ldx, const int32_t
   }
 }
 
-template <int OUT, bool STATS, int DPXC, bool TMA, bool SK>
+template <int OUT, bool STATS, int DPXC, bool TMA, bool SK, int TN>
 int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
                   cudaStream_t st, int nsplit, const PeerB &pb, const TmaOps *tma) {
   static bool attr_set[64] = {};
+  const size_t smem = (size_t)kStages * kBK2 * (kTile + TN) * 4 + (TMA ? 1024 : 0);
   int dev = 0;
   RD_CUDA_CHECK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kSmemBytes + (TMA ? 1024 : 0))));
+    RD_CUDA_CHECK(cudaFuncSetAttribute(minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK, TN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
-  const int nti = (int)(Mp / kTile), ntj = (int)(Np / kTile);
+  const int nti = (int)(Mp / kTile), ntj = (int)(Np / TN);
   TmaOps t{};
   if (tma) t = *tma;
   // stream-K steps: sk_nfull whole-tile CTAs, then sk_nsk CTAs sharing the remaining tiles
   const unsigned gx = SK ? (unsigned)(epi.sk_nfull + epi.sk_nsk) : (unsigned)(nti * ntj);
-  minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK><<<dim3(gx, (unsigned)nsplit), kThreads,
-                                              kSmemBytes + (TMA ? 1024 : 0), st>>>(
+  minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK, TN><<<dim3(gx, (unsigned)nsplit), kThreads, smem, st>>>(
       XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb, t);
   RD_CUDA_CHECK(cudaGetLastError());
   return RD_OK;
@@ -517,6 +528,13 @@ int launch_gemm32_v(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t l
                                                      int64_t, void *, int64_t, int64_t, int64_t, int64_t,  \
                                                      int64_t, const rd::EpiArgs &, cudaStream_t, int,      \
                                                      const rd::PeerB &, const rd::TmaOps *);
+// TN = 64 instances (PM output, cp.async): RD_INST_GEMM64_ALL(STATS)
+#define RD_INST_GEMM64(STATS, D)                                                                           \
+  template int rd::launch_gemm_v<rd::kOutPM, STATS, D, false, false, 64>(                                  \
+      const uint32_t *, int64_t, const uint32_t *, int64_t, int64_t, void *, int64_t, int64_t, int64_t,     \
+      int64_t, int64_t, const rd::EpiArgs &, cudaStream_t, int, const rd::PeerB &, const rd::TmaOps *);
+#define RD_INST_GEMM64_ALL(STATS) \
+  RD_INST_GEMM64(STATS, 0) RD_INST_GEMM64(STATS, 2) RD_INST_GEMM64(STATS, 3) RD_INST_GEMM64(STATS, 4) RD_INST_GEMM64(STATS, 8)
 #define RD_INST_GEMM_ALL(OUT, STATS, TMA, ...)                                                               \
   RD_INST_GEMM(OUT, STATS, 0, TMA, ##__VA_ARGS__) RD_INST_GEMM(OUT, STATS, 2, TMA, ##__VA_ARGS__)             \
   RD_INST_GEMM(OUT, STATS, 3, TMA, ##__VA_ARGS__) RD_INST_GEMM(OUT, STATS, 4, TMA, ##__VA_ARGS__)             \

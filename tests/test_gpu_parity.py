@@ -1087,3 +1087,26 @@ def test_small_chain_kernel_generic_matrices(N, seed):
     assert (got["found"], got["n0"], got["alpha"], got["beta"], got["k_stop"]) == (
         ref["found"], ref["n0"], ref["alpha"], ref["beta"], ref["k_stop"])
     assert got["diag"][1:ref["k_stop"] + 1] == ref["diag"][1:ref["k_stop"] + 1]
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3, 4, 8])
+def test_tile64_chain_equals_oracle(variant):
+    """128 x 64 tiles (rd_set_gemm_tile(64): 8 x 4 accumulators per thread, 3 CTAs per SM): every
+    power of m = 5 and a ragged m = 7 row panel equal the oracle, for every instruction mix, with
+    and without split-K."""
+    rd.rd_set_gemm_tile(64)
+    rd.rd_set_gemm_variant(variant)
+    try:
+        for m, r0, r1, split in ((5, 0, 287, True), (7, 128, 1000, True), (7, 0, 2507, False)):
+            rd.rd_set_split_k(split)
+            ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+            P = {k: X for k, X in O.powers(m, 6)}
+            for k in range(2, 7):
+                s = ch.step().cpu().numpy()
+                assert (ch.read_rows(k) == to_inf(P[k][r0:r1], OINF, RINF, np.int16)).all(), (m, k)
+                assert s[0] == min(int(min(P[k][i, i] for i in range(r0, r1))), RINF)
+            ch.close()
+    finally:
+        rd.rd_set_gemm_tile(128)
+        rd.rd_set_gemm_variant(3)
+        rd.rd_set_split_k(True)

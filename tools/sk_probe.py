@@ -24,20 +24,24 @@ def med(m, r0, r1, reps=10):
     return statistics.median(a.elapsed_time(b) for a, b in ev)
 
 
-MODES = {"plain": (False, 0), "splitk": (True, 0), "streamk": (False, 2), "model": (True, 1)}
-cases = [(6, 1), (7, 1), (7, 2), (8, 1), (8, 2), (8, 4), (8, 8), (9, 2), (9, 4), (9, 8)]
+MODES = {"plain": (False, 0, 128), "splitk": (True, 0, 128), "t64": (False, 0, 64), "t64split": (True, 0, 64)}
+cases = [(6, 1), (7, 1), (7, 2), (8, 1), (8, 2), (8, 4), (8, 8), (9, 1), (9, 8)]
 if len(sys.argv) > 1:
     cases = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]]
 for m, parts in cases:
     N = rd.count_words(m)
     r0, r1 = D.panel_bounds(N, parts, 0)
     res = {}
-    for name, (split, sk) in MODES.items():
+    for name, (split, sk, tn) in MODES.items():
         rd.rd_set_split_k(split)
         rd.rd_set_stream_k(sk)
+        rd.rd_set_gemm_tile(tn)
+        rd.rd_set_gemm_tma(0 if tn == 64 else 1)
         res[name] = med(m, r0, r1, reps=10 if m < 9 else 3)
     rd.rd_set_split_k(True)
     rd.rd_set_stream_k(0)
+    rd.rd_set_gemm_tile(128)
+    rd.rd_set_gemm_tma(1)
     terms = (r1 - r0) * N * N
     print(f"m={m} p={parts} rows=[{r0},{r1}) " + "  ".join(f"{k} {v:.4f} ms ({terms / v / 1e9:.1f} T)" for k, v in res.items()),
           flush=True)
