@@ -163,6 +163,16 @@ def _cpu_model():
     return None
 
 
+def _measured_hbm_gbs():
+    """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written), else the profiling guide's
+    fallback of 6.5 TB/s."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6500.0
+
+
 def cores_used():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
@@ -410,6 +420,27 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                                "data": "uniform [0, 2^29) int32, 1% inf, seeds 7, 8"}
         del X32, Y32, C32
 
+    # the standalone reductions (a3 + a4 of the all-gather form, rd_panel_stats): diag-min and
+    # the periodicity stats of a full m-sized power against alpha_max earlier ones, HBM-bound;
+    # algorithmic bytes (1 + alpha_max) * 2 N^2 per call
+    reductions = None
+    if rank == 0 and not args.no_e2e:
+        g = torch.Generator(device=dev).manual_seed(0)
+        cur = torch.randint(100, 140, (N, N), dtype=torch.int16, device=dev, generator=g)
+        prevs = [torch.randint(60 + 4 * a, 100, (N, N), dtype=torch.int16, device=dev, generator=g)
+                 for a in range(am)]
+        sr = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device=dev)
+        med, best = timed(lambda: rd.rd_panel_stats(cur, prevs, 0, am, sr, stream=stream))
+        byts = (1 + am) * 2 * float(N) * N
+        hbm = _measured_hbm_gbs()
+        reductions = {"call": "rd_panel_stats (diag min + periodicity stats of alpha = 1..alpha_max, one pass)",
+                      "N": N, "alpha_max": am, "ms_median": round(med * 1e3, 4), "ms_best": round(best * 1e3, 4),
+                      "algorithmic_bytes": int(byts), "achieved_gbs": round(byts / med / 1e9, 1),
+                      "peak_gbs": hbm, "frac": round(byts / med / 1e9 / hbm, 4) if hbm else None,
+                      "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy read+write)",
+                      "data": "uniform int16 bands (seeded), fully finite"}
+        del cur, prevs
+
     # time to periodicity per m (Alg 2 to first detection): build (words, A(G), upload,
     # packing) and chain (products + fused checks + per-step stats decision), max over ranks
     ttp = {}
@@ -542,6 +573,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_periodicity": ttp,
+            "reductions": reductions,
             "gops_by_m": gops_by_m,
             "operand_invariance": invariance,
             "paper_context": {"k80_cumatrixtrop_gops_derived": PAPER_K80_GOPS.get(m),

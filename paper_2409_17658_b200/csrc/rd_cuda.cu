@@ -653,6 +653,133 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
   }
 }
 
+// Streaming form of panel_stats_kernel for 16-byte aligned panels (ld % 8 == 0): every thread
+// keeps PS stages of its chunks (the current power's and each earlier power's 16 bytes) in
+// flight with cp.async into its own shared-memory slots — no registers held by outstanding
+// loads, so one 256-thread block per SM sustains ~PS x 45 KB in flight — and folds a stage
+// once it lands.  A ragged last chunk of a row is zero-filled by cp.async and re-marked +inf.
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, int bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+
+template <int NA, int PS>
+__global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_t *__restrict__ cur, int64_t rows,
+                                                                  int64_t cols, int64_t ld, int64_t diag_row0,
+                                                                  PanelStatsArgs pa, int a0,
+                                                                  int32_t *__restrict__ stats) {
+  constexpr int NR = NA > 0 ? NA : 1;
+  extern __shared__ uint4 sbuf[];   // [PS][1 + NA][256]
+  __shared__ int32_t red[8][1 + 4 * NR];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int32_t dmin = INT_MAX;
+  uint32_t lo2[NR], hi2[NR], mis[NR], fin[NR];
+#pragma unroll
+  for (int a = 0; a < NR; ++a) { lo2[a] = 0x7FFF7FFFu; hi2[a] = 0x80008000u; mis[a] = 0; fin[a] = 0; }
+  const int16_t *pp[NR];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) pp[a] = pa.prev[a0 + a];
+  const int64_t cpr = (cols + 7) / 8, total = rows * cpr;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x, v0 = (int64_t)blockIdx.x * blockDim.x + tid;
+  auto slot = [&](int st, int arr) -> uint4 * { return &sbuf[(st * (1 + NA) + arr) * 256 + tid]; };
+  auto issue = [&](int st, int64_t v) {
+    if (v < total) {
+      const int64_t i = v / cpr, j = (v - i * cpr) * 8, off = i * ld + j;
+      const int bytes = j + 8 <= cols ? 16 : (int)(cols - j) * 2;
+      cp_async16_zfill(slot(st, 0), cur + off, bytes);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) cp_async16_zfill(slot(st, 1 + a), pp[a] + off, bytes);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < PS - 1; ++st) issue(st, v0 + st * gs);
+  for (int64_t it = 0;; ++it) {
+    const int64_t v = v0 + it * gs;
+    if (v >= total) break;
+    issue((int)((it + PS - 1) % PS), v + (PS - 1) * gs);
+    cp_async_wait<PS - 1>();
+    const int st = (int)(it % PS);
+    const int64_t i = v / cpr, j = (v - i * cpr) * 8;
+    // lanes past the row's end (zero-filled) become +inf in both powers: neutral in the stats
+    uint4 x = *slot(st, 0);
+    uint32_t o[4] = {x.x, x.y, x.z, x.w};
+    uint32_t padw[4] = {0, 0, 0, 0};
+    if (j + 8 > cols) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        padw[q] = (j + 2 * q < cols ? 0u : 0x0000FFFFu) | (j + 2 * q + 1 < cols ? 0u : 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q] | padw[q], kInf2);
+    if (a0 == 0) {
+      const int64_t gi = diag_row0 + i;
+      if (gi >= j && gi < j + 8 && gi < cols) {
+        const int t = (int)(gi - j);
+        dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const uint4 y = *slot(st, 1 + a);
+      const uint32_t w[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q] | padw[q], kInf2), lo2[a], hi2[a], mis[a], fin[a]);
+    }
+  }
+  cp_async_wait<0>();
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  if (lane == 0) red[warp][0] = dmin;
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    int32_t lo = min((int32_t)(int16_t)(lo2[a] & 0xFFFF), (int32_t)(int16_t)(lo2[a] >> 16));
+    int32_t hi = max((int32_t)(int16_t)(hi2[a] & 0xFFFF), (int32_t)(int16_t)(hi2[a] >> 16));
+    if (!(fin[a] & 0xFFFF) && !(fin[a] >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
+    const int32_t v0r = __reduce_min_sync(0xffffffffu, lo), v1 = __reduce_min_sync(0xffffffffu, -hi);
+    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis[a] ? -1 : 0);
+    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin[a] ? -1 : 0);
+    if (lane == 0) {
+      red[warp][1 + 4 * a] = v0r; red[warp][2 + 4 * a] = v1; red[warp][3 + 4 * a] = v2; red[warp][4 + 4 * a] = v3;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 1 + 4 * NA; e += blockDim.x) {
+    int32_t v = red[0][e];
+#pragma unroll
+    for (int w2 = 1; w2 < 8; ++w2) v = min(v, red[w2][e]);
+    if (e == 0) {
+      if (a0 == 0) atomicMin(stats, v);
+    } else {
+      atomicMin(stats + 4 * a0 + e, v);
+    }
+  }
+}
+
+template <int NA>
+static int launch_panel_stats(const int16_t *cur, int64_t rows, int64_t cols, int64_t ld, int64_t diag_row0,
+                              const PanelStatsArgs &pa, int a0, int32_t *stats, int sms, cudaStream_t st, bool vec) {
+  const int64_t chunks = rows * ((cols + 7) / 8);
+  if (vec) {
+    constexpr int PS = (1 + NA) * 4096 * 4 <= 200 * 1024 ? 4 : 3;
+    constexpr int smem = PS * (1 + NA) * 4096;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !attr[dev]) {
+      RD_CUDA_CHECK(cudaFuncSetAttribute(panel_stats_stream_kernel<NA, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem));
+      attr[dev] = true;
+    }
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms));
+    panel_stats_stream_kernel<NA, PS><<<grid, 256, smem, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats);
+  } else {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms * 4));
+    panel_stats_kernel<NA><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats);
+  }
+  RD_CUDA_CHECK(cudaGetLastError());
+  return RD_OK;
+}
+
 extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, int nprev, int64_t rows,
                               int64_t cols, int64_t ld, int64_t diag_row0, int alpha_max, int32_t *stats_dev,
                               void *cuda_stream) try {
@@ -675,18 +802,20 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one thread per 16-byte chunk of the panel, grid-strided; every alpha of a pass in one sweep
-  const int64_t chunks = rows * ((cols + 7) / 8);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms * 4));
+  // (16-byte aligned panels: the cp.async streaming kernel, one block per SM)
+  bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
+  for (int a = 0; a < nprev; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a]) & 15) == 0);
   for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 16) {
     const int na = std::min(16, nprev - a0);
+    int rc = RD_OK;
     switch (na) {
 #define RD_PS(K) \
-  case K: panel_stats_kernel<K><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev); break;
+  case K: rc = launch_panel_stats<K>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev, sms, st, vec); break;
       RD_PS(0) RD_PS(1) RD_PS(2) RD_PS(3) RD_PS(4) RD_PS(5) RD_PS(6) RD_PS(7) RD_PS(8)
       RD_PS(9) RD_PS(10) RD_PS(11) RD_PS(12) RD_PS(13) RD_PS(14) RD_PS(15) RD_PS(16)
 #undef RD_PS
     }
-    RD_CUDA_CHECK(cudaGetLastError());
+    if (rc != RD_OK) return rc;
   }
   return RD_OK;
 } RD_ABI_CATCH("rd_panel_stats")
