@@ -338,7 +338,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   if (OUT_PM && STATS && epi.sk_nsk > 0) {   // stream-K step (rd_set_stream_k)
 #define RD_LGS(D, T) launch_gemm_v<kOutPM, true, D, T, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, 1, pb, tma)
 #define RD_LGS2(D) return tma ? RD_LGS(D, true) : RD_LGS(D, false)
-    switch (g_dpx_cols) {
+    switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
       case 0: RD_LGS2(0);
       case 2: RD_LGS2(2);
       case 3: RD_LGS2(3);
@@ -350,7 +350,9 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
-    switch (g_dpx_cols) {
+    switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
+      case 13: return RD_LGT(13);
+      case 14: return RD_LGT(14);
       case 0: return RD_LGT(0);
       case 2: return RD_LGT(2);
       case 3: return RD_LGT(3);
@@ -372,6 +374,8 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
   switch (g_dpx_cols) {
+    case 13: return RD_LG(13);
+    case 14: return RD_LG(14);
     case 0: return RD_LG(0);
     case 2: return RD_LG(2);
     case 3: return RD_LG(3);
@@ -384,7 +388,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
 int launch_gemm32(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
 #define RD_LG32(D) launch_gemm32_v<D>(XT, ldx, BP, ldb, kp, C, ldc, M, N, Mp, Np, accumulate, st)
-  switch (g_dpx_cols) {
+  switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
     case 0: return RD_LG32(0);
     case 2: return RD_LG32(2);
     case 3: return RD_LG32(3);
@@ -414,8 +418,9 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 
 extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   rd_enter();
-  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
-    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
+  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8 && dpx_cols != 13 &&
+      dpx_cols != 14)
+    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8, 13, 14");
   g_dpx_cols = dpx_cols;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")
@@ -660,7 +665,7 @@ __global__ void __launch_bounds__(256) panel_stats_kernel(const int16_t *__restr
 // once it lands.  A ragged last chunk of a row is zero-filled by cp.async and re-marked +inf.
 __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, int bytes) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes));
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes));
 }
 
 template <int NA, int PS>
@@ -2869,7 +2874,7 @@ extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) try {
   int rc;
 #define RD_AG(D) launch_gemm_v<kOutRP, true, D>(c->XL, c->Mp, nullptr, c->P, c->P / 2, c->slot(knew), c->P, c->Mr, \
                                                  c->N, c->Mp, c->P, epi, c->st, 1, pb)
-  switch (g_dpx_cols) {
+  switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
     case 0: rc = RD_AG(0); break;
     case 2: rc = RD_AG(2); break;
     case 3: rc = RD_AG(3); break;

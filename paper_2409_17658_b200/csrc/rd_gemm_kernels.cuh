@@ -157,6 +157,23 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             b0[4 * h] = p.x; b0[4 * h + 1] = p.y; b0[4 * h + 2] = p.z; b0[4 * h + 3] = p.w;
             b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
+          if constexpr (DPXC >= 10 && NC == 8) {
+            // DPXC = 10 + d: the same mix with d DPX columns, written in pipe-alternating order
+            // (IMAD, DPX, IMAD, DPX, VIMNMX3, ...) per row
+            constexpr int D = DPXC - 10;
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+              for (int u = 0; u < 8 - D || u < D; ++u) {
+                const int ci = D + u, cd = u;
+                uint32_t s0 = 0, s1 = 0;
+                if (ci < 8) s0 = x0[r] * one + b0[ci];
+                if (cd < D) acc[r][cd] = __viaddmin_s16x2(x0[r], b0[cd], acc[r][cd]);
+                if (ci < 8) s1 = x1[r] * one + b1[ci];
+                if (cd < D) acc[r][cd] = __viaddmin_s16x2(x1[r], b1[cd], acc[r][cd]);
+                if (ci < 8) acc[r][ci] = __vimin3_s16x2(acc[r][ci], s0, s1);
+              }
+          } else {
 #pragma unroll
           for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -170,6 +187,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                 acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
               }
             }
+          }
         }
       }
       if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages

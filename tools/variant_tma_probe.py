@@ -27,7 +27,7 @@ def run(m, d, steps=6, reps=5):
 
 for m in (8, 9):
     base = None
-    for d in (3, 4, 2, 8, 3):
+    for d in ((3, 13, 4, 14, 3) if len(sys.argv) < 2 else [int(x) for x in sys.argv[1:]]):
         s, x, t = run(m, d)
         if base is None:
             base = (s, x)
