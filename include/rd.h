@@ -363,10 +363,11 @@ int rd_set_gemm_tile(int tn);
  * always.  Identical results.  RD_EINVAL outside 0..2. */
 int rd_set_gemm_tma(int mode);
 
-/* rd_set_split_k — process-wide switch (default on) of split-K in dense chain steps whose
- * grid is under 3 waves (2 CTAs x the SM count): the k-range is split over 2 or 4 CTAs per
- * tile and a combine kernel takes the min, stores the power and computes the stats.
- * Identical results.  Always RD_OK. */
+/* rd_set_split_k — process-wide split-K policy of dense chain steps: 1 (default) = split the
+ * k-range over n <= 8 CTAs per tile when the wave model predicts >= 3% (small grids); 0 = never;
+ * n >= 2 = always n ways (probes, tests).  Each split CTA writes its partial tile to a
+ * workspace and takes a ticket; the last CTA of a tile folds the partials, stores the power and
+ * computes the fused stats (no separate combine pass).  Identical results.  Always RD_OK. */
 int rd_set_split_k(int enable);
 
 /* rd_set_stream_k — process-wide choice for dense chain steps whose last wave of

@@ -338,13 +338,14 @@ def rd_set_gemm_tma(mode):
     _check(lib().rd_set_gemm_tma(int(mode)))
 
 
-def rd_set_split_k(enable: bool):
-    """Split-K for small dense chain grids (default on; identical results)."""
-    _check(lib().rd_set_split_k(1 if enable else 0))
+def rd_set_split_k(enable):
+    """Split-K policy of dense chain steps (rd.h): True/1 model (default), False/0 never,
+    n >= 2 always n ways; identical results."""
+    _check(lib().rd_set_split_k(int(enable) if not isinstance(enable, bool) else (1 if enable else 0)))
 
 
 def rd_set_stream_k(mode: int):
-    """Stream-K remainder of dense chain steps (rd.h): 0 off, 1 model (default), 2 forced."""
+    """Stream-K remainder of dense chain steps (rd.h): 0 off (default), 1 model, 2 forced."""
     _check(lib().rd_set_stream_k(int(mode)))
 
 

@@ -338,7 +338,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   if (OUT_PM && STATS && epi.sk_nsk > 0) {   // stream-K step (rd_set_stream_k)
 #define RD_LGS(D, T) launch_gemm_v<kOutPM, true, D, T, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, 1, pb, tma)
 #define RD_LGS2(D) return tma ? RD_LGS(D, true) : RD_LGS(D, false)
-    switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
+    switch (g_dpx_cols) {
       case 0: RD_LGS2(0);
       case 2: RD_LGS2(2);
       case 3: RD_LGS2(3);
@@ -350,7 +350,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
-    switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
+    switch (g_dpx_cols) {
       case 13: return RD_LGT(13);
       case 14: return RD_LGT(14);
       case 0: return RD_LGT(0);
@@ -374,8 +374,6 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
   switch (g_dpx_cols) {
-    case 13: return RD_LG(13);
-    case 14: return RD_LG(14);
     case 0: return RD_LG(0);
     case 2: return RD_LG(2);
     case 3: return RD_LG(3);
@@ -388,7 +386,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
 int launch_gemm32(const int32_t *XT, int64_t ldx, const int32_t *BP, int64_t ldb, int64_t kp, int32_t *C,
                   int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, int accumulate, cudaStream_t st) {
 #define RD_LG32(D) launch_gemm32_v<D>(XT, ldx, BP, ldb, kp, C, ldc, M, N, Mp, Np, accumulate, st)
-  switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
+  switch (g_dpx_cols) {
     case 0: return RD_LG32(0);
     case 2: return RD_LG32(2);
     case 3: return RD_LG32(3);
@@ -418,9 +416,8 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 
 extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   rd_enter();
-  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8 && dpx_cols != 13 &&
-      dpx_cols != 14)
-    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8, 13, 14");
+  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
+    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
   g_dpx_cols = dpx_cols;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")
@@ -1909,6 +1906,7 @@ struct rd_chain {
   uint32_t *ent = nullptr;
   int16_t *wcol = nullptr;   // uniform-label format (see minplus_sparse_kernel)
   uint32_t *ws = nullptr;    // method 0 split-K partial tiles (small grids), lazily allocated
+  int *tile_cnt = nullptr;   // method 0 split-K fixup tickets, one per tile (self-resetting)
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
@@ -2314,6 +2312,7 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
+static int g_split_force = 0;   // rd_set_split_k(n >= 2): every dense step splits K n ways (probes, tests)
 // rd_set_stream_k: 0 (default) off, 1 by the wave model, 2 whenever the last wave is partial
 static int g_stream_k = 0;
 // rd_set_small_chain: dense Algorithm 2 of orders N <= kSmallMaxN as one device-resident kernel
@@ -2390,6 +2389,7 @@ extern "C" int rd_set_sparse_bytes(int enable) try {
 
 extern "C" int rd_set_split_k(int enable) try {
   g_split_k_off = enable ? 0 : 1;
+  g_split_force = enable >= 2 ? std::min(enable, 8) : 0;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_split_k")   // rd_set_sparse_variant (default: measured best, 1024 threads)
 
@@ -2480,6 +2480,7 @@ extern "C" int rd_chain_destroy(rd_chain *c) try {
   chain_free(c, c->ent);
   chain_free(c, c->wcol);
   chain_free(c, c->ws);
+  chain_free(c, c->tile_cnt);
   chain_free(c, c->spread);
   for (void *p : {(void *)c->perm, (void *)c->inv, (void *)c->lane_col, (void *)c->slab_start, (void *)c->desc,
                   (void *)c->ent8})
@@ -2571,7 +2572,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const int64_t slots = 2 * (int64_t)sms;
-    const double t_stage = 8.2e-6, bw = 6.0e12, slot_bytes = 4.0 * (double)c->slot_words;
+    const double t_stage = 8.2e-6, bw = 6.0e12;
     const double tile_bytes = 4.0 * kTile * kTile / 2;
     const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
     const double lone = 0.74;
@@ -2581,10 +2582,11 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     for (int n = 2; n <= 8 && kstages >= 2 * n; ++n) {
       const double waves = (double)((ntiles * n + slots - 1) / slots);
       double cost = waves * ((double)kstages / n + 2.0);   // + pipeline fill / epilogue per CTA
-      cost += (n + 2 + epi.nprev) * slot_bytes / bw / t_stage;
+      cost += 0.2 * n;   // in-kernel fixup: each split CTA writes its partial, the last reads them
       if (cost < best) { best = cost; nsplit = n; }
     }
     if (g_split_k_off) { nsplit = 1; best = cost1; }
+    if (g_split_force) { nsplit = (int)std::min<int64_t>(g_split_force, std::max<int64_t>(1, kstages / 2)); best = 0.0; }
     if (g_stream_k && rem > 0) {
       const int64_t R = rem * kstages;
       const int nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, R / 4));   // >= 4 stages each
@@ -2628,26 +2630,25 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
                                      c->N, c->Mp, c->P, epi, c->st, 1, tma);
     if (rc != RD_OK) return rc;
   } else {
+    // split-K with the in-kernel fixup: partial tiles in c->ws, the last CTA of each tile folds
+    // them, stores the power and computes the stats (no separate combine pass)
     if (!c->ws || c->nsplit < nsplit) {
       chain_free(c, c->ws);
       c->ws = nullptr;
       RD_CUDA_CHECK(chain_malloc(c, &c->ws, (size_t)nsplit * c->slot_words * 4));
       c->nsplit = nsplit;
     }
-    EpiArgs ge{};
-    ge.split_stride = c->slot_words;
-    int rc = launch_gemm<true, false>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->ws, c->Mp, c->Mr, c->N, c->Mp,
-                                      c->P, ge, c->st, nsplit, tma);
-    if (rc != RD_OK) return rc;
-    int dev = c->device, sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t nv = c->slot_words / 4;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, (int64_t)sms * 8));
-    for (int a0 = 0; a0 < std::max(epi.nprev, 1); a0 += 8) {
-      combine_pm_kernel<<<grid, 256, 0, c->st>>>(c->ws, c->slot_words, nsplit, c->slot(knew), c->slot_words, c->Mp,
-                                                 epi, a0);
-      RD_CUDA_CHECK(cudaGetLastError());
+    const int64_t max_tiles = (c->Mp / kTile) * (c->P / 64);
+    if (!c->tile_cnt) {
+      RD_CUDA_CHECK(chain_malloc(c, &c->tile_cnt, (size_t)max_tiles * 4));
+      RD_CUDA_CHECK(cudaMemsetAsync(c->tile_cnt, 0, (size_t)max_tiles * 4, c->st));
     }
+    epi.split_stride = c->slot_words;
+    epi.split_ws = c->ws;
+    epi.split_cnt = c->tile_cnt;
+    int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
+                                     c->N, c->Mp, c->P, epi, c->st, nsplit, tma);
+    if (rc != RD_OK) return rc;
   }
   c->k = knew;
   return RD_OK;
@@ -2874,7 +2875,7 @@ extern "C" int rd_agchain_step(rd_agchain *c, int32_t *stats_dev) try {
   int rc;
 #define RD_AG(D) launch_gemm_v<kOutRP, true, D>(c->XL, c->Mp, nullptr, c->P, c->P / 2, c->slot(knew), c->P, c->Mr, \
                                                  c->N, c->Mp, c->P, epi, c->st, 1, pb)
-  switch (g_dpx_cols % 10) {   // 13, 14: the interleaved PM forms only
+  switch (g_dpx_cols) {
     case 0: rc = RD_AG(0); break;
     case 2: rc = RD_AG(2); break;
     case 3: rc = RD_AG(3); break;

@@ -56,6 +56,12 @@ struct EpiArgs {
   int64_t diag_row0;       // global row index of local row 0 (row panels)
   int accumulate;          // row-major output only: C = min(C, X (x) B)
   int64_t split_stride;    // split-K (gridDim.y > 1, PM output): u32 between the splits' partial tiles
+  // split-K with in-kernel fixup (split_cnt != nullptr, PM output): every split CTA writes its
+  // partial tile to split_ws + blockIdx.y * split_stride and takes a ticket on split_cnt[tile];
+  // the last one folds the others' partials into its registers and runs the ordinary epilogue
+  // (store into C, fused stats).  The counters reset themselves.
+  uint32_t *split_ws;
+  int *split_cnt;
   const int *spread_in;    // structured step: 1 if some row of X has a finite spread > 254 (nullable)
   int *spread_out;         // ... the same flag for the output, for the next step (nullable)
   // Stream-K remainder (PM output, DESIGN.md §5 "Wave quantisation"): CTAs [0, sk_nfull)

@@ -157,23 +157,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             b0[4 * h] = p.x; b0[4 * h + 1] = p.y; b0[4 * h + 2] = p.z; b0[4 * h + 3] = p.w;
             b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
-          if constexpr (DPXC >= 10 && NC == 8) {
-            // DPXC = 10 + d: the same mix with d DPX columns, written in pipe-alternating order
-            // (IMAD, DPX, IMAD, DPX, VIMNMX3, ...) per row
-            constexpr int D = DPXC - 10;
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-#pragma unroll
-              for (int u = 0; u < 8 - D || u < D; ++u) {
-                const int ci = D + u, cd = u;
-                uint32_t s0 = 0, s1 = 0;
-                if (ci < 8) s0 = x0[r] * one + b0[ci];
-                if (cd < D) acc[r][cd] = __viaddmin_s16x2(x0[r], b0[cd], acc[r][cd]);
-                if (ci < 8) s1 = x1[r] * one + b1[ci];
-                if (cd < D) acc[r][cd] = __viaddmin_s16x2(x1[r], b1[cd], acc[r][cd]);
-                if (ci < 8) acc[r][ci] = __vimin3_s16x2(acc[r][ci], s0, s1);
-              }
-          } else {
 #pragma unroll
           for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -187,7 +170,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                 acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
               }
             }
-          }
         }
       }
       if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages
@@ -261,6 +243,36 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     mainloop(i0, j0, kb0, KB, 0);
   }
   fold();
+  bool fixed_up = false;
+  if constexpr (OUT == kOutPM && STATS) {
+    if (gridDim.y > 1 && epi.split_cnt) {   // split-K: the last CTA of the tile finishes it
+      __shared__ int s_last;
+      store_pm(epi.split_ws + (int64_t)blockIdx.y * epi.split_stride, i0, j0);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = atomicAdd(&epi.split_cnt[blockIdx.x], 1) == (int)gridDim.y - 1;
+      __syncthreads();
+      if (!s_last) return;
+      __threadfence();
+      for (int sp = 0; sp < (int)gridDim.y; ++sp) {
+        if (sp == (int)blockIdx.y) continue;
+        const uint32_t *W = epi.split_ws + (int64_t)sp * epi.split_stride;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int p = 0; p < NC / 2; ++p) {
+            const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+            const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(W + jp * ldc + i0 + g * 64 + ty * 4));
+            out[g * 4 + 0][p] = __vmins2(out[g * 4 + 0][p], w.x);
+            out[g * 4 + 1][p] = __vmins2(out[g * 4 + 1][p], w.y);
+            out[g * 4 + 2][p] = __vmins2(out[g * 4 + 2][p], w.z);
+            out[g * 4 + 3][p] = __vmins2(out[g * 4 + 3][p], w.w);
+          }
+      }
+      if (tid == 0) epi.split_cnt[blockIdx.x] = 0;   // ready for the next step
+      fixed_up = true;
+    }
+  }
 
   // RP word (rows 2q', 2q'+1 of row group g; columns h*64 + tx*4 + e) from the folded pairs
   auto rp_word = [&](int g, int q, int h, int e) -> uint32_t {
@@ -280,7 +292,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           *reinterpret_cast<uint4 *>(C + pr * ldc + j0 + h * 64 + tx * 4) = v;
         }
   } else if constexpr (OUT == kOutPM) {
-    store_pm(reinterpret_cast<uint32_t *>(Cv) + (int64_t)blockIdx.y * epi.split_stride, i0, j0);
+    store_pm(reinterpret_cast<uint32_t *>(Cv) + (fixed_up ? 0 : (int64_t)blockIdx.y * epi.split_stride), i0, j0);
   } else {
     int16_t *C = reinterpret_cast<int16_t *>(Cv);
 #pragma unroll

@@ -1110,3 +1110,29 @@ def test_tile64_chain_equals_oracle(variant):
         rd.rd_set_gemm_tile(128)
         rd.rd_set_gemm_variant(3)
         rd.rd_set_split_k(True)
+
+
+@pytest.mark.parametrize("tn", [128, 64])
+def test_forced_split_k_fixup_equals_oracle(tn):
+    """Split-K with the in-kernel fixup (the last CTA of a tile folds the partials and runs the
+    fused epilogue): forced 2, 3, 5 and 8 ways, both tile widths, every power and stats vector
+    equal the single-pass step, and the powers equal the oracle."""
+    rd.rd_set_gemm_tile(tn)
+    try:
+        for m, r0, r1 in ((5, 0, 287), (7, 128, 1000)):
+            P = {k: X for k, X in O.powers(m, 7)}
+            ref = None
+            for n in (0, 2, 3, 5, 8):
+                rd.rd_set_split_k(n)
+                ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+                st = [ch.step().cpu().numpy() for _ in range(6)]
+                rows = ch.read_rows(7)
+                ch.close()
+                assert (rows == to_inf(P[7][r0:r1], OINF, RINF, np.int16)).all(), (m, n)
+                if ref is None:
+                    ref = st
+                for a, b in zip(st, ref):
+                    assert (a == b).all(), (m, n)
+    finally:
+        rd.rd_set_split_k(1)
+        rd.rd_set_gemm_tile(128)
