@@ -351,8 +351,6 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
     switch (g_dpx_cols) {
-      case 13: return RD_LGT(13);
-      case 14: return RD_LGT(14);
       case 0: return RD_LGT(0);
       case 2: return RD_LGT(2);
       case 3: return RD_LGT(3);
