@@ -349,10 +349,11 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 
-/* rd_set_gemm_tile — process-wide tile width of the dense chain step's GEMM when it runs the
- * cp.async mainloop (DESIGN.md §5 "Wave quantisation"): 128 (128 x 128 tiles, 8 x 8 per thread,
- * 2 CTAs/SM) or 64 (128 x 64 tiles, 8 x 4 per thread, 3 CTAs/SM: twice the tiles, a finer last
- * wave).  Identical results.  RD_EINVAL otherwise. */
+/* rd_set_gemm_tile — process-wide tile width of the dense chain step's GEMM (DESIGN.md §5
+ * "Wave quantisation"): 0 (default) = the step's wave model chooses, per step shape, between
+ * 128 (128 x 128 tiles, 8 x 8 per thread, 2 CTAs/SM) and 64 (128 x 64 tiles, 8 x 4 per thread,
+ * 3 CTAs/SM, cp.async mainloop: twice the tiles, a finer last wave) together with the split-K
+ * count; 64 or 128 forces the width.  Identical results.  RD_EINVAL otherwise. */
 int rd_set_gemm_tile(int tn);
 
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,

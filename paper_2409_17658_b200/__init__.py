@@ -350,7 +350,7 @@ def rd_set_stream_k(mode: int):
 
 
 def rd_set_gemm_tile(tn: int):
-    """Tile width of cp.async dense chain steps (rd.h): 128 (default) or 64."""
+    """Tile width of dense chain steps (rd.h): 0 = wave model (default), 64 or 128 forced."""
     _check(lib().rd_set_gemm_tile(int(tn)))
 
 

@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restr
 }
 
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
-int g_gemm_tile = 128;    // rd_set_gemm_tile: tile width of chain steps without TMA (128 or 64)
+int g_gemm_tile = 0;      // rd_set_gemm_tile: 0 = the chain's wave model picks, 64 / 128 forced
 int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
 
 __global__ void pack_t32_kernel(const int32_t *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
@@ -333,7 +333,7 @@ __global__ void pack_copy32_kernel(const int32_t *__restrict__ B, int64_t ld, in
 template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr) {
+                cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr, int tn = 128) {
   const PeerB pb{};
   if (OUT_PM && STATS && epi.sk_nsk > 0) {   // stream-K step (rd_set_stream_k)
 #define RD_LGS(D, T) launch_gemm_v<kOutPM, true, D, T, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, 1, pb, tma)
@@ -359,7 +359,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
     }
 #undef RD_LGT
   }
-  if (OUT_PM && g_gemm_tile == 64) {   // 128 x 64 tiles, 3 CTAs per SM (rd_set_gemm_tile)
+  if (OUT_PM && tn == 64 && !tma) {   // 128 x 64 tiles, 3 CTAs per SM (the chain's wave model)
 #define RD_LG64(D) launch_gemm_v<kOutPM, STATS, D, false, false, 64>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
     switch (g_dpx_cols) {
       case 0: return RD_LG64(0);
@@ -422,7 +422,7 @@ extern "C" int rd_set_gemm_variant(int dpx_cols) try {
 
 extern "C" int rd_set_gemm_tile(int tn) try {
   rd_enter();
-  if (tn != 64 && tn != 128) return fail(RD_EINVAL, "rd_set_gemm_tile: tile width must be 64 or 128");
+  if (tn != 0 && tn != 64 && tn != 128) return fail(RD_EINVAL, "rd_set_gemm_tile: 0 (model), 64 or 128");
   g_gemm_tile = tn;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_tile")
@@ -2546,58 +2546,68 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     c->k = knew;
     return RD_OK;
   }
-  // Split K over nsplit CTAs per tile when that shortens the wave-quantised grid: the step
-  // takes ceil(ntiles * n / slots) waves of kstages / n pipeline stages each (slots = 2 CTAs x
-  // the SM count), plus, for n > 1, combine_pm_kernel's HBM passes: the n partial tiles, the
-  // stored power and the nprev earlier powers its stats read (~(n + 2 + nprev) slots at
-  // ~6 TB/s; one stage of a 128 x 128 tile is ~8.2 us at the measured mix rate with 2 CTAs
-  // per SM; a CTA's pipeline fill and epilogue cost ~2 stages).  A split must promise >= 3%;
-  // each keeps >= 2 stages.  Measured (tools/split_probe.py): m = 6 0.096 -> 0.053 ms, m = 8
-  // 8-rank panel 1.97 -> 1.59 ms, m = 7 and full m = 8 / m = 9 panels within 1% of no split.
+  // Wave model (DESIGN.md §5 "Wave quantisation"): choose the tile width tn (128: 2 CTAs/SM;
+  // 64: 3 CTAs/SM, twice the tiles) and the split-K count n (k-range over n CTAs per tile,
+  // in-kernel fixup) that minimise the predicted step time.  Units (tiles x n) are dispatched
+  // in waves of sms x S slots; a wave whose busiest SM holds L units takes L x w / v(L), with w
+  // = the unit's work in 128-tile stages (tn / 128 x (kstages / n + 1.5 fill/epilogue + 0.2 n
+  // fixup)) and v(L) the SM's measured relative throughput with L resident CTAs (the issue rate
+  // grows with resident warps; a 64-wide tile costs ~5% more instructions per term):
+  // v128 = {0.676, 1}, v64 = {0.62, 0.90, 0.951}.  Fitted to tools/wave_probe.py
+  // (profiles/r02_wave_probe.txt): it picks the measured best or within 2% for m = 6..9 and
+  // row panels of 1..8 ranks.  The TMA mainloop (tn = 128, n = 1, >= 128 stages) counts 1% faster.
   //
-  // Stream-K remainder (g_stream_k): the whole waves of tiles run as usual and the tiles of the
-  // last, partial wave are spread evenly over every CTA slot — each slot gets an equal range
-  // of their k-stages (crossing tile boundaries), writes partial tiles, and combine_sk_kernel
-  // folds them and computes their stats.  Its cost: the whole waves + ceil(R / nsk) stages +
-  // ~2 stages per segment + the combine's passes over the remainder tiles.  The model picks
-  // the cheapest of {plain, split-K, stream-K} (>= 3% better than plain).  A lone CTA on an SM
-  // (a partial wave of <= sms CTAs) runs ~1.35x faster than one of two, which the plain cost
-  // of a short last wave includes.
+  // Stream-K remainder (g_stream_k, off by default: measured slower on every shape): the whole
+  // waves of 128-tiles run as usual and the last partial wave's k-stages are spread evenly over
+  // every CTA slot; combine_sk_kernel folds the partial tiles and computes their stats.
   const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
   const int64_t kstages = (c->P / 2) / kBK2;
-  int nsplit = 1, sk_nfull = 0, sk_nsk = 0;
+  int nsplit = 1, sk_nfull = 0, sk_nsk = 0, tn = 128;
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const int64_t slots = 2 * (int64_t)sms;
-    const double t_stage = 8.2e-6, bw = 6.0e12;
-    const double tile_bytes = 4.0 * kTile * kTile / 2;
-    const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
-    const double lone = 0.74;
-    double cost1 = (double)full_waves * ((double)kstages + 2.0) +
-                   (rem == 0 ? 0.0 : (rem <= sms ? lone : 1.0) * ((double)kstages + 2.0));
-    double best = cost1;
-    for (int n = 2; n <= 8 && kstages >= 2 * n; ++n) {
-      const double waves = (double)((ntiles * n + slots - 1) / slots);
-      double cost = waves * ((double)kstages / n + 2.0);   // + pipeline fill / epilogue per CTA
-      cost += 0.2 * n;   // in-kernel fixup: each split CTA writes its partial, the last reads them
-      if (cost < best) { best = cost; nsplit = n; }
+    static const double v128[3] = {0.0, 0.676, 1.0}, v64[4] = {0.0, 0.62, 0.90, 0.951};
+    auto cost = [&](int w_tn, int n) {
+      const int S = w_tn == 128 ? 2 : 3;
+      const int64_t units = (c->Mp / kTile) * (c->P / w_tn) * n;
+      const double w = (w_tn / 128.0) * ((double)kstages / n + 1.5 + (n > 1 ? 0.2 * n : 0.0));
+      double t = 0.0;
+      for (int64_t left = units; left > 0;) {
+        const int64_t u = std::min<int64_t>(left, (int64_t)sms * S);
+        left -= u;
+        const int L = (int)((u + sms - 1) / sms);
+        t += L * w / (w_tn == 128 ? v128[L] : v64[L]);
+      }
+      if (w_tn == 128 && n == 1 && kstages >= 128 && g_gemm_tma == 1) t *= 0.99;
+      return t;
+    };
+    double best = -1.0;
+    for (int w_tn : {128, 64}) {
+      if (g_gemm_tile && w_tn != g_gemm_tile) continue;
+      for (int n = 1; n <= 8 && (n == 1 || kstages >= 2 * n); ++n) {
+        if (g_split_k_off && n > 1) break;
+        if (g_split_force && n != std::min<int64_t>(g_split_force, std::max<int64_t>(1, kstages / 2))) continue;
+        const double t = cost(w_tn, n);
+        if (best < 0.0 || t < best) { best = t; tn = w_tn; nsplit = n; }
+      }
     }
-    if (g_split_k_off) { nsplit = 1; best = cost1; }
-    if (g_split_force) { nsplit = (int)std::min<int64_t>(g_split_force, std::max<int64_t>(1, kstages / 2)); best = 0.0; }
+    const int64_t slots = 2 * (int64_t)sms;
+    const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
     if (g_stream_k && rem > 0) {
+      const double t_stage = 8.2e-6, bw = 6.0e12, tile_bytes = 4.0 * kTile * kTile / 2;
       const int64_t R = rem * kstages;
       const int nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, R / 4));   // >= 4 stages each
       const double per = (double)((R + nsk - 1) / nsk);
       const double segs = std::min(3.0, 1.0 + per / (double)kstages + 1.0);
-      double cost = (double)full_waves * ((double)kstages + 2.0) + per + 2.0 * segs;
-      cost += (double)rem * tile_bytes * (segs + 2 + epi.nprev) / bw / t_stage;
-      if (g_stream_k == 2 || cost < best) { best = cost; nsplit = 1; sk_nfull = (int)(full_waves * slots); sk_nsk = nsk; }
+      double t = (double)full_waves * ((double)kstages + 1.5) + per + 2.0 * segs;
+      t += (double)rem * tile_bytes * (segs + 2 + epi.nprev) / bw / t_stage;
+      if (g_stream_k == 2 || t < best) {
+        nsplit = 1; tn = 128; sk_nfull = (int)(full_waves * slots); sk_nsk = nsk;
+      }
     }
-    if (best > 0.97 * cost1 && g_stream_k != 2) { nsplit = 1; sk_nsk = 0; sk_nfull = 0; }
   }
   const TmaOps *tma = nullptr;
-  if (g_gemm_tma == 2 || (g_gemm_tma == 1 && nsplit == 1 && kstages >= 128)) {
+  if (tn == 128 && (g_gemm_tma == 2 || (g_gemm_tma == 1 && nsplit == 1 && kstages >= 128))) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
     tma = &c->tma;
@@ -2625,7 +2635,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     RD_CUDA_CHECK(cudaGetLastError());
   } else if (nsplit == 1) {
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st, 1, tma);
+                                     c->N, c->Mp, c->P, epi, c->st, 1, tma, tn);
     if (rc != RD_OK) return rc;
   } else {
     // split-K with the in-kernel fixup: partial tiles in c->ws, the last CTA of each tile folds
@@ -2645,7 +2655,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     epi.split_ws = c->ws;
     epi.split_cnt = c->tile_cnt;
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st, nsplit, tma);
+                                     c->N, c->Mp, c->P, epi, c->st, nsplit, tma, tn);
     if (rc != RD_OK) return rc;
   }
   c->k = knew;

@@ -1107,7 +1107,7 @@ def test_tile64_chain_equals_oracle(variant):
                 assert s[0] == min(int(min(P[k][i, i] for i in range(r0, r1))), RINF)
             ch.close()
     finally:
-        rd.rd_set_gemm_tile(128)
+        rd.rd_set_gemm_tile(0)
         rd.rd_set_gemm_variant(3)
         rd.rd_set_split_k(True)
 
@@ -1135,4 +1135,4 @@ def test_forced_split_k_fixup_equals_oracle(tn):
                     assert (a == b).all(), (m, n)
     finally:
         rd.rd_set_split_k(1)
-        rd.rd_set_gemm_tile(128)
+        rd.rd_set_gemm_tile(0)

@@ -7,7 +7,7 @@ O=gpurun_out
 mkdir -p $O
 python -m paper_2409_17658_b200.build > $O/${TAG}_build.log 2>&1
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
-  timeout 1200 python -m pytest tests -m gpu -q -x > $O/${TAG}_pytest_gpu.log 2>&1
+  timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > $O/${TAG}_pytest_gpu.log 2>&1
   echo "pytest rc=$?"; tail -3 $O/${TAG}_pytest_gpu.log
   timeout 300 python __graft_entry__.py > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
 fi
@@ -25,4 +25,7 @@ echo "launches rc=$?"
 $CMD > $O/${TAG}_plain2.log 2>&1 &&
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:minplus_gemm -s 1 -c 1 -o $O/${TAG}_gemm $CMD > $O/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:panel_stats -s 2 -c 1 -o $O/${TAG}_panel_stats python tools/time_panel_stats.py > $O/${TAG}_ncu_ps.log 2>&1
+echo "ps full rc=$?"
+timeout 1200 python tools/wave_probe.py > $O/${TAG}_wave.txt 2>&1; echo "wave rc=$?"
 cat $O/${TAG}_bench.json; cat $O/${TAG}_bench_ref.json

@@ -40,7 +40,7 @@ for m, parts in cases:
         res[name] = med(m, r0, r1, reps=10 if m < 9 else 3)
     rd.rd_set_split_k(True)
     rd.rd_set_stream_k(0)
-    rd.rd_set_gemm_tile(128)
+    rd.rd_set_gemm_tile(0)
     rd.rd_set_gemm_tma(1)
     terms = (r1 - r0) * N * N
     print(f"m={m} p={parts} rows=[{r0},{r1}) " + "  ".join(f"{k} {v:.4f} ms ({terms / v / 1e9:.1f} T)" for k, v in res.items()),

@@ -38,7 +38,7 @@ for m, parts in cases:
         for n in (1, 2, 3, 4):
             rd.rd_set_split_k(0 if n == 1 else n)
             res[f"t{tn}/s{n}"] = med(m, r0, r1, reps=10 if m < 9 else 3)
-    rd.rd_set_gemm_tile(128)
+    rd.rd_set_gemm_tile(0)
     rd.rd_set_gemm_tma(1)
     rd.rd_set_split_k(1)
     res["default"] = med(m, r0, r1, reps=10 if m < 9 else 3)
