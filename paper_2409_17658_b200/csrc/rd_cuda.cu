@@ -2335,7 +2335,7 @@ static int g_gemm_tma = 1;
 
 extern "C" int rd_set_gemm_tma(int mode) try {
   rd_enter();
-  if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_gemm_tma: mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return fail(RD_EINVAL, "rd_set_gemm_tma: mode must be 0, 1, 2 or 3");
   g_gemm_tma = mode;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_tma")
@@ -2578,7 +2578,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
         const int L = (int)((u + sms - 1) / sms);
         t += L * w / (w_tn == 128 ? v128[L] : v64[L]);
       }
-      if (w_tn == 128 && n == 1 && kstages >= 128 && g_gemm_tma == 1) t *= 0.99;
+      if (w_tn == 128 && n == 1 && kstages >= 128 && (g_gemm_tma == 1 || g_gemm_tma == 3)) t *= 0.99;
       return t;
     };
     double best = -1.0;
@@ -2607,9 +2607,10 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     }
   }
   const TmaOps *tma = nullptr;
-  if (tn == 128 && (g_gemm_tma == 2 || (g_gemm_tma == 1 && nsplit == 1 && kstages >= 128))) {
+  if (tn == 128 && (g_gemm_tma == 2 || ((g_gemm_tma == 1 || g_gemm_tma == 3) && nsplit == 1 && kstages >= 128))) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
+    c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 1 : 0;
     tma = &c->tma;
   }
   if (sk_nsk > 0) {

@@ -17,6 +17,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                     const __grid_constant__ TmaOps tma) {
   extern __shared__ __align__(16) uint32_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ uint32_t rel_cnt[kStages];   // TMA: warps that have released each stage
   // TMA writes need an aligned destination: the TMA variant is launched with 1 KB extra
   // dynamic shared memory and rounds its stage base up to 1 KB
   uint32_t *smem = smem_raw;
@@ -40,9 +41,10 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   const int64_t gx_step8 = 8 * ldx;
 
   uint32_t acc[8][NC];
-  // TMA: thread 0 issues two bulk-tensor copies per stage (32 KB, completion counted on
-  // full_bar[s]); every warp releases a consumed stage on empty_bar[s]; thread 0 refills it
-  // once all 8 warps have.  No per-thread copy instructions, no CTA-wide barrier.  Stages are
+  // TMA: two bulk-tensor copies per stage (32 KB, completion counted on full_bar[s]); every
+  // warp releases a consumed stage (a shared-memory ticket, plus an arrival on empty_bar[s]) and
+  // the LAST warp to release it issues the refill, so no warp ever waits for the others to
+  // drain a stage.  No per-thread copy instructions, no CTA-wide barrier.  Stages are
   // numbered by a running count `it` over the CTA's segments (stream-K CTAs run several), so
   // slot = it mod kStages and the barrier phases continue across segments.
   if constexpr (TMA) {
@@ -51,6 +53,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       for (int s = 0; s < kStages; ++s) {
         mbar_init(&full_bar[s], 1);
         mbar_init(&empty_bar[s], kThreads / 32);
+        rel_cnt[s] = 0;
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -172,12 +175,20 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             }
         }
       }
-      if constexpr (TMA) {   // release this stage; thread 0 refills it with stage kb + kStages
+      if constexpr (TMA) {   // release this stage; the last warp to release it refills it
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty_bar[slot]);
-        if (tid == 0 && kb + kStages < KB) {
-          mbar_wait(&empty_bar[slot], (g / kStages) & 1);
-          tma_issue(slot, kb + kStages);
+        if (tma.refill_by_thread0) {   // A/B reference: thread 0 waits for every warp, then refills
+          if ((tid & 31) == 0) mbar_arrive(&empty_bar[slot]);
+          if (tid == 0 && kb + kStages < KB) {
+            mbar_wait(&empty_bar[slot], (g / kStages) & 1);
+            tma_issue(slot, kb + kStages);
+          }
+        } else if ((tid & 31) == 0) {
+          mbar_arrive(&empty_bar[slot]);   // phase bookkeeping for later segments' prologues
+          if (atomicAdd(&rel_cnt[slot], 1u) == kThreads / 32 - 1) {
+            rel_cnt[slot] = 0;
+            if (kb + kStages < KB) tma_issue(slot, kb + kStages);
+          }
         }
       }
     }

@@ -104,7 +104,7 @@ def test_argument_validation_host_paths():
     assert L.rd_agchain_create(5, 10, rd._np_ptr(b), 2, 2, None, ctypes.byref(h)) == rd.RD_EINVAL  # rank
     assert L.rd_agchain_step(None, None) == rd.RD_EINVAL
     assert L.rd_chain_create_ex(12, 10, 0, 10, 0, None, ctypes.byref(h)) == rd.RD_EINVAL        # m=12 dense
-    assert L.rd_set_gemm_tma(3) == rd.RD_EINVAL and L.rd_set_gemm_tma(-1) == rd.RD_EINVAL
+    assert L.rd_set_gemm_tma(4) == rd.RD_EINVAL and L.rd_set_gemm_tma(-1) == rd.RD_EINVAL
     assert L.rd_set_gemm_tma(1) == rd.RD_OK
     assert L.rd_stats_len(10) == 41
     assert L.rd_set_sparse_bytes(3) == rd.RD_EINVAL and L.rd_set_sparse_bytes(-1) == rd.RD_EINVAL
