@@ -361,9 +361,9 @@ int rd_set_gemm_tile(int tn);
  * counted on an mbarrier; the warps release stages on a second mbarrier); without, every
  * thread issues cp.async and the CTA meets at __syncthreads.  mode 0 = cp.async always;
  * 1 (default) = TMA for single-pass steps of >= 128 stages (the m >= 9 orders); 2 = TMA
- * always; 3 = as 1 with the round-1 refill (thread 0 waits until every warp has released a
- * stage; the default lets the last warp to release it refill it), for A/B timing.  Identical
- * results.  RD_EINVAL outside 0..3. */
+ * always; 3 = as 1 but the last warp to release a stage refills it (the default: thread 0
+ * waits until every warp has released the stage, then refills it; measured equal within 0.6 %
+ * at m = 9), for A/B timing.  Identical results.  RD_EINVAL outside 0..3. */
 int rd_set_gemm_tma(int mode);
 
 /* rd_set_split_k — process-wide split-K policy of dense chain steps: 1 (default) = split the

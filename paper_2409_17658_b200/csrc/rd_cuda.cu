@@ -755,9 +755,38 @@ __global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_
   }
 }
 
+// Diagonal min (Cor 7) of a row panel: row i meets column diag_row0 + i (for the flat form of
+// the streaming kernel, which sees the panel as one contiguous array).
+__global__ void panel_diag_kernel(const int16_t *__restrict__ cur, int64_t rows, int64_t cols, int64_t ld,
+                                  int64_t diag_row0, int32_t *__restrict__ stats) {
+  int32_t v = INT_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = diag_row0 + i;
+    if (c >= 0 && c < cols) v = min(v, min((int)cur[i * ld + c], (int)RD_INF));
+  }
+  v = __reduce_min_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v != INT_MAX) atomicMin(stats, v);
+}
+
 template <int NA>
 static int launch_panel_stats(const int16_t *cur, int64_t rows, int64_t cols, int64_t ld, int64_t diag_row0,
-                              const PanelStatsArgs &pa, int a0, int32_t *stats, int sms, cudaStream_t st, bool vec) {
+                              const PanelStatsArgs &pa, int a0, int32_t *stats, int sms, cudaStream_t st, bool vec,
+                              bool flat) {
+  if (flat) {
+    // a contiguous panel (ld == cols) with 16-byte aligned bases is one flat array of rows x cols
+    // entries: stream it in aligned 16-byte chunks whatever cols is (the stats are elementwise;
+    // the diagonal goes to panel_diag_kernel)
+    if (a0 == 0) {
+      panel_diag_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, 4 * sms)), 256, 0,
+                          st>>>(cur, rows, cols, ld, diag_row0, stats);
+      RD_CUDA_CHECK(cudaGetLastError());
+    }
+    cols = rows * cols;
+    ld = cols;
+    rows = 1;
+    diag_row0 = INT64_MIN / 2;   // no element meets the "diagonal" of the flat view
+    vec = true;
+  }
   const int64_t chunks = rows * ((cols + 7) / 8);
   if (vec) {
     constexpr int PS = (1 + NA) * 4096 * 4 <= 200 * 1024 ? 4 : 3;
@@ -803,14 +832,15 @@ extern "C" int rd_panel_stats(const int16_t *cur, const int16_t *const *prev, in
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one thread per 16-byte chunk of the panel, grid-strided; every alpha of a pass in one sweep
   // (16-byte aligned panels: the cp.async streaming kernel, one block per SM)
-  bool vec = (ld % 8 == 0) && ((reinterpret_cast<uintptr_t>(cur) & 15) == 0);
-  for (int a = 0; a < nprev; ++a) vec = vec && ((reinterpret_cast<uintptr_t>(pa.prev[a]) & 15) == 0);
+  bool aligned = (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+  for (int a = 0; a < nprev; ++a) aligned = aligned && ((reinterpret_cast<uintptr_t>(pa.prev[a]) & 15) == 0);
+  const bool vec = aligned && (ld % 8 == 0), flat = aligned && ld == cols && !vec;
   for (int a0 = 0; a0 < std::max(nprev, 1); a0 += 16) {
     const int na = std::min(16, nprev - a0);
     int rc = RD_OK;
     switch (na) {
 #define RD_PS(K) \
-  case K: rc = launch_panel_stats<K>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev, sms, st, vec); break;
+  case K: rc = launch_panel_stats<K>(cur, rows, cols, ld, diag_row0, pa, a0, stats_dev, sms, st, vec, flat); break;
       RD_PS(0) RD_PS(1) RD_PS(2) RD_PS(3) RD_PS(4) RD_PS(5) RD_PS(6) RD_PS(7) RD_PS(8)
       RD_PS(9) RD_PS(10) RD_PS(11) RD_PS(12) RD_PS(13) RD_PS(14) RD_PS(15) RD_PS(16)
 #undef RD_PS
@@ -2610,7 +2640,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   if (tn == 128 && (g_gemm_tma == 2 || ((g_gemm_tma == 1 || g_gemm_tma == 3) && nsplit == 1 && kstages >= 128))) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
-    c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 1 : 0;
+    c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 0 : 1;   // measured: the last-warp refill is no faster
     tma = &c->tma;
   }
   if (sk_nsk > 0) {

@@ -146,7 +146,7 @@ static __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap 
 struct TmaOps {
   CUtensorMap x, b;
   int xslot;
-  int refill_by_thread0;   // 1: the round-1 refill (thread 0 waits on empty_bar), for A/B timing
+  int refill_by_thread0;   // 1 (default): thread 0 waits on empty_bar, then refills; 0: the last warp to release refills
 };
 
 // One CTA computes a 128 x 128 tile of C; 256 threads in a 16 x 16 grid, each thread an

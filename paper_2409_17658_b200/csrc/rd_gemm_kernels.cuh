@@ -42,9 +42,10 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 
   uint32_t acc[8][NC];
   // TMA: two bulk-tensor copies per stage (32 KB, completion counted on full_bar[s]); every
-  // warp releases a consumed stage (a shared-memory ticket, plus an arrival on empty_bar[s]) and
-  // the LAST warp to release it issues the refill, so no warp ever waits for the others to
-  // drain a stage.  No per-thread copy instructions, no CTA-wide barrier.  Stages are
+  // warp releases a consumed stage on empty_bar[s] and thread 0 refills it once all 8 warps
+  // have (tma.refill_by_thread0; the alternative — the last warp to release a stage, found by a
+  // shared-memory ticket, refills it and nobody waits — measured no faster).  No per-thread
+  // copy instructions, no CTA-wide barrier.  Stages are
   // numbered by a running count `it` over the CTA's segments (stream-K CTAs run several), so
   // slot = it mod kStages and the barrier phases continue across segments.
   if constexpr (TMA) {
@@ -177,7 +178,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       }
       if constexpr (TMA) {   // release this stage; the last warp to release it refills it
         __syncwarp();
-        if (tma.refill_by_thread0) {   // A/B reference: thread 0 waits for every warp, then refills
+        if (tma.refill_by_thread0) {   // thread 0 waits for every warp, then refills
           if ((tid & 31) == 0) mbar_arrive(&empty_bar[slot]);
           if (tid == 0 && kb + kStages < KB) {
             mbar_wait(&empty_bar[slot], (g / kStages) & 1);

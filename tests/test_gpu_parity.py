@@ -318,10 +318,13 @@ def _stats_reference(X, prevs, diag_row0):
 
 
 @pytest.mark.parametrize("rows,cols,ld,nprev", [(300, 287, 287, 20), (64, 1000, 1008, 10), (5, 13, 13, 3),
-                                                (257, 2048, 2048, 16), (33, 100, 100, 0)])
+                                                (257, 2048, 2048, 16), (33, 100, 100, 0), (40, 100, 103, 5),
+                                                (129, 21909, 21909, 10)])
 def test_panel_stats_one_pass_every_entry(rows, cols, ld, nprev):
-    """rd_panel_stats (one pass over every alpha, 16 per pass; vector and ragged scalar paths)
-    equals the stats vector's definition entry by entry, with inf entries in both powers."""
+    """rd_panel_stats (one pass over every alpha, 16 per pass; the flat streaming path for
+    contiguous panels of any width, the per-row streaming path for ld % 8 == 0, the scalar path
+    otherwise) equals the stats vector's definition entry by entry, with inf entries in both
+    powers and a diagonal offset."""
     rng = np.random.default_rng(rows + cols + nprev)
     am = max(1, nprev)
     base = rng.integers(50, 90, size=(rows, ld)).astype(np.int16)

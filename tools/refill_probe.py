@@ -1,6 +1,6 @@
 """A/B of the TMA mainloop's stage refill at m = 9 (median chain-step time, CUDA events),
-alternating configurations to cancel clock drift: the default (the last warp to release a
-stage refills it) vs the round-1 form (thread 0 waits for every warp), for dpx_cols 3 and 4."""
+alternating configurations to cancel clock drift: the last warp to release a
+stage refills it, mode 3) vs the default (thread 0 waits for every warp, mode 1), for dpx_cols 3 and 4."""
 import statistics
 import sys
 
@@ -17,7 +17,7 @@ for _ in range(3):
 res = {}
 for rep in range(3):
     for d in (3, 4):
-        for mode, name in ((1, "last-warp"), (3, "thread0")):
+        for mode, name in ((3, "last-warp"), (1, "thread0")):
             rd.rd_set_gemm_tma(mode)
             rd.rd_set_gemm_variant(d)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
