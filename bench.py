@@ -427,7 +427,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
     if rank == 0 and not args.no_e2e:
         g = torch.Generator(device=dev).manual_seed(0)
         cur = torch.randint(100, 140, (N, N), dtype=torch.int16, device=dev, generator=g)
-        prevs = [torch.randint(60 + 4 * a, 100, (N, N), dtype=torch.int16, device=dev, generator=g)
+        prevs = [torch.randint(40 + 2 * a, 100, (N, N), dtype=torch.int16, device=dev, generator=g)
                  for a in range(am)]
         sr = torch.empty(rd.rd_stats_len(am), dtype=torch.int32, device=dev)
         med, best = timed(lambda: rd.rd_panel_stats(cur, prevs, 0, am, sr, stream=stream))

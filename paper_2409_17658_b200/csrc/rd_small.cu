@@ -53,6 +53,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 // arrive resets the count and bumps the generation; the others spin on the generation.
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
   __syncthreads();
+  if (gridDim.x == 1) return;   // one CTA (m <= 3): the block barrier orders its global writes
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned g = gen;

@@ -1,0 +1,10 @@
+set -u
+O=gpurun_out
+mkdir -p $O
+python -m paper_2409_17658_b200.build > $O/s10_build.log 2>&1; echo "build rc=$?"
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "small_chain or panel_stats" > $O/s10_pytest.log 2>&1
+echo "pytest rc=$?"; tail -2 $O/s10_pytest.log
+timeout 300 python tools/time_panel_stats.py 0 1 2 4 10 16 > $O/s10_panel_stats.txt 2>&1; cat $O/s10_panel_stats.txt
+timeout 300 python tools/small_m_latency.py 3 4 5 6 > $O/s10_small.txt 2>&1; cat $O/s10_small.txt
+timeout 600 ncu --set full --clock-control none -k regex:panel_stats -s 2 -c 1 -o $O/s10_panel_stats python tools/time_panel_stats.py 10 > $O/s10_ncu_ps.log 2>&1; echo "ncu rc=$?"
+timeout 900 python tools/hash_repro.py 1 3 > $O/s10_hash.txt 2>&1; cat $O/s10_hash.txt | cut -c1-400

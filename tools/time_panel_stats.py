@@ -11,7 +11,7 @@ N = 21909
 alphas = [int(a) for a in sys.argv[1:]] or [10]
 g = torch.Generator(device="cuda").manual_seed(0)
 cur = torch.randint(100, 140, (N, N), dtype=torch.int16, device="cuda", generator=g)
-prevs = [torch.randint(60 + 4 * a, 100, (N, N), dtype=torch.int16, device="cuda", generator=g) for a in range(max(alphas))]
+prevs = [torch.randint(40 + 2 * a, 100, (N, N), dtype=torch.int16, device="cuda", generator=g) for a in range(max(alphas))]
 for am in alphas:
     s = torch.empty(rd.rd_stats_len(max(am, 1)), dtype=torch.int32, device="cuda")
     for _ in range(3):
