@@ -663,14 +663,13 @@ __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, i
   asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes));
 }
 
-template <int NA, int PS>
-__global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_t *__restrict__ cur, int64_t rows,
-                                                                  int64_t cols, int64_t ld, int64_t diag_row0,
-                                                                  PanelStatsArgs pa, int a0,
-                                                                  int32_t *__restrict__ stats) {
-  constexpr int NR = NA > 0 ? NA : 1;
-  extern __shared__ uint4 sbuf[];   // [PS][1 + NA][256]
-  __shared__ int32_t red[8][1 + 4 * NR];
+template <int NA, int PS, int T>
+__global__ void __launch_bounds__(T, 1) panel_stats_stream_kernel(const int16_t *__restrict__ cur, int64_t rows,
+                                                                int64_t cols, int64_t ld, int64_t diag_row0,
+                                                                PanelStatsArgs pa, int a0, int32_t *__restrict__ stats) {
+  constexpr int NR = NA > 0 ? NA : 1, NW = T / 32;
+  extern __shared__ uint4 sbuf[];   // [PS][1 + NA][T]
+  __shared__ int32_t red[NW][1 + 4 * NR];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int32_t dmin = INT_MAX;
   uint32_t lo2[NR], hi2[NR], mis[NR], fin[NR];
@@ -679,30 +678,43 @@ __global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_
   const int16_t *pp[NR];
 #pragma unroll
   for (int a = 0; a < NA; ++a) pp[a] = pa.prev[a0 + a];
+  // chunk v = (row i, column chunk jc); a thread walks v = v0, v0 + gs, ... with (i, jc) kept
+  // incrementally (no divisions in the loop): one cursor for the loads, one for the folds
   const int64_t cpr = (cols + 7) / 8, total = rows * cpr;
-  const int64_t gs = (int64_t)gridDim.x * blockDim.x, v0 = (int64_t)blockIdx.x * blockDim.x + tid;
-  auto slot = [&](int st, int arr) -> uint4 * { return &sbuf[(st * (1 + NA) + arr) * 256 + tid]; };
-  auto issue = [&](int st, int64_t v) {
-    if (v < total) {
-      const int64_t i = v / cpr, j = (v - i * cpr) * 8, off = i * ld + j;
+  const int64_t gs = (int64_t)gridDim.x * T, v0 = (int64_t)blockIdx.x * T + tid;
+  const int64_t gs_q = gs / cpr, gs_r = gs - gs_q * cpr;
+  struct Cursor {
+    int64_t v, i, jc;
+  };
+  auto advance = [&](Cursor &c) {
+    c.v += gs;
+    c.i += gs_q;
+    c.jc += gs_r;
+    if (c.jc >= cpr) { c.jc -= cpr; ++c.i; }
+  };
+  Cursor ld_c{v0, v0 / cpr, v0 - (v0 / cpr) * cpr}, cs = ld_c;
+  auto slot = [&](int st, int arr) -> uint4 * { return &sbuf[(st * (1 + NA) + arr) * T + tid]; };
+  auto issue = [&](int st) {
+    if (ld_c.v < total) {
+      const int64_t j = ld_c.jc * 8, off = ld_c.i * ld + j;
       const int bytes = j + 8 <= cols ? 16 : (int)(cols - j) * 2;
       cp_async16_zfill(slot(st, 0), cur + off, bytes);
 #pragma unroll
       for (int a = 0; a < NA; ++a) cp_async16_zfill(slot(st, 1 + a), pp[a] + off, bytes);
     }
     cp_async_commit();
+    advance(ld_c);
   };
 #pragma unroll
-  for (int st = 0; st < PS - 1; ++st) issue(st, v0 + st * gs);
-  for (int64_t it = 0;; ++it) {
-    const int64_t v = v0 + it * gs;
-    if (v >= total) break;
-    issue((int)((it + PS - 1) % PS), v + (PS - 1) * gs);
+  for (int st = 0; st < PS - 1; ++st) issue(st);
+  int st_ld = PS - 1, st = 0;
+  for (; cs.v < total; advance(cs)) {
+    issue(st_ld);
+    st_ld = st_ld + 1 == PS ? 0 : st_ld + 1;
     cp_async_wait<PS - 1>();
-    const int st = (int)(it % PS);
-    const int64_t i = v / cpr, j = (v - i * cpr) * 8;
+    const int64_t j = cs.jc * 8;
     // lanes past the row's end (zero-filled) become +inf in both powers: neutral in the stats
-    uint4 x = *slot(st, 0);
+    const uint4 x = *slot(st, 0);
     uint32_t o[4] = {x.x, x.y, x.z, x.w};
     uint32_t padw[4] = {0, 0, 0, 0};
     if (j + 8 > cols) {
@@ -710,10 +722,14 @@ __global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_
       for (int q = 0; q < 4; ++q)
         padw[q] = (j + 2 * q < cols ? 0u : 0x0000FFFFu) | (j + 2 * q + 1 < cols ? 0u : 0xFFFF0000u);
     }
+    uint32_t io = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = __vminu2(o[q] | padw[q], kInf2);
+    for (int q = 0; q < 4; ++q) {
+      o[q] = __vminu2(o[q] | padw[q], kInf2);
+      io |= __vcmpeq2(o[q], kInf2);
+    }
     if (a0 == 0) {
-      const int64_t gi = diag_row0 + i;
+      const int64_t gi = diag_row0 + cs.i;
       if (gi >= j && gi < j + 8 && gi < cols) {
         const int t = (int)(gi - j);
         dmin = min(dmin, (int)((o[t >> 1] >> (16 * (t & 1))) & 0xFFFF));
@@ -722,10 +738,27 @@ __global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_
 #pragma unroll
     for (int a = 0; a < NA; ++a) {
       const uint4 y = *slot(st, 1 + a);
-      const uint32_t w[4] = {y.x, y.y, y.z, y.w};
+      uint32_t w[4] = {y.x, y.y, y.z, y.w};
+      uint32_t iw = io;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) stats_pair(o[q], __vminu2(w[q] | padw[q], kInf2), lo2[a], hi2[a], mis[a], fin[a]);
+      for (int q = 0; q < 4; ++q) {
+        w[q] = __vminu2(w[q] | padw[q], kInf2);
+        iw |= __vcmpeq2(w[q], kInf2);
+      }
+      if (iw == 0) {   // every lane finite in both powers (every entry from k = 4 on)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t d = __vsub2(o[q], w[q]);
+          lo2[a] = __vmins2(lo2[a], d);
+          hi2[a] = __vmaxs2(hi2[a], d);
+        }
+        fin[a] = 0xFFFFFFFFu;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) stats_pair(o[q], w[q], lo2[a], hi2[a], mis[a], fin[a]);
+      }
     }
+    st = st + 1 == PS ? 0 : st + 1;
   }
   cp_async_wait<0>();
   dmin = __reduce_min_sync(0xffffffffu, dmin);
@@ -743,10 +776,10 @@ __global__ void __launch_bounds__(256, 1) panel_stats_stream_kernel(const int16_
     }
   }
   __syncthreads();
-  for (int e = tid; e < 1 + 4 * NA; e += blockDim.x) {
+  for (int e = tid; e < 1 + 4 * NA; e += T) {
     int32_t v = red[0][e];
 #pragma unroll
-    for (int w2 = 1; w2 < 8; ++w2) v = min(v, red[w2][e]);
+    for (int w2 = 1; w2 < NW; ++w2) v = min(v, red[w2][e]);
     if (e == 0) {
       if (a0 == 0) atomicMin(stats, v);
     } else {
@@ -789,18 +822,22 @@ static int launch_panel_stats(const int16_t *cur, int64_t rows, int64_t cols, in
   }
   const int64_t chunks = rows * ((cols + 7) / 8);
   if (vec) {
-    constexpr int PS = (1 + NA) * 4096 * 4 <= 200 * 1024 ? 4 : 3;
-    constexpr int smem = PS * (1 + NA) * 4096;
+    // 512 threads (16 warps) and 2-4 stages while the stage buffers fit 200 KB; 256 threads and
+    // 3 stages for the widest passes
+    constexpr int T = (1 + NA) * 8192 * 2 <= 200 * 1024 ? 512 : 256;
+    constexpr int PS0 = (220 * 1024) / ((1 + NA) * 16 * T);
+    constexpr int PS = PS0 > 4 ? 4 : (PS0 < 2 ? 2 : PS0);
+    constexpr int smem = PS * (1 + NA) * 16 * T;
     static bool attr[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr[dev]) {
-      RD_CUDA_CHECK(cudaFuncSetAttribute(panel_stats_stream_kernel<NA, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem));
+      RD_CUDA_CHECK(cudaFuncSetAttribute(panel_stats_stream_kernel<NA, PS, T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr[dev] = true;
     }
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms));
-    panel_stats_stream_kernel<NA, PS><<<grid, 256, smem, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + T - 1) / T, (int64_t)sms));
+    panel_stats_stream_kernel<NA, PS, T><<<grid, T, smem, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats);
   } else {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)sms * 4));
     panel_stats_kernel<NA><<<grid, 256, 0, st>>>(cur, rows, cols, ld, diag_row0, pa, a0, stats);
