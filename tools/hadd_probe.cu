@@ -1,0 +1,129 @@
+// Register-tile probe of the fp16-encoded (min,+) forms (not part of the product; informs the
+// mainloop mix).  Entries <= 2048 are exact fp16 integers and positive fp16 bit
+// patterns order like unsigned 16-bit integers, so s = HADD2(x, b) (fma pipe) and a 3-input
+// unsigned 16-bit min VIMNMX3.U16x2 (alu) fold two k-pairs into an accumulator of fp16 bits.
+// The question is whether HADD2/HFMA2 issue at twice IMAD's rate (both fma sub-pipes).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o hadd_probe hadd_probe.cu
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#define OPQ(x) asm volatile("" : "+r"(x))
+
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+// FORM 0: independent IMAD chains (packed int add via x*one+b)   -> instr/clk
+// FORM 1: independent HADD2 chains                                  -> instr/clk
+// FORM 2: independent FFMA chains                                   -> instr/clk
+// FORM 3: GEMM 8x8 tile, every column [2 HADD2 + VIMNMX3.U16x2]     -> terms/clk
+// FORM 4: GEMM 8x8 tile, d=3 DPX + 5 x [2 IMAD + VIMNMX3] (today's mix)
+// FORM 5: GEMM 8x8 tile, 4 x [2 IMAD + VIMNMX3] + 4 x [2 HADD2 + VIMNMX3]
+template <int FORM>
+__global__ void __launch_bounds__(256, 2) probe(uint32_t *sink, long long *cyc, int iters, uint32_t one) {
+  long long t0 = 0, t1 = 0;
+  uint32_t h = 0;
+  if (FORM <= 2) {
+    uint32_t c[32], a0[4], b0[8];
+    const uint32_t s = (one ^ threadIdx.x) & 0x000F000Fu;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a0[q] = 0x3C003C00u + s + q;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b0[q] = 0x3C003C00u + s + 3 * q;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) c[u] = 0x10001000u + u;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) OPQ(a0[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) OPQ(b0[q]);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        if (FORM == 0) c[u] = a0[u >> 3] * one + c[u];
+        else if (FORM == 1) c[u] = hadd2(b0[u & 7], c[u]);
+        else c[u] = __float_as_uint(fmaf(__uint_as_float(a0[u >> 3]), __uint_as_float(b0[u & 7]), __uint_as_float(c[u])));
+      }
+    }
+    t1 = clock64();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) h ^= c[u];
+  } else {
+    uint32_t acc[8][8], x0[8], x1[8], b0[8], b1[8];
+    const uint32_t s = threadIdx.x * 0x00010001u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { x0[i] = s + i; x1[i] = s + 2 * i; b0[i] = s + 3 * i; b1[i] = s + 5 * i; }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0x3FFF3FFFu;
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { OPQ(x0[i]); OPQ(x1[i]); OPQ(b0[i]); OPQ(b1[i]); }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (FORM == 4 && c < 3) {
+            acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+            acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+          } else if (FORM == 3 || (FORM == 5 && c >= 4)) {
+            acc[r][c] = __vimin3_u16x2(acc[r][c], hadd2(x0[r], b0[c]), hadd2(x1[r], b1[c]));
+          } else {
+            acc[r][c] = __vimin3_s16x2(acc[r][c], x0[r] * one + b0[c], x1[r] * one + b1[c]);
+          }
+        }
+    }
+    t1 = clock64();
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) h ^= acc[r][c];
+  }
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = h;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int FORM>
+void run(int sms, const char *name) {
+  const int blocks = sms * 2, threads = 256, iters = FORM <= 2 ? 8192 : 2000;
+  uint32_t *sink;
+  long long *cyc;
+  cudaMalloc(&sink, blocks * threads * 4);
+  cudaMalloc(&cyc, blocks * 8);
+  probe<FORM><<<blocks, threads>>>(sink, cyc, 16, 1);
+  probe<FORM><<<blocks, threads>>>(sink, cyc, iters, 1);
+  cudaDeviceSynchronize();
+  long long *h = new long long[blocks];
+  cudaMemcpy(h, cyc, blocks * 8, cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int b = 0; b < blocks; ++b) mx = h[b] > mx ? h[b] : mx;
+  if (FORM <= 2) {
+    const double ipc = (double)iters * 32 * (threads / 32) * 2 / (double)mx;
+    printf("%-44s %.3f warp-instr/clk/SM\n", name, ipc);
+  } else {
+    const double t = (double)iters * 256.0 * threads * 2 / (double)mx;
+    printf("%-44s %.1f (min,+) terms/clk/SM\n", name, t);
+  }
+  delete[] h;
+  cudaFree(sink);
+  cudaFree(cyc);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<0>(sms, "IMAD packed add (independent)");
+  run<1>(sms, "HADD2 (independent)");
+  run<2>(sms, "FFMA (independent)");
+  run<3>(sms, "8x8 tile: all [2 HADD2 + VIMNMX3.U16x2]");
+  run<4>(sms, "8x8 tile: 3 DPX + 5 [2 IMAD + VIMNMX3] (GEMM)");
+  run<5>(sms, "8x8 tile: 4 [IMAD] + 4 [HADD2] groups");
+  return 0;
+}
