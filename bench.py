@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 37751291136}   # profiles/r01r_gemm_ncu_summary.txt (TMA mainloop, final code): 36.676 GB read + 1.075 GB write
+TRAFFIC = {9: 37686883000}   # profiles/r02b_gemm_ncu_summary.txt (TMA mainloop): 36.583 GB read + 1.104 GB write
 
 
 def parse():
@@ -461,8 +461,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             nn = rd.count_words(mm)
-            ttp[str(mm)] = {"build_s": round(float(tt[0]), 4), "chain_s": round(float(tt[1]), 4),
-                            "total_s": round(float(tt[0] + tt[1]), 4), "k_stop": res["k_stop"],
+            ttp[str(mm)] = {"build_s": round(float(tt[0]), 6), "chain_s": round(float(tt[1]), 6),
+                            "total_s": round(float(tt[0] + tt[1]), 6), "k_stop": res["k_stop"],
                             "triple": [res["n0"], res["alpha"], res["beta"]],
                             "chain_gops": round((res["k_stop"] - 1) * float(nn) ** 3 / float(tt[1]) / 1e9, 1)}
             # the structured step (NEXT-3: finite terms of the sparse right operand only),
@@ -475,8 +475,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
             if world > 1:
                 dist.all_reduce(ts, op=dist.ReduceOp.MAX)
             assert (rs["n0"], rs["alpha"], rs["beta"]) == (res["n0"], res["alpha"], res["beta"])
-            ttp[str(mm)]["structured"] = {"build_s": round(float(ts[0]), 4), "chain_s": round(float(ts[1]), 4),
-                                          "total_s": round(float(ts[0] + ts[1]), 4),
+            ttp[str(mm)]["structured"] = {"build_s": round(float(ts[0]), 6), "chain_s": round(float(ts[1]), 6),
+                                          "total_s": round(float(ts[0] + ts[1]), 6),
                                           "terms_per_step": NNZ.get(mm, 0) * nn,
                                           "chain_gterms": round((rs["k_stop"] - 1) * NNZ.get(mm, 0) * nn
                                                                 / float(ts[1]) / 1e9, 1)}
@@ -519,7 +519,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
         for mm in args.oracle_ttp_m:
             t0 = time.perf_counter()
             r = O.power_chain(mm, 50, am, 0)
-            ttp_o[str(mm)] = {"seconds": round(time.perf_counter() - t0, 4), "triple": [r["n0"], r["alpha"], r["beta"]]}
+            ttp_o[str(mm)] = {"seconds": round(time.perf_counter() - t0, 6), "triple": [r["n0"], r["alpha"], r["beta"]]}
         cpu["time_to_periodicity"] = ttp_o
         # SURVEY §8(d) oracle timings: the dense product at each small order (full N^3, same
         # OpenMP i-j-k loop) and the independent checkers on points of their domains

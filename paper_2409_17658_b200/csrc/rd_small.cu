@@ -71,13 +71,22 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
   __syncthreads();
 }
 
+// Loads of data written earlier in the same launch: ld.global.cg (L2, coherent across CTAs);
+// a one-CTA grid reads through L1 (its own writes, ordered by the block barrier).
+template <bool ONE, typename T>
+__device__ __forceinline__ T ldc(const T *p) {
+  if constexpr (ONE) return *p;
+  else return __ldcg(p);
+}
+
 // Alg 2 step 4 on a reduced stats vector (same rule as rd_stats_decide, rd_host.cpp).
+template <bool ONE>
 __device__ __forceinline__ bool decide(const int32_t *s, int alpha_max, int k, int only, int &alpha, int &beta) {
   const int amax = min(alpha_max, k - 1);
   for (int a = 1; a <= amax; ++a) {
     if (only > 0 && a != only) continue;
     const int32_t *e = s + 1 + 4 * (a - 1);
-    const int32_t lo = __ldcg(e), mhi = __ldcg(e + 1), mis = __ldcg(e + 2), fin = __ldcg(e + 3);
+    const int32_t lo = ldc<ONE>(e), mhi = ldc<ONE>(e + 1), mis = ldc<ONE>(e + 2), fin = ldc<ONE>(e + 3);
     if (mis == 0 && fin != 0 && (int64_t)lo == -(int64_t)mhi && lo >= 0) {
       alpha = a;
       beta = lo;
@@ -87,11 +96,13 @@ __device__ __forceinline__ bool decide(const int32_t *s, int alpha_max, int k, i
   return false;
 }
 
+template <bool ONE>
 __global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa) {
   __shared__ __align__(16) uint32_t sX[2][kST][kSKC];   // [row][k-pair]
   __shared__ __align__(16) uint32_t sB[2][kSKC][kST];   // [k-pair][column]
   __shared__ int32_t red[kSThreads / 32][1 + 4 * kMaxAlpha];
   __shared__ int s_stop;
+  __shared__ int32_t s_st[1 + 4 * kMaxAlpha];   // one-CTA grid: the power's stats in shared memory
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t N = sa.N, P = sa.P, P2 = P / 2;
   const int am = sa.alpha_max, slen = 1 + 4 * am;
@@ -151,6 +162,11 @@ __global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa)
     int16_t *C = slot(k);
     const int nprev = min(am, k - 1);
     int32_t *st = sa.stats + (int64_t)k * slen;
+    if constexpr (ONE) {   // a lone CTA reduces and decides in shared memory (no global atomics)
+      st = s_st;
+      for (int e = tid; e < slen; e += kSThreads) s_st[e] = (e == 0 || (e - 1) % 4 < 2) ? INT_MAX : 0;
+      __syncthreads();
+    }
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int64_t i0 = (int64_t)(tile / ntile) * kST, j0 = (int64_t)(tile % ntile) * kST;
       uint32_t acc[4][4];
@@ -168,9 +184,9 @@ __global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa)
         for (int q = 0; q < kQ; ++q) {
           const int e = q * kSThreads + tid;
           const int r = e / kSKC, tp = e % kSKC;   // consecutive threads: consecutive k-pairs of a row
-          px[q] = t0 + tp < P2 ? __ldcg(reinterpret_cast<const uint32_t *>(X + (i0 + r) * P) + t0 + tp) : kInf2;
+          px[q] = t0 + tp < P2 ? ldc<ONE>(reinterpret_cast<const uint32_t *>(X + (i0 + r) * P) + t0 + tp) : kInf2;
           const int bt = e / kST, bc = e % kST;    // consecutive threads: consecutive columns
-          pb[q] = t0 + bt < P2 ? __ldcg(sa.BP + (t0 + bt) * P + j0 + bc) : kInf2;
+          pb[q] = t0 + bt < P2 ? ldc<ONE>(sa.BP + (t0 + bt) * P + j0 + bc) : kInf2;
         }
       };
       auto stash = [&](int buf) {
@@ -244,7 +260,7 @@ __global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa)
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int q = lane + 32 * (8 * h + u), row = q >> 3, c8 = q & 7;
-            pv[u] = __ldcg(reinterpret_cast<const uint4 *>(Pv + (i0 + row) * P + j0 + c8 * 8));
+            pv[u] = ldc<ONE>(reinterpret_cast<const uint4 *>(Pv + (i0 + row) * P + j0 + c8 * 8));
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -281,18 +297,18 @@ __global__ void __launch_bounds__(kSThreads, 2) small_chain_kernel(SmallArgs sa)
       int a = 0, b = 0;
       int stop = 0;
       if (found_k < 0) {
-        if (decide(st, am, k, 0, a, b)) {
+        if (decide<ONE>(st, am, k, 0, a, b)) {
           found_k = k; n0 = k - a; al = a; be = b;
           if (sa.policy == 0) stop = 1;
         }
       } else {
         const int aa = k - n0;
-        if (aa <= am && decide(st, am, k, aa, a, b)) { al = a; be = b; }
+        if (aa <= am && decide<ONE>(st, am, k, aa, a, b)) { al = a; be = b; }
         if (aa >= am) stop = 1;
       }
       s_stop = stop;
       if (blockIdx.x == 0) {
-        const int32_t d = __ldcg(st);
+        const int32_t d = ldc<ONE>(st);
         sa.result[6 + k] = d >= RD_INF ? INT_MAX : d;
       }
     }
@@ -360,11 +376,12 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_chain_kernel, kSThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_chain_kernel<false>, kSThreads, 0);
     const int ntiles = (int)((P / kST) * (P / kST));
     const int grid = std::max(1, std::min(ntiles, sms * std::max(1, per_sm)));
     void *args[] = {&sa};
-    if ((e = cudaLaunchCooperativeKernel((void *)small_chain_kernel, grid, kSThreads, args, 0, st)) != cudaSuccess ||
+    void *fn = grid == 1 ? (void *)small_chain_kernel<true> : (void *)small_chain_kernel<false>;
+    if ((e = cudaLaunchCooperativeKernel(fn, grid, kSThreads, args, 0, st)) != cudaSuccess ||
         (e = cudaMemcpyAsync(h_res, sa.result, (size_t)(6 + kmax + 1) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
         (e = cudaStreamSynchronize(st)) != cudaSuccess)
       rc = fail(RD_ECUDA, "small_power_sequence: %s", cudaGetErrorString(e));

@@ -1,8 +1,9 @@
-// Register-tile probe of the fp16-encoded (min,+) forms (not part of the product; informs the
-// mainloop mix).  Entries <= 2048 are exact fp16 integers and positive fp16 bit
-// patterns order like unsigned 16-bit integers, so s = HADD2(x, b) (fma pipe) and a 3-input
-// unsigned 16-bit min VIMNMX3.U16x2 (alu) fold two k-pairs into an accumulator of fp16 bits.
-// The question is whether HADD2/HFMA2 issue at twice IMAD's rate (both fma sub-pipes).
+// Register-tile probe of a third add form for the (min,+) mainloop (not part of the product;
+// informs the mix).  HADD2 on raw int16 bit patterns is the exact integer sum
+// while operands and sum stay below 2048: a value k < 2048 read as fp16 is k * 2^-24 (the
+// subnormals and the first binade), whose bit pattern is k; RD_INF = 0x3FFF plus any such k
+// rounds back to 0x3FFF.  So s = HADD2(x, b) can stand in for the IMAD packed add on the same
+// operands.  The question is whether HADD2 issues beside IMAD (the other fma sub-pipe).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o hadd_probe hadd_probe.cu
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -24,6 +25,12 @@ __device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
 // FORM 3: GEMM 8x8 tile, every column [2 HADD2 + VIMNMX3.U16x2]     -> terms/clk
 // FORM 4: GEMM 8x8 tile, d=3 DPX + 5 x [2 IMAD + VIMNMX3] (today's mix)
 // FORM 5: GEMM 8x8 tile, 4 x [2 IMAD + VIMNMX3] + 4 x [2 HADD2 + VIMNMX3]
+// FORM 6: GEMM 8x8 tile, 3 DPX + 2 x [2 IMAD + VIMNMX3] + 3 x [2 HADD2 + VIMNMX3]
+// FORM 7: GEMM 8x8 tile, 3 DPX + 5 x [2 HADD2 + VIMNMX3]
+// FORM 8: GEMM 8x8 tile, 2 DPX + 3 x [IMAD] + 3 x [HADD2]
+// FORM 9: GEMM 8x8 tile, 4 DPX + 2 x [IMAD] + 2 x [HADD2]
+// (HADD2 on int16 bit patterns is the exact integer sum below 2048: a value k < 2048 read as
+// fp16 is the subnormal/first-binade number k * 2^-24 whose bit pattern is k.)
 template <int FORM>
 __global__ void __launch_bounds__(256, 2) probe(uint32_t *sink, long long *cyc, int iters, uint32_t one) {
   long long t0 = 0, t1 = 0;
@@ -70,10 +77,13 @@ __global__ void __launch_bounds__(256, 2) probe(uint32_t *sink, long long *cyc, 
       for (int r = 0; r < 8; ++r)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          if (FORM == 4 && c < 3) {
+          constexpr int D = FORM == 4 || FORM == 6 || FORM == 7 ? 3 : (FORM == 8 ? 2 : (FORM == 9 ? 4 : 0));
+          const bool h16 = FORM == 3 || (FORM == 5 && c >= 4) || (FORM == 6 && c >= 5) || (FORM == 7 && c >= 3) ||
+                           (FORM == 8 && c >= 5) || (FORM == 9 && c >= 6);
+          if (c < D) {
             acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
             acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
-          } else if (FORM == 3 || (FORM == 5 && c >= 4)) {
+          } else if (h16) {
             acc[r][c] = __vimin3_u16x2(acc[r][c], hadd2(x0[r], b0[c]), hadd2(x1[r], b1[c]));
           } else {
             acc[r][c] = __vimin3_s16x2(acc[r][c], x0[r] * one + b0[c], x1[r] * one + b1[c]);
@@ -125,5 +135,9 @@ int main() {
   run<3>(sms, "8x8 tile: all [2 HADD2 + VIMNMX3.U16x2]");
   run<4>(sms, "8x8 tile: 3 DPX + 5 [2 IMAD + VIMNMX3] (GEMM)");
   run<5>(sms, "8x8 tile: 4 [IMAD] + 4 [HADD2] groups");
+  run<6>(sms, "8x8 tile: 3 DPX + 2 [IMAD] + 3 [HADD2]");
+  run<7>(sms, "8x8 tile: 3 DPX + 5 [HADD2]");
+  run<8>(sms, "8x8 tile: 2 DPX + 3 [IMAD] + 3 [HADD2]");
+  run<9>(sms, "8x8 tile: 4 DPX + 2 [IMAD] + 2 [HADD2]");
   return 0;
 }
