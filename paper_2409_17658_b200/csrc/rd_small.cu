@@ -373,15 +373,30 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
     rc = fail(RD_ECUDA, "small_power_sequence: upload: %s", cudaGetErrorString(e));
   const auto t1 = std::chrono::steady_clock::now();
   if (rc == RD_OK) {
-    int dev = 0, sms = 0, per_sm = 0;
+    // co-resident CTAs per device, queried once (the launch is cooperative: every CTA meets
+    // the grid barrier); a one-tile order runs one CTA with an ordinary launch
+    static int s_sms[64] = {}, s_per_sm[64] = {};
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_chain_kernel<false>, kSThreads, 0);
+    int sms = 148, per_sm = 1;
+    if (dev >= 0 && dev < 64 && s_sms[dev]) {
+      sms = s_sms[dev];
+      per_sm = s_per_sm[dev];
+    } else {
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_chain_kernel<false>, kSThreads, 0);
+      if (dev >= 0 && dev < 64) { s_sms[dev] = sms; s_per_sm[dev] = per_sm; }
+    }
     const int ntiles = (int)((P / kST) * (P / kST));
     const int grid = std::max(1, std::min(ntiles, sms * std::max(1, per_sm)));
     void *args[] = {&sa};
-    void *fn = grid == 1 ? (void *)small_chain_kernel<true> : (void *)small_chain_kernel<false>;
-    if ((e = cudaLaunchCooperativeKernel(fn, grid, kSThreads, args, 0, st)) != cudaSuccess ||
+    if (grid == 1) {
+      small_chain_kernel<true><<<1, kSThreads, 0, st>>>(sa);
+      e = cudaGetLastError();
+    } else {
+      e = cudaLaunchCooperativeKernel((void *)small_chain_kernel<false>, grid, kSThreads, args, 0, st);
+    }
+    if (e != cudaSuccess ||
         (e = cudaMemcpyAsync(h_res, sa.result, (size_t)(6 + kmax + 1) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
         (e = cudaStreamSynchronize(st)) != cudaSuccess)
       rc = fail(RD_ECUDA, "small_power_sequence: %s", cudaGetErrorString(e));
