@@ -100,6 +100,69 @@ __global__ void __launch_bounds__(256, 2) probe(uint32_t *sink, long long *cyc, 
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// FORM 10: three k-pairs per step, every column [3 IMAD + VIMNMX3(s0,s1,s2) + VIMNMX(acc, m)]
+// FORM 11: three k-pairs per step, 3 DPX columns (3 DPX each) + 5 columns as FORM 10
+template <int FORM>
+__global__ void __launch_bounds__(256, 2) probe3(uint32_t *sink, long long *cyc, int iters, uint32_t one) {
+  uint32_t acc[8][8], x0[8], x1[8], x2[8], b0[8], b1[8], b2[8];
+  const uint32_t s = threadIdx.x * 0x00010001u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    x0[i] = s + i; x1[i] = s + 2 * i; x2[i] = s + 7 * i; b0[i] = s + 3 * i; b1[i] = s + 5 * i; b2[i] = s + 11 * i;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0x3FFF3FFFu;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { OPQ(x0[i]); OPQ(x1[i]); OPQ(x2[i]); OPQ(b0[i]); OPQ(b1[i]); OPQ(b2[i]); }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (FORM == 11 && c < 3) {
+          acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+          acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+          acc[r][c] = __viaddmin_s16x2(x2[r], b2[c], acc[r][c]);
+        } else {
+          const uint32_t m = __vimin3_s16x2(x0[r] * one + b0[c], x1[r] * one + b1[c], x2[r] * one + b2[c]);
+          acc[r][c] = __vmins2(acc[r][c], m);
+        }
+      }
+  }
+  const long long t1 = clock64();
+  uint32_t h = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) h ^= acc[r][c];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = h;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int FORM>
+void run3(int sms, const char *name) {
+  const int blocks = sms * 2, threads = 256, iters = 2000;
+  uint32_t *sink;
+  long long *cyc;
+  cudaMalloc(&sink, blocks * threads * 4);
+  cudaMalloc(&cyc, blocks * 8);
+  probe3<FORM><<<blocks, threads>>>(sink, cyc, 16, 1);
+  probe3<FORM><<<blocks, threads>>>(sink, cyc, iters, 1);
+  cudaDeviceSynchronize();
+  long long *h = new long long[blocks];
+  cudaMemcpy(h, cyc, blocks * 8, cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int b = 0; b < blocks; ++b) mx = h[b] > mx ? h[b] : mx;
+  const double t = (double)iters * 384.0 * threads * 2 / (double)mx;   // 64 acc x 3 k-pairs x 2 lanes
+  printf("%-44s %.1f (min,+) terms/clk/SM\n", name, t);
+  delete[] h;
+  cudaFree(sink);
+  cudaFree(cyc);
+}
+
 template <int FORM>
 void run(int sms, const char *name) {
   const int blocks = sms * 2, threads = 256, iters = FORM <= 2 ? 8192 : 2000;
@@ -139,5 +202,7 @@ int main() {
   run<7>(sms, "8x8 tile: 3 DPX + 5 [HADD2]");
   run<8>(sms, "8x8 tile: 2 DPX + 3 [IMAD] + 3 [HADD2]");
   run<9>(sms, "8x8 tile: 4 DPX + 2 [IMAD] + 2 [HADD2]");
+  run3<10>(sms, "8x8 tile, 3 k-pairs: all [3 IMAD + V3 + VMIN]");
+  run3<11>(sms, "8x8 tile, 3 k-pairs: 3 DPX + 5 [3 IMAD+V3+VMIN]");
   return 0;
 }
