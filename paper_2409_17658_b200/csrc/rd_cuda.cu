@@ -350,7 +350,6 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
-    if (STATS && g_dpx_cols == 23) return launch_gemm_v<kOutPM, true, 23, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma);
     switch (g_dpx_cols) {
       case 0: return RD_LGT(0);
       case 2: return RD_LGT(2);
@@ -372,7 +371,6 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
 #undef RD_LG64
   }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
-  if (OUT_PM && STATS && g_dpx_cols == 23) return launch_gemm_v<kOutPM, true, 23>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb);
   switch (g_dpx_cols) {
     case 0: return RD_LG(0);
     case 2: return RD_LG(2);
@@ -416,8 +414,8 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 
 extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   rd_enter();
-  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8 && dpx_cols != 23)
-    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8, 23");
+  if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
+    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
   g_dpx_cols = dpx_cols;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")

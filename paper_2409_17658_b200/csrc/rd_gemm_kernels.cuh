@@ -1,8 +1,6 @@
 // Kernel templates of the (min,+) GEMM and their launchers; included only by the
 // instantiation units rd_gemm_*.cu (compiled in parallel).  See rd_gemm.cuh.
 #pragma once
-#include <type_traits>
-
 #include "rd_gemm.cuh"
 
 namespace rd {
@@ -145,12 +143,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             for (int c = 0; c < NC; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
         }
       } else {
-        // DPXC = 20 + d: the mix of d, with warps 4..7 walking the accumulators in reverse
-        // order (IMAD columns first), so each SMSP's two warps of a CTA are in opposite phases
-        constexpr int D = DPXC % 10;
-        constexpr bool DEPH = DPXC >= 20;
-        auto stage_body = [&](auto rev) {
-          constexpr bool REV = decltype(rev)::value;
 #pragma unroll
         for (int t = 0; t < kBK2; t += 2) {
           uint32_t x0[8], x1[8], b0[NC], b1[NC];
@@ -170,11 +162,10 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
 #pragma unroll
-          for (int rr = 0; rr < 8; ++rr)
+          for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int cc = 0; cc < NC; ++cc) {
-              const int r = REV ? 7 - rr : rr, c = REV ? NC - 1 - cc : cc;
-              if ((r * NC + c) % 8 < D) {
+            for (int c = 0; c < NC; ++c) {
+              if ((r * NC + c) % 8 < DPXC) {
                 acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
                 acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
               } else {
@@ -184,9 +175,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
               }
             }
         }
-        };
-        if (DEPH && (tid & 128)) stage_body(std::true_type{});
-        else stage_body(std::false_type{});
       }
       if constexpr (TMA) {   // release this stage; the last warp to release it refills it
         __syncwarp();

@@ -3,4 +3,3 @@
 #include "rd_gemm_kernels.cuh"
 
 RD_INST_GEMM_ALL(rd::kOutPM, true, false)
-RD_INST_GEMM(rd::kOutPM, true, 23, false)

@@ -16,8 +16,8 @@ for _ in range(3):
     ch.step()
 res = {}
 for rep in range(3):
-    for d in ((3, 23) if len(sys.argv) > 2 else (3, 4)):
-        for mode, name in (((1, "thread0"),) if len(sys.argv) > 2 else ((3, "last-warp"), (1, "thread0"))):
+    for d in (3, 4):
+        for mode, name in ((3, "last-warp"), (1, "thread0")):
             rd.rd_set_gemm_tma(mode)
             rd.rd_set_gemm_variant(d)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
