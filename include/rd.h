@@ -356,6 +356,14 @@ int rd_set_gemm_variant(int dpx_cols);
  * count; 64 or 128 forces the width.  Identical results.  RD_EINVAL otherwise. */
 int rd_set_gemm_tile(int tn);
 
+/* rd_dense_step_plan — the dense chain step's wave model, for inspection (host only): for a
+ * row panel of `rows` rows of an order-N power on a device with `sms` SMs, the tile width
+ * (*tile: 128 or 64) and split-K count (*nsplit: 1..8) rd_chain_step will use under the current
+ * switches (rd_set_gemm_tile, rd_set_split_k, rd_set_gemm_tma), and the predicted step time
+ * (*cost, nullable; units: 128 x 128-tile pipeline stages at full occupancy).
+ * "Wave quantisation".  Errors: RD_EINVAL. */
+int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, double *cost);
+
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
  * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
  * counted on an mbarrier; the warps release stages on a second mbarrier); without, every

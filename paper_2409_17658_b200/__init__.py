@@ -87,6 +87,8 @@ def lib():
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_stream_k.argtypes = [ci]
         L.rd_set_gemm_tile.argtypes = [ci]
+        L.rd_dense_step_plan.argtypes = [i64, i64, ci, p, p, p]
+        L.rd_dense_step_plan.restype = ci
         L.rd_set_gemm_tile.restype = ci
         L.rd_set_small_chain.argtypes = [ci]
         L.rd_set_small_chain.restype = ci
@@ -347,6 +349,13 @@ def rd_set_split_k(enable):
 def rd_set_stream_k(mode: int):
     """Stream-K remainder of dense chain steps (rd.h): 0 off (default), 1 model, 2 forced."""
     _check(lib().rd_set_stream_k(int(mode)))
+
+
+def rd_dense_step_plan(rows: int, N: int, sms: int = 148):
+    """(tile width, split count, predicted cost) of a dense chain step's wave model (rd.h)."""
+    tile, ns, cost = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check(lib().rd_dense_step_plan(rows, N, sms, ctypes.byref(tile), ctypes.byref(ns), ctypes.byref(cost)))
+    return tile.value, ns.value, cost.value
 
 
 def rd_set_gemm_tile(tn: int):

@@ -2407,6 +2407,54 @@ extern "C" int rd_set_gemm_tma(int mode) try {
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_tma")
 
+// The dense step's wave model (see rd_chain_step): predicted time, in 128-tile stages at full
+// occupancy, of (tile width, split count); writes the best pair.  Mp = padded panel rows, P =
+// padded order; tile_force 0/64/128; no_split; split_force >= 2 forces n; tma = the TMA
+// mainloop is available for tn = 128, n = 1.
+static double dense_step_plan(int64_t Mp, int64_t P, int sms, int tile_force, int no_split, int split_force, bool tma,
+                              int *tn_out, int *n_out) {
+  static const double v128[3] = {0.0, 0.676, 1.0}, v64[4] = {0.0, 0.62, 0.90, 0.951};
+  const int64_t kstages = (P / 2) / kBK2;
+  auto cost = [&](int w_tn, int n) {
+    const int S = w_tn == 128 ? 2 : 3;
+    const int64_t units = (Mp / kTile) * (P / w_tn) * n;
+    const double w = (w_tn / 128.0) * ((double)kstages / n + 1.5 + (n > 1 ? 0.2 * n : 0.0));
+    double t = 0.0;
+    for (int64_t left = units; left > 0;) {
+      const int64_t u = std::min<int64_t>(left, (int64_t)sms * S);
+      left -= u;
+      const int L = (int)((u + sms - 1) / sms);
+      t += L * w / (w_tn == 128 ? v128[L] : v64[L]);
+    }
+    if (w_tn == 128 && n == 1 && kstages >= 128 && tma) t *= 0.99;
+    return t;
+  };
+  double best = -1.0;
+  *tn_out = 128;
+  *n_out = 1;
+  for (int w_tn : {128, 64}) {
+    if (tile_force && w_tn != tile_force) continue;
+    for (int n = 1; n <= 8 && (n == 1 || kstages >= 2 * n); ++n) {
+      if (no_split && n > 1) break;
+      if (split_force && n != std::min<int64_t>(split_force, std::max<int64_t>(1, kstages / 2))) continue;
+      const double t = cost(w_tn, n);
+      if (best < 0.0 || t < best) { best = t; *tn_out = w_tn; *n_out = n; }
+    }
+  }
+  return best;
+}
+
+extern "C" int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, double *cost) try {
+  rd_enter();
+  if (rows < 1 || N < 1 || rows > N || sms < 1 || !tile || !nsplit)
+    return fail(RD_EINVAL, "rd_dense_step_plan: need 1 <= rows <= N, sms >= 1, non-NULL outputs");
+  const double t = dense_step_plan(round_up(rows, kTile), round_up(N, kTile), sms, g_gemm_tile, g_split_k_off ? 1 : 0,
+                                   g_split_force, g_gemm_tma == 1 || g_gemm_tma == 3, tile, nsplit);
+  if (cost) *cost = t;
+  return RD_OK;
+} RD_ABI_CATCH("rd_dense_step_plan")
+
+
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -2633,31 +2681,8 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    static const double v128[3] = {0.0, 0.676, 1.0}, v64[4] = {0.0, 0.62, 0.90, 0.951};
-    auto cost = [&](int w_tn, int n) {
-      const int S = w_tn == 128 ? 2 : 3;
-      const int64_t units = (c->Mp / kTile) * (c->P / w_tn) * n;
-      const double w = (w_tn / 128.0) * ((double)kstages / n + 1.5 + (n > 1 ? 0.2 * n : 0.0));
-      double t = 0.0;
-      for (int64_t left = units; left > 0;) {
-        const int64_t u = std::min<int64_t>(left, (int64_t)sms * S);
-        left -= u;
-        const int L = (int)((u + sms - 1) / sms);
-        t += L * w / (w_tn == 128 ? v128[L] : v64[L]);
-      }
-      if (w_tn == 128 && n == 1 && kstages >= 128 && (g_gemm_tma == 1 || g_gemm_tma == 3)) t *= 0.99;
-      return t;
-    };
-    double best = -1.0;
-    for (int w_tn : {128, 64}) {
-      if (g_gemm_tile && w_tn != g_gemm_tile) continue;
-      for (int n = 1; n <= 8 && (n == 1 || kstages >= 2 * n); ++n) {
-        if (g_split_k_off && n > 1) break;
-        if (g_split_force && n != std::min<int64_t>(g_split_force, std::max<int64_t>(1, kstages / 2))) continue;
-        const double t = cost(w_tn, n);
-        if (best < 0.0 || t < best) { best = t; tn = w_tn; nsplit = n; }
-      }
-    }
+    const double best = dense_step_plan(c->Mp, c->P, sms, g_gemm_tile, g_split_k_off ? 1 : 0, g_split_force,
+                                        g_gemm_tma == 1 || g_gemm_tma == 3, &tn, &nsplit);
     const int64_t slots = 2 * (int64_t)sms;
     const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
     if (g_stream_k && rem > 0) {

@@ -214,3 +214,55 @@ def test_every_status_entry_is_a_function_try_block():
             body_start = src.index("{", mt.end())
             assert src[mt.end():body_start].rstrip().endswith("try"), name
             assert f'RD_ABI_CATCH("{name}")' in src, name
+
+
+# Measured dense step times (ms, median of 10) of every (tile width, split) configuration on one
+# B200, profiles/r02b_wave_probe.txt; m = 9 p = 8 "t128/s1" is the TMA default's time.
+WAVE_TABLE = {
+    (6, 1): {"t128/s1": 0.0945, "t128/s2": 0.0673, "t128/s3": 0.0593, "t128/s4": 0.0720, "t64/s1": 0.0540,
+             "t64/s2": 0.0608, "t64/s3": 0.0479, "t64/s4": 0.0507},
+    (7, 1): {"t128/s1": 0.5677, "t128/s2": 0.5754, "t128/s3": 0.5798, "t128/s4": 0.5549, "t64/s1": 0.5775,
+             "t64/s2": 0.5457, "t64/s3": 0.5675, "t64/s4": 0.5621},
+    (7, 2): {"t128/s1": 0.3848, "t128/s2": 0.3070, "t128/s3": 0.3374, "t128/s4": 0.3132, "t64/s1": 0.2998,
+             "t64/s2": 0.3101, "t64/s3": 0.3076, "t64/s4": 0.2901},
+    (7, 4): {"t128/s1": 0.2097, "t128/s2": 0.2195, "t128/s3": 0.2252, "t128/s4": 0.1689, "t64/s1": 0.2051,
+             "t64/s2": 0.1652, "t64/s3": 0.1806, "t64/s4": 0.1678},
+    (8, 1): {"t128/s1": 11.3222, "t128/s2": 11.4041, "t128/s3": 11.4160, "t128/s4": 11.4322, "t64/s1": 11.8344,
+             "t64/s2": 11.8199, "t64/s3": 11.8988, "t64/s4": 11.9254},
+    (8, 2): {"t128/s1": 5.9261, "t128/s2": 5.7440, "t128/s3": 5.8119, "t128/s4": 5.7870, "t64/s1": 5.9364,
+             "t64/s2": 5.9763, "t64/s3": 6.0036, "t64/s4": 5.9794},
+    (8, 4): {"t128/s1": 3.0006, "t128/s2": 3.0089, "t128/s3": 3.0159, "t128/s4": 3.0259, "t64/s1": 3.1149,
+             "t64/s2": 3.1313, "t64/s3": 3.1424, "t64/s4": 3.1528},
+    (8, 8): {"t128/s1": 2.0115, "t128/s2": 1.7723, "t128/s3": 1.6985, "t128/s4": 1.6644, "t64/s1": 1.8322,
+             "t64/s2": 1.7125, "t64/s3": 1.6787, "t64/s4": 1.7258},
+    (9, 8): {"t128/s1": 36.3663, "t128/s2": 36.9964, "t128/s3": 36.6186, "t128/s4": 36.7558, "t64/s1": 38.8295,
+             "t64/s2": 38.5407, "t64/s3": 38.4853, "t64/s4": 38.4956},
+}
+
+
+def test_wave_model_picks_near_measured_best():
+    """rd_dense_step_plan (the dense step's wave model, host only) picks, for every measured shape,
+    a (tile width, split) whose measured time is within 4 % of the best of the 8 configurations
+    (configuration-to-configuration noise is ~2 %), while the plain 128-tile step is up to 2x off."""
+    from paper_2409_17658_b200 import dist as D
+    worst_plain = 0.0
+    for (m, p), t in WAVE_TABLE.items():
+        N = rd.count_words(m)
+        r0, r1 = D.panel_bounds(N, p, 0)
+        tile, ns, _ = rd.rd_dense_step_plan(r1 - r0, N)
+        key = f"t{tile}/s{ns}"
+        best = min(t.values())
+        assert key in t, (m, p, key)
+        assert t[key] <= 1.04 * best, (m, p, key, t[key], best)
+        worst_plain = max(worst_plain, t["t128/s1"] / best)
+    assert worst_plain > 1.9
+    # forcing knobs reach the plan
+    rd.rd_set_gemm_tile(128)
+    rd.rd_set_split_k(0)
+    try:
+        assert rd.rd_dense_step_plan(848, 848)[:2] == (128, 1)
+    finally:
+        rd.rd_set_gemm_tile(0)
+        rd.rd_set_split_k(1)
+    with pytest.raises(rd.RDError):
+        rd.rd_dense_step_plan(0, 848)
