@@ -28,6 +28,6 @@ echo "full rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:panel_stats -s 2 -c 1 -o $O/${TAG}_panel_stats python tools/time_panel_stats.py > $O/${TAG}_ncu_ps.log 2>&1
 echo "ps full rc=$?"
 timeout 1200 python tools/wave_probe.py > $O/${TAG}_wave.txt 2>&1; echo "wave rc=$?"
-[ -x tools/hadd_probe ] && timeout 120 tools/hadd_probe > $O/${TAG}_hadd_probe.txt 2>&1; cat $O/${TAG}_hadd_probe.txt
+timeout 300 python tools/alpha_cost_probe.py > $O/${TAG}_alpha_cost.txt 2>&1; cat $O/${TAG}_alpha_cost.txt
 timeout 900 python tools/hash_repro.py 1 2 > $O/${TAG}_hash.txt 2>&1; cat $O/${TAG}_hash.txt
 cat $O/${TAG}_bench.json; cat $O/${TAG}_bench_ref.json
