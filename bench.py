@@ -327,6 +327,7 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
     peak = SM_COUNT * PIPE_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
     dpx_peak = SM_COUNT * DPX_MINPLUS_PER_CLK_SM * SM_MAX_MHZ * 1e6 / 1e9
     mix_peak = SM_COUNT * probe["mixed_minplus_per_clk_sm"] * SM_MAX_MHZ * 1e6 / 1e9
+    dpx_used = chain.gemm_variant if chain is not None and hasattr(chain, "gemm_variant") else None
     if chain is not None:
         chain.close()
 
@@ -572,7 +573,8 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                          "dpx_issue_peak_basis": "DPX-only: 148 SMs x 128 (min,+)/clk/SM (VIADDMNMX.S16x2 at 2 warp-instr/clk/SM, measured) x 1965 MHz",
                          "mix_ceiling": round(mix_peak, 1), "frac_of_mix_ceiling": round(achieved / mix_peak, 4),
                          "mix_ceiling_basis": "register-tile probe of the GEMM's DPX+IMAD/VIMNMX3 mix (rd_alu_probe, live) x 148 SMs x 1965 MHz",
-                         "probe": {k: round(v, 2) for k, v in probe.items()}},
+                         "probe": {k: round(v, 2) for k, v in probe.items()},
+                         "dpx_cols": dpx_used},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps * world,
             "e2e": e2e,

@@ -346,8 +346,13 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * set it before launching work).  dpx_cols in {0, 2, 3, 4, 8}: of each thread's 8
  * accumulator columns, that many use one VIADDMNMX.S16x2 (alu pipe) per k-pair; the rest
  * use two IMAD packed adds (fma pipe) + one VIMNMX3.S16x2 (alu) per two k-pairs
- * (DESIGN.md §5).  Every variant computes the identical result.  Errors: RD_EINVAL. */
+ * (DESIGN.md §5).  Every variant computes the identical result.  By default (or after
+ * dpx_cols = -1) a dense chain whose steps use the TMA mainloop times its first step with 3
+ * and its second with 4 DPX columns and keeps the faster (the two trade places by ~1.5 % from
+ * one B200 to the next); any explicit value turns that off.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
+/* The DPX column count a chain's steps use (after its tuning steps), or -1 for NULL. */
+int rd_chain_gemm_variant(const rd_chain *c);
 
 /* rd_set_gemm_tile — process-wide tile width of the dense chain step's GEMM (DESIGN.md §5
  * "Wave quantisation"): 0 (default) = the step's wave model chooses, per step shape, between

@@ -77,6 +77,7 @@ def lib():
         L.rd_chain_order.argtypes = [p]; L.rd_chain_order.restype = i64
         L.rd_chain_current_k.argtypes = [p]
         L.rd_chain_diag1.argtypes = [p]; L.rd_chain_diag1.restype = i32
+        L.rd_chain_gemm_variant.argtypes = [p]; L.rd_chain_gemm_variant.restype = ci
         L.rd_stats_len.argtypes = [ci]
         L.rd_chain_step.argtypes = [p, p]
         L.rd_chain_read_rows.argtypes = [p, ci, p]
@@ -328,7 +329,8 @@ def rd_roman_cylinder(m: int, n: int, method: int | None = None) -> int:
 
 
 def rd_set_gemm_variant(dpx_cols: int):
-    """Mainloop instruction mix (rd.h): dpx_cols in {0, 2, 3, 4, 8}."""
+    """Mainloop instruction mix (rd.h): dpx_cols in {0, 2, 3, 4, 8}; -1 = default (3, tuned
+    against 4 per long chain)."""
     _check(lib().rd_set_gemm_variant(dpx_cols))
 
 
@@ -442,6 +444,11 @@ class Chain:
     @property
     def k(self) -> int:
         return lib().rd_chain_current_k(self._h)
+
+    @property
+    def gemm_variant(self) -> int:
+        """DPX column count of this chain's dense steps (rd_chain_gemm_variant)."""
+        return lib().rd_chain_gemm_variant(self._h)
 
     def step(self, stats=None):
         s = self.stats if stats is None else stats

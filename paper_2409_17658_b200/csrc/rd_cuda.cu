@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restr
 }
 
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
+int g_dpx_auto = 1;       // long dense chain steps tune 3 vs 4 per chain until rd_set_gemm_variant is called
 int g_gemm_tile = 0;      // rd_set_gemm_tile: 0 = the chain's wave model picks, 64 / 128 forced
 int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
 
@@ -333,12 +334,13 @@ __global__ void pack_copy32_kernel(const int32_t *__restrict__ B, int64_t ld, in
 template <bool OUT_PM, bool STATS>
 int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb, int64_t kpairs, void *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t Mp, int64_t Np, const EpiArgs &epi,
-                cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr, int tn = 128) {
+                cudaStream_t st, int nsplit = 1, const TmaOps *tma = nullptr, int tn = 128, int dpx = -1) {
   const PeerB pb{};
+  const int dcols = dpx >= 0 ? dpx : g_dpx_cols;
   if (OUT_PM && STATS && epi.sk_nsk > 0) {   // stream-K step (rd_set_stream_k)
 #define RD_LGS(D, T) launch_gemm_v<kOutPM, true, D, T, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, 1, pb, tma)
 #define RD_LGS2(D) return tma ? RD_LGS(D, true) : RD_LGS(D, false)
-    switch (g_dpx_cols) {
+    switch (dcols) {
       case 0: RD_LGS2(0);
       case 2: RD_LGS2(2);
       case 3: RD_LGS2(3);
@@ -350,7 +352,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
   if (OUT_PM && tma) {   // the chain's PM step with the TMA mainloop (rd_set_gemm_tma)
 #define RD_LGT(D) launch_gemm_v<kOutPM, STATS, D, true>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb, tma)
-    switch (g_dpx_cols) {
+    switch (dcols) {
       case 0: return RD_LGT(0);
       case 2: return RD_LGT(2);
       case 3: return RD_LGT(3);
@@ -361,7 +363,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
   }
   if (OUT_PM && tn == 64 && !tma) {   // 128 x 64 tiles, 3 CTAs per SM (the chain's wave model)
 #define RD_LG64(D) launch_gemm_v<kOutPM, STATS, D, false, false, 64>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
-    switch (g_dpx_cols) {
+    switch (dcols) {
       case 0: return RD_LG64(0);
       case 2: return RD_LG64(2);
       case 3: return RD_LG64(3);
@@ -371,7 +373,7 @@ int launch_gemm(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t ldb
 #undef RD_LG64
   }
 #define RD_LG(D) launch_gemm_v<OUT_PM ? kOutPM : kOutRow, STATS, D>(XT, ldx, BP, ldb, kpairs, C, ldc, M, N, Mp, Np, epi, st, nsplit, pb)
-  switch (g_dpx_cols) {
+  switch (dcols) {
     case 0: return RD_LG(0);
     case 2: return RD_LG(2);
     case 3: return RD_LG(3);
@@ -414,9 +416,15 @@ int pack_right(const int16_t *B, int64_t ld, int64_t K, int64_t N, uint32_t *BP,
 
 extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   rd_enter();
+  if (dpx_cols == -1) {   // back to the default: 3, tuned per long chain
+    g_dpx_cols = 3;
+    g_dpx_auto = 1;
+    return RD_OK;
+  }
   if (dpx_cols != 0 && dpx_cols != 2 && dpx_cols != 3 && dpx_cols != 4 && dpx_cols != 8)
-    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of 0, 2, 3, 4, 8");
+    return fail(RD_EINVAL, "rd_set_gemm_variant: dpx_cols must be one of -1 (auto), 0, 2, 3, 4, 8");
   g_dpx_cols = dpx_cols;
+  g_dpx_auto = 0;   // an explicit choice: no per-chain tuning
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")
 
@@ -1972,6 +1980,10 @@ struct rd_chain {
   int16_t *wcol = nullptr;   // uniform-label format (see minplus_sparse_kernel)
   uint32_t *ws = nullptr;    // method 0 split-K partial tiles (small grids), lazily allocated
   int *tile_cnt = nullptr;   // method 0 split-K fixup tickets, one per tile (self-resetting)
+  // method 0, long steps: the DPX column count is tuned on the chain's first two TMA steps
+  // (3, then 4, each timed with events; the faster is kept) unless rd_set_gemm_variant fixed it
+  int dpx = -1, tune_state = 0;
+  cudaEvent_t tune_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
@@ -2592,6 +2604,8 @@ extern "C" int rd_chain_destroy(rd_chain *c) try {
   chain_free(c, c->colptr);
   chain_free(c, c->ent);
   chain_free(c, c->wcol);
+  for (cudaEvent_t &e : c->tune_ev)
+    if (e) cudaEventDestroy(e);
   chain_free(c, c->ws);
   chain_free(c, c->tile_cnt);
   chain_free(c, c->spread);
@@ -2605,6 +2619,10 @@ extern "C" int rd_chain_destroy(rd_chain *c) try {
 extern "C" int64_t rd_chain_order(const rd_chain *c) { return c ? c->N : -1; }
 extern "C" int rd_chain_current_k(const rd_chain *c) { return c ? c->k : -1; }
 extern "C" int32_t rd_chain_diag1(const rd_chain *c) { return c ? c->diag1 : INT32_MAX; }
+extern "C" int rd_chain_gemm_variant(const rd_chain *c) {
+  if (!c) return -1;
+  return c->dpx >= 0 ? c->dpx : g_dpx_cols;
+}
 extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
   if (!c) return -1.0;
   return c->method == 0 ? (double)c->Mr * (double)c->N * (double)c->N : (double)c->Mr * (double)c->nnz;
@@ -2727,9 +2745,31 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
         (int)kstages, epi);
     RD_CUDA_CHECK(cudaGetLastError());
   } else if (nsplit == 1) {
+    // the DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
+    // §5), so a chain of long TMA steps times one step with each and keeps the faster
+    int dpx = -1;
+    if (tma && g_dpx_auto && c->tune_state < 3) {
+      if (c->tune_state == 0) {
+        for (cudaEvent_t &e : c->tune_ev) RD_CUDA_CHECK(cudaEventCreate(&e));
+        dpx = 3;
+      } else if (c->tune_state == 1) {
+        dpx = 4;
+      } else {
+        float t3 = 0.f, t4 = 0.f;
+        RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[3]));
+        RD_CUDA_CHECK(cudaEventElapsedTime(&t3, c->tune_ev[0], c->tune_ev[1]));
+        RD_CUDA_CHECK(cudaEventElapsedTime(&t4, c->tune_ev[2], c->tune_ev[3]));
+        c->dpx = t4 < t3 ? 4 : 3;
+      }
+    }
+    if (tma && g_dpx_auto && c->tune_state >= 2) dpx = c->dpx;
+    const int tuning = (tma && g_dpx_auto && c->tune_state < 2) ? c->tune_state : -1;
+    if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning], c->st));
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st, 1, tma, tn);
+                                     c->N, c->Mp, c->P, epi, c->st, 1, tma, tn, dpx);
     if (rc != RD_OK) return rc;
+    if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning + 1], c->st));
+    if (tma && g_dpx_auto && c->tune_state < 3) ++c->tune_state;
   } else {
     // split-K with the in-kernel fixup: partial tiles in c->ws, the last CTA of each tile folds
     // them, stores the power and computes the stats (no separate combine pass)

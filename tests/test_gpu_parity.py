@@ -247,7 +247,7 @@ def test_every_gemm_variant_bit_exact(variant):
         assert (ch.read_rows(5) == P[5]).all()
         ch.close()
     finally:
-        rd.rd_set_gemm_variant(3)
+        rd.rd_set_gemm_variant(-1)
 
 
 def test_alu_probe_reports_rates():
@@ -895,7 +895,7 @@ def test_minplus_mul32_every_variant_and_int16_agreement(variant):
                                   _gpu(to_inf(B16, RINF, RINF32, np.int32))).cpu().numpy()
         C16 = rd.rd_minplus_mul(_gpu(A16), _gpu(B16)).cpu().numpy()
     finally:
-        rd.rd_set_gemm_variant(3)
+        rd.rd_set_gemm_variant(-1)
     assert (C32 == to_inf(C16, RINF, RINF32, np.int32)).all()
     assert (C32 == _oracle_mul32(to_inf(A16, RINF, RINF32, np.int32), to_inf(B16, RINF, RINF32, np.int32))).all()
 
@@ -1111,7 +1111,7 @@ def test_tile64_chain_equals_oracle(variant):
             ch.close()
     finally:
         rd.rd_set_gemm_tile(0)
-        rd.rd_set_gemm_variant(3)
+        rd.rd_set_gemm_variant(-1)
         rd.rd_set_split_k(True)
 
 
@@ -1139,3 +1139,27 @@ def test_forced_split_k_fixup_equals_oracle(tn):
     finally:
         rd.rd_set_split_k(1)
         rd.rd_set_gemm_tile(0)
+
+
+def test_chain_tunes_dpx_mix_bit_exact():
+    """A dense chain on the TMA mainloop times its first step with 3 and its second with 4 DPX
+    columns and keeps the faster (rd_set_gemm_variant default): every power stays equal to the
+    oracle's and the chosen variant is 3 or 4; an explicit variant switches the tuning off."""
+    rd.rd_set_gemm_tma(2)
+    try:
+        P = {k: X for k, X in O.powers(7, 7)}
+        ch = rd.Chain(7, alpha_max=4)
+        for k in range(2, 8):
+            ch.step()
+            assert (ch.read_rows(k) == to_inf(P[k], OINF, RINF, np.int16)).all(), k
+        assert ch.gemm_variant in (3, 4)
+        ch.close()
+        rd.rd_set_gemm_variant(8)
+        ch = rd.Chain(7, alpha_max=4)
+        for _ in range(4):
+            ch.step()
+        assert ch.gemm_variant == 8
+        ch.close()
+    finally:
+        rd.rd_set_gemm_variant(-1)
+        rd.rd_set_gemm_tma(1)

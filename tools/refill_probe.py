@@ -26,7 +26,7 @@ for rep in range(3):
             torch.cuda.synchronize()
             res.setdefault(f"d={d} {name}", []).extend(a.elapsed_time(b) for a, b in ev)
 rd.rd_set_gemm_tma(1)
-rd.rd_set_gemm_variant(3)
+rd.rd_set_gemm_variant(-1)
 ch.close()
 N = rd.count_words(m)
 for k, v in res.items():

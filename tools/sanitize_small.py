@@ -17,7 +17,7 @@ for N in (1, 33, 130, 300):
 for v in (0, 2, 3, 4, 8):
     rd.rd_set_gemm_variant(v)
     rd.rd_minplus_mul(torch.from_numpy(operand(257, 257, 3)).cuda(), torch.from_numpy(operand(257, 257, 4)).cuda())
-rd.rd_set_gemm_variant(3)
+rd.rd_set_gemm_variant(-1)
 for method in (0, 1):
     for m in (3, 5):
         print(m, method, rd.rd_power_sequence(m, 50, method=method)["n0"])
