@@ -900,20 +900,6 @@ def test_minplus_mul32_every_variant_and_int16_agreement(variant):
     assert (C32 == _oracle_mul32(to_inf(A16, RINF, RINF32, np.int32), to_inf(B16, RINF, RINF32, np.int32))).all()
 
 
-@pytest.mark.skipif(__import__("os").environ.get("RD_LONG") != "2", reason="~16 min of GPU; RD_LONG=2")
-def test_m12_panel_sequential_pins():
-    # m = 12 (N = 566059) on one GPU, 26 panels: Cor 12 (26n/5 for 5 | n) and the
-    # independent row DP X3 for n = 3..10; the conjectured (n0, 5, 26)
-    from paper_2409_17658_b200 import dist as rdist
-    got = rdist.power_sequence_panels(12, 45, alpha_max=5, panel_rows=22528, method=1)
-    assert got["found"] and (got["alpha"], got["beta"]) == (5, 26)
-    d = got["diag"]
-    for n in range(5, got["k_stop"] + 1, 5):
-        assert d[n] == 26 * n // 5, n
-    for n in range(3, 11):
-        assert d[n] == O.gamma_rowdp(12, n), n
-
-
 @pytest.mark.parametrize("M,N,K", [(7, 130, 33), (129, 5, 300)])
 def test_minplus_mul32_ex_strided_guard(M, N, K):
     # leading dimensions larger than the shapes; nothing written outside the N columns of C
