@@ -204,7 +204,7 @@ def test_every_status_entry_is_a_function_try_block():
     C++ exception crosses the ABI (rd.h "Errors")."""
     import re
     csrc = os.path.join(ROOT, "paper_2409_17658_b200", "csrc")
-    plain = {"rd_stats_len", "rd_stats_decide", "rd_chain_current_k"}   # no allocation, no status
+    plain = {"rd_stats_len", "rd_stats_decide", "rd_chain_current_k", "rd_chain_gemm_variant"}   # accessors, no status
     for fn in ("rd_cuda.cu", "rd_host.cpp"):
         src = open(os.path.join(csrc, fn)).read()
         for mt in re.finditer(r'extern "C" int (rd_[a-z0-9_]+)\(', src):
