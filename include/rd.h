@@ -369,11 +369,6 @@ int rd_set_gemm_tile(int tn);
  * "Wave quantisation".  Errors: RD_EINVAL. */
 int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, double *cost);
 
-/* rd_set_stats_prefetch — process-wide switch (default 1): a dense chain step's CTAs ask L2 for
- * the earlier powers' chunks of their tile a few stages before the tile ends, so the fused
- * periodicity stats (Alg 2 step 4) read them from L2.  Identical results.  Always RD_OK. */
-int rd_set_stats_prefetch(int enable);
-
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
  * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
  * counted on an mbarrier; the warps release stages on a second mbarrier); without, every

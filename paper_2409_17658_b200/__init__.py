@@ -88,8 +88,6 @@ def lib():
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_stream_k.argtypes = [ci]
         L.rd_set_gemm_tile.argtypes = [ci]
-        L.rd_set_stats_prefetch.argtypes = [ci]
-        L.rd_set_stats_prefetch.restype = ci
         L.rd_dense_step_plan.argtypes = [i64, i64, ci, p, p, p]
         L.rd_dense_step_plan.restype = ci
         L.rd_set_gemm_tile.restype = ci
@@ -360,11 +358,6 @@ def rd_dense_step_plan(rows: int, N: int, sms: int = 148):
     tile, ns, cost = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
     _check(lib().rd_dense_step_plan(rows, N, sms, ctypes.byref(tile), ctypes.byref(ns), ctypes.byref(cost)))
     return tile.value, ns.value, cost.value
-
-
-def rd_set_stats_prefetch(enable: bool):
-    """L2 prefetch of the fused stats' earlier-power chunks in dense chain steps (rd.h)."""
-    _check(lib().rd_set_stats_prefetch(1 if enable else 0))
 
 
 def rd_set_gemm_tile(tn: int):

@@ -304,7 +304,6 @@ __global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restr
 
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
 int g_dpx_auto = 1;       // long dense chain steps tune 3 vs 4 per chain until rd_set_gemm_variant is called
-int g_stats_prefetch = 1; // rd_set_stats_prefetch: L2 prefetch of the fused stats' earlier-power chunks
 int g_gemm_tile = 0;      // rd_set_gemm_tile: 0 = the chain's wave model picks, 64 / 128 forced
 int g_sparse_bytes = 2;   // rd_set_sparse_bytes: 0 16-bit kernel, 1 byte kernel, 2 slab byte kernel
 
@@ -428,12 +427,6 @@ extern "C" int rd_set_gemm_variant(int dpx_cols) try {
   g_dpx_auto = 0;   // an explicit choice: no per-chain tuning
   return RD_OK;
 } RD_ABI_CATCH("rd_set_gemm_variant")
-
-extern "C" int rd_set_stats_prefetch(int enable) try {
-  rd_enter();
-  g_stats_prefetch = enable ? 1 : 0;
-  return RD_OK;
-} RD_ABI_CATCH("rd_set_stats_prefetch")
 
 extern "C" int rd_set_gemm_tile(int tn) try {
   rd_enter();
@@ -2645,7 +2638,6 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   for (int a = 1; a <= epi.nprev; ++a) epi.prev[a - 1] = c->slot(knew - a);
   epi.stats = stats_dev;
   epi.diag_row0 = c->r0;
-  epi.l2_prefetch = g_stats_prefetch;
   stats_init_kernel<<<1, 1 + 4 * kMaxAlpha, 0, c->st>>>(stats_dev, c->alpha_max);
   RD_CUDA_CHECK(cudaGetLastError());
   if (c->method == 1 && c->ent8) {

@@ -62,7 +62,6 @@ struct EpiArgs {
   // (store into C, fused stats).  The counters reset themselves.
   uint32_t *split_ws;
   int *split_cnt;
-  int l2_prefetch;         // PM + stats: prefetch the earlier powers' chunks into L2 before the epilogue
   const int *spread_in;    // structured step: 1 if some row of X has a finite spread > 254 (nullable)
   int *spread_out;         // ... the same flag for the output, for the next step (nullable)
   // Stream-K remainder (PM output, DESIGN.md §5 "Wave quantisation"): CTAs [0, sk_nfull)

@@ -192,20 +192,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           }
         }
       }
-      // a few stages before the tile's end, ask L2 for the earlier powers' chunks the fused
-      // periodicity stats will read (no registers held; the epilogue's loads then hit L2)
-      if constexpr (STATS && OUT == kOutPM) {
-        if (epi.l2_prefetch && kb == (KB > 6 ? KB - 6 : 0) && gridDim.y == 1) {
-          for (int a = 0; a < epi.nprev; ++a)
-#pragma unroll
-            for (int gq = 0; gq < 2; ++gq)
-#pragma unroll
-              for (int p = 0; p < NC / 2; ++p) {
-                const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(epi.prev[a] + jp * ldc + i0 + gq * 64 + ty * 4));
-              }
-        }
-      }
     }
     if constexpr (!TMA) cp_async_wait<0>();
   };
