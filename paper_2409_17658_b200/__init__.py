@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librd.so")
+LIB_PATH = os.environ.get("RD_LIB", os.path.join(PKG, "librd.so"))   # RD_LIB: A/B builds (tools/)
 
 RD_INF = 0x3FFF
 RD_STAT_NONE = 2**31 - 1
