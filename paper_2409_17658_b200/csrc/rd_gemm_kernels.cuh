@@ -354,11 +354,13 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 
   // periodicity stats against A^{k+1-a}: same PM address in the previous slots
   uint4 pv[2][NC / 2];
-  uint32_t out_inf = 0;   // some lane of this thread's output is inf
+  uint32_t out_inf = 0;   // some lane of this thread's output is inf (TMA instance's fast path)
+  if constexpr (TMA) {
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int p = 0; p < NC / 2; ++p) out_inf |= __vcmpeq2(out[r][p], kInf2);
+      for (int p = 0; p < NC / 2; ++p) out_inf |= __vcmpeq2(out[r][p], kInf2);
+  }
   if constexpr (OUT != kOutRP) {
     if (epi.nprev > 0) {
 #pragma unroll
@@ -386,7 +388,10 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
             for (int e = 0; e < 4; ++e) stats_pair(rp_word(g, q, h, e), pw[e], lo2, hi2, mis, fin);
           }
-    } else {
+    } else if constexpr (TMA) {
+      // (the TMA instance: one load batch per alpha and an all-finite fast path; the cp.async
+      // instances keep the next-alpha prefetch — each form measured best for its instance,
+      // profiles/r02i_epilogue_fastpath_ab.txt)
       if (a > 0) {
         const uint32_t *Pa = epi.prev[a];
 #pragma unroll
@@ -430,6 +435,32 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
           }
       }
+    } else {
+      // this alpha's chunks were fetched during the previous alpha (pv); fetch the next ones
+      // before folding these, so the earlier powers' loads overlap the reductions
+      uint4 nx[2][NC / 2];
+      if (a + 1 < epi.nprev) {
+        const uint32_t *Pn = epi.prev[a + 1];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int p = 0; p < NC / 2; ++p) {
+            const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+            nx[g][p] = __ldg(reinterpret_cast<const uint4 *>(Pn + jp * ldc + i0 + g * 64 + ty * 4));
+          }
+      }
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int p = 0; p < NC / 2; ++p) {
+          const uint32_t pw[4] = {pv[g][p].x, pv[g][p].y, pv[g][p].z, pv[g][p].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stats_pair(out[g * 4 + q][p], pw[q], lo2, hi2, mis, fin);
+        }
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int p = 0; p < NC / 2; ++p) pv[g][p] = nx[g][p];
     }
     int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
     int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
