@@ -5,6 +5,11 @@
 
 namespace rd {
 
+#ifndef RD_T_UNROLL
+#define RD_T_UNROLL 16   // mainloop k-pair pairs per stage: fully unrolled (A/B builds may pass -DRD_T_UNROLL)
+#endif
+constexpr int kTUnroll = RD_T_UNROLL;
+
 // TN = tile width (columns of C): 128 (thread tile 8 x 8, 2 CTAs/SM) or 64 (8 x 4, 3 CTAs/SM,
 // twice the tiles for the same work: finer wave quantisation).  Accumulator (r, c) of a
 // thread uses the DPX form when (r * NC + c) mod 8 < DPXC (TN = 128: c < DPXC), so both widths
@@ -143,7 +148,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             for (int c = 0; c < NC; ++c) acc[r][c] = __viaddmin_s16x2(x[r], b[c], acc[r][c]);
         }
       } else {
-#pragma unroll
+#pragma unroll kTUnroll
         for (int t = 0; t < kBK2; t += 2) {
           uint32_t x0[8], x1[8], b0[NC], b1[NC];
           {

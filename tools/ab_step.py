@@ -1,0 +1,25 @@
+"""Median m-order dense chain step (CUDA events) for the librd build named by RD_LIB (A/B of
+compile variants, tools/build_ab.sh).  python tools/ab_step.py [m] [steps]"""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+import paper_2409_17658_b200 as rd  # noqa: E402
+
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 9
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+st = torch.cuda.current_stream()
+ch = rd.Chain(m, alpha_max=10, stream=st)
+for _ in range(5):
+    ch.step()
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+for a, b in ev:
+    a.record(st); ch.step(); b.record(st)
+torch.cuda.synchronize()
+t = statistics.median(a.elapsed_time(b) for a, b in ev)
+print(f"{os.path.basename(os.environ.get('RD_LIB', 'librd.so'))} m={m} d={ch.gemm_variant} step {t:.3f} ms "
+      f"({float(ch.N) ** 3 / t / 1e9:.1f} T)", flush=True)
+ch.close()
