@@ -9,6 +9,10 @@ namespace rd {
 #define RD_T_UNROLL 16   // mainloop k-pair pairs per stage: fully unrolled (A/B builds may pass -DRD_T_UNROLL)
 #endif
 constexpr int kTUnroll = RD_T_UNROLL;
+#ifndef RD_DPX_ROW_SHIFT
+#define RD_DPX_ROW_SHIFT 0   // which accumulators take the DPX form: (r * shift + r * NC + c) mod 8 < d
+#endif
+constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
 
 // TN = tile width (columns of C): 128 (thread tile 8 x 8, 2 CTAs/SM) or 64 (8 x 4, 3 CTAs/SM,
 // twice the tiles for the same work: finer wave quantisation).  Accumulator (r, c) of a
@@ -170,7 +174,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           for (int r = 0; r < 8; ++r)
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-              if ((r * NC + c) % 8 < DPXC) {
+              if ((r * kDpxRowShift + r * NC + c) % 8 < DPXC) {
                 acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
                 acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
               } else {
