@@ -1,9 +1,9 @@
 set -u
 O=gpurun_out
 mkdir -p $O
-python -m paper_2409_17658_b200.build > $O/s21_build.log 2>&1; echo "build rc=$?"
+python -m paper_2409_17658_b200.build > $O/s22_build.log 2>&1; echo "build rc=$?"
 for rep in 1 2 3; do
   for v in librd.so librd_sh1.so librd_sh3.so; do
     RD_LIB=$PWD/paper_2409_17658_b200/$v timeout 300 python tools/ab_step.py 9 5
   done
-done > $O/s21_shift_ab.txt 2>&1; cat $O/s21_shift_ab.txt
+done > $O/s22_shift_ab.txt 2>&1; cat $O/s22_shift_ab.txt
