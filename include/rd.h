@@ -363,11 +363,13 @@ int rd_set_gemm_tile(int tn);
 
 /* rd_dense_step_plan — the dense chain step's wave model, for inspection (host only): for a
  * row panel of `rows` rows of an order-N power on a device with `sms` SMs, the tile width
- * (*tile: 128 or 64) and split-K count (*nsplit: 1..8) rd_chain_step will use under the current
- * switches (rd_set_gemm_tile, rd_set_split_k, rd_set_gemm_tma), and the predicted step time
- * (*cost, nullable; units: 128 x 128-tile pipeline stages at full occupancy).
- * "Wave quantisation".  Errors: RD_EINVAL. */
-int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, double *cost);
+ * (*tile: 128 or 64), split-K count (*nsplit: 1..8) and split form (*tail, nullable: 0 = every
+ * tile split nsplit ways, 1 = the whole waves of tiles unsplit and only the tiles of the last,
+ * partial wave split nsplit ways) rd_chain_step will use under the current switches
+ * (rd_set_gemm_tile, rd_set_split_k, rd_set_gemm_tma), and the predicted step time (*cost,
+ * nullable; units: 128 x 128-tile pipeline stages at full occupancy).  DESIGN.md §5 "Wave
+ * quantisation".  Errors: RD_EINVAL. */
+int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, int *tail, double *cost);
 
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
  * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
@@ -386,14 +388,22 @@ int rd_set_gemm_tma(int mode);
  * computes the fused stats (no separate combine pass).  Identical results.  Always RD_OK. */
 int rd_set_split_k(int enable);
 
-/* rd_set_stream_k — process-wide choice for dense chain steps whose last wave of
- * tiles is partial (DESIGN.md §5 "Wave quantisation"): the whole waves run one tile per CTA
- * and the remaining tiles' k-stages are split evenly over every CTA slot (contiguous ranges
- * that cross tile boundaries, "stream-K"); a combine kernel folds the partial tiles, stores
- * them and computes their stats.  mode 0 (default) = never, 1 = when the wave model predicts
- * >= 3%, 2 = whenever the last wave is partial (tests).  Identical results.  Measured slower
- * than the plain / split-K steps on every shape tried, hence off by default.
+/* rd_set_split_tail — process-wide form of dense chain step splits (DESIGN.md §5 "Wave
+ * quantisation"): 0 = every tile split the same number of ways; 1 (default) = the wave model may
+ * also leave the whole waves of tiles unsplit and split only the tiles of the last, partial wave
+ * (one launch; the tiles' last splits finish them in-kernel); 2 = tail splits only (with
+ * rd_set_split_k(n >= 2): the tail tiles split n ways), for probes.  Identical results.
  * RD_EINVAL outside 0..2. */
+int rd_set_split_tail(int mode);
+
+/* rd_set_stream_k — process-wide choice of "stream-K" dense chain steps (DESIGN.md §5 "Wave
+ * quantisation"): CTAs take equal contiguous ranges of k-stages that cross tile boundaries, and
+ * a tile computed in pieces is finished inside the GEMM kernel by its last piece (min over the
+ * partial tiles, store, fused stats).  mode 0 (default) = never; 1 = when the stage-cost model
+ * predicts >= 3% over the wave model's plan; 2 = hybrid whenever the last wave is partial (the
+ * whole waves one tile per CTA, the partial wave's stages spread over every CTA slot); 3 = full
+ * stream-K always (every stage of the step spread over 2 x SMs CTAs).  Identical results.
+ * RD_EINVAL outside 0..3. */
 int rd_set_stream_k(int mode);
 
 /* rd_set_small_chain — process-wide switch (default 1): the dense Algorithm 2 of orders with

@@ -88,12 +88,14 @@ def lib():
         L.rd_set_split_k.argtypes = [ci]
         L.rd_set_stream_k.argtypes = [ci]
         L.rd_set_gemm_tile.argtypes = [ci]
-        L.rd_dense_step_plan.argtypes = [i64, i64, ci, p, p, p]
+        L.rd_dense_step_plan.argtypes = [i64, i64, ci, p, p, p, p]
         L.rd_dense_step_plan.restype = ci
         L.rd_set_gemm_tile.restype = ci
         L.rd_set_small_chain.argtypes = [ci]
         L.rd_set_small_chain.restype = ci
         L.rd_set_stream_k.restype = ci
+        L.rd_set_split_tail.argtypes = [ci]
+        L.rd_set_split_tail.restype = ci
         L.rd_set_gemm_tma.argtypes = [ci]
         L.rd_set_gemm_tma.restype = ci
         L.rd_set_sparse_bytes.argtypes = [ci]
@@ -349,15 +351,22 @@ def rd_set_split_k(enable):
 
 
 def rd_set_stream_k(mode: int):
-    """Stream-K remainder of dense chain steps (rd.h): 0 off (default), 1 model, 2 forced."""
+    """Stream-K dense chain steps (rd.h): 0 off (default), 1 model, 2 hybrid, 3 full."""
     _check(lib().rd_set_stream_k(int(mode)))
 
 
 def rd_dense_step_plan(rows: int, N: int, sms: int = 148):
-    """(tile width, split count, predicted cost) of a dense chain step's wave model (rd.h)."""
-    tile, ns, cost = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-    _check(lib().rd_dense_step_plan(rows, N, sms, ctypes.byref(tile), ctypes.byref(ns), ctypes.byref(cost)))
-    return tile.value, ns.value, cost.value
+    """(tile width, split count, tail-only split, predicted cost) of a dense chain step's wave
+    model (rd.h)."""
+    tile, ns, tail, cost = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check(lib().rd_dense_step_plan(rows, N, sms, ctypes.byref(tile), ctypes.byref(ns), ctypes.byref(tail),
+                                    ctypes.byref(cost)))
+    return tile.value, ns.value, bool(tail.value), cost.value
+
+
+def rd_set_split_tail(mode: int):
+    """Split form of dense chain steps (rd.h): 0 uniform, 1 wave model (default), 2 tail only."""
+    _check(lib().rd_set_split_tail(int(mode)))
 
 
 def rd_set_gemm_tile(tn: int):

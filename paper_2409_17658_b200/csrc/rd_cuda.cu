@@ -226,82 +226,6 @@ __global__ void __launch_bounds__(256) combine_pm_kernel(const uint32_t *__restr
   }
 }
 
-// Stream-K combine: the remainder tiles [nfull, ntiles) of a step whose stream-K CTAs wrote
-// partial PM tiles (segment s at ws + s * stride): one CTA per tile takes the min over the
-// tile's segments, stores the power into the ring slot C and computes its diagonal min and the
-// periodicity stats of every alpha in one pass (the tile is held in registers; HBM/L2-bound).
-__global__ void __launch_bounds__(256) combine_sk_kernel(const uint32_t *__restrict__ ws, int64_t stride,
-                                                         uint32_t *__restrict__ C, int64_t ldc, int nti, int ntj,
-                                                         int kgroup, int KBt, EpiArgs epi) {
-  __shared__ int32_t red[8][1 + 4 * kMaxAlpha];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r = blockIdx.x;
-  const int64_t R = (int64_t)(nti * ntj - epi.sk_nfull) * KBt;
-  const int s0 = sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
-  const int nseg = sk_owner((int64_t)(r + 1) * KBt - 1, R, epi.sk_nsk) - s0 + 1;
-  int64_t i0, j0;
-  tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);
-  // the tile in PM: 64 k-pair rows (jp) of 128 u32 (i); thread: 8 uint4 at rows jr = w*8 + warp
-  uint4 o[8];
-  int32_t dmin = INT_MAX;
-  const int ic = lane * 4;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const int jr = w * 8 + warp;
-    const int64_t e = (j0 / 2 + jr) * ldc + i0 + ic;
-    uint4 v = *reinterpret_cast<const uint4 *>(ws + e);
-    for (int sg = 1; sg < nseg; ++sg) {
-      const uint4 u = *reinterpret_cast<const uint4 *>(ws + (int64_t)sg * stride + e);
-      v.x = __vmins2(v.x, u.x); v.y = __vmins2(v.y, u.y); v.z = __vmins2(v.z, u.z); v.w = __vmins2(v.w, u.w);
-    }
-    *reinterpret_cast<uint4 *>(C + e) = v;
-    o[w] = v;
-    // diagonal (Cor 7): global row diag_row0 + i0 + ic + q meets column j0 + 2 jr + h
-    const uint32_t ow[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t gi = epi.diag_row0 + i0 + ic + q, j = j0 + 2 * jr;
-      if (gi == j) dmin = min(dmin, (int)(ow[q] & 0xFFFF));
-      if (gi == j + 1) dmin = min(dmin, (int)(ow[q] >> 16));
-    }
-  }
-  dmin = __reduce_min_sync(0xffffffffu, dmin);
-  if (lane == 0) red[warp][0] = dmin;
-  for (int a = 0; a < epi.nprev; ++a) {
-    const uint32_t *P = epi.prev[a];
-    uint32_t lo2 = 0x7FFF7FFFu, hi2 = 0x80008000u, mis = 0, fin = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int jr = w * 8 + warp;
-      const uint4 pv = __ldg(reinterpret_cast<const uint4 *>(P + (j0 / 2 + jr) * ldc + i0 + ic));
-      stats_pair(o[w].x, pv.x, lo2, hi2, mis, fin);
-      stats_pair(o[w].y, pv.y, lo2, hi2, mis, fin);
-      stats_pair(o[w].z, pv.z, lo2, hi2, mis, fin);
-      stats_pair(o[w].w, pv.w, lo2, hi2, mis, fin);
-    }
-    int32_t lo = min((int32_t)(int16_t)(lo2 & 0xFFFF), (int32_t)(int16_t)(lo2 >> 16));
-    int32_t hi = max((int32_t)(int16_t)(hi2 & 0xFFFF), (int32_t)(int16_t)(hi2 >> 16));
-    if (!(fin & 0xFFFF) && !(fin >> 16)) { lo = INT_MAX; hi = INT_MIN + 1; }
-    const int32_t v0 = __reduce_min_sync(0xffffffffu, lo);
-    const int32_t v1 = __reduce_min_sync(0xffffffffu, -hi);
-    const int32_t v2 = __reduce_min_sync(0xffffffffu, mis ? -1 : 0);
-    const int32_t v3 = __reduce_min_sync(0xffffffffu, fin ? -1 : 0);
-    if (lane == 0) {
-      red[warp][1 + 4 * a + 0] = v0;
-      red[warp][1 + 4 * a + 1] = v1;
-      red[warp][1 + 4 * a + 2] = v2;
-      red[warp][1 + 4 * a + 3] = v3;
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < 1 + 4 * epi.nprev; e += 256) {
-    int32_t v = red[0][e];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) v = min(v, red[w][e]);
-    atomicMin(epi.stats + e, v);
-  }
-}
-
 int g_dpx_cols = 3;       // rd_set_gemm_variant (default: measured best)
 int g_dpx_auto = 1;       // long dense chain steps tune 3 vs 4 per chain until rd_set_gemm_variant is called
 int g_gemm_tile = 0;      // rd_set_gemm_tile: 0 = the chain's wave model picks, 64 / 128 forced
@@ -2390,7 +2314,9 @@ extern "C" int rd_chain_packed_operand(const rd_chain *c, const uint32_t **bp_de
 static int g_sparse_variant = 3;
 static int g_split_k_off = 0;   // rd_set_split_k(0) disables split-K for small grids
 static int g_split_force = 0;   // rd_set_split_k(n >= 2): every dense step splits K n ways (probes, tests)
-// rd_set_stream_k: 0 (default) off, 1 by the wave model, 2 whenever the last wave is partial
+static int g_split_tail = 1;    // rd_set_split_tail: 0 uniform splits only, 1 model (default), 2 tail only
+// rd_set_stream_k: 0 (default) off, 1 by the stage-cost model, 2 hybrid whenever the last wave is
+// partial, 3 full stream-K always
 static int g_stream_k = 0;
 // rd_set_small_chain: dense Algorithm 2 of orders N <= kSmallMaxN as one device-resident kernel
 static int g_small_chain = 1;
@@ -2401,9 +2327,16 @@ extern "C" int rd_set_small_chain(int enable) try {
   return RD_OK;
 } RD_ABI_CATCH("rd_set_small_chain")
 
+extern "C" int rd_set_split_tail(int mode) try {
+  rd_enter();
+  if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_split_tail: mode must be 0, 1 or 2");
+  g_split_tail = mode;
+  return RD_OK;
+} RD_ABI_CATCH("rd_set_split_tail")
+
 extern "C" int rd_set_stream_k(int mode) try {
   rd_enter();
-  if (mode < 0 || mode > 2) return fail(RD_EINVAL, "rd_set_stream_k: mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return fail(RD_EINVAL, "rd_set_stream_k: mode must be 0..3");
   g_stream_k = mode;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_stream_k")
@@ -2423,14 +2356,14 @@ extern "C" int rd_set_gemm_tma(int mode) try {
 // occupancy, of (tile width, split count); writes the best pair.  Mp = padded panel rows, P =
 // padded order; tile_force 0/64/128; no_split; split_force >= 2 forces n; tma = the TMA
 // mainloop is available for tn = 128, n = 1.
-static double dense_step_plan(int64_t Mp, int64_t P, int sms, int tile_force, int no_split, int split_force, bool tma,
-                              int *tn_out, int *n_out) {
+// tail_mode: 0 = uniform splits only, 1 = uniform or tail splits, 2 = tail splits only (n > 1)
+static double dense_step_plan(int64_t Mp, int64_t P, int sms, int tile_force, int no_split, int split_force,
+                              int tail_mode, bool tma, int *tn_out, int *n_out, int *tail_out) {
   static const double v128[3] = {0.0, 0.676, 1.0}, v64[4] = {0.0, 0.62, 0.90, 0.951};
   const int64_t kstages = (P / 2) / kBK2;
-  auto cost = [&](int w_tn, int n) {
+  // waves of `units` units of work w (in 128-tile stages) on sms x S slots
+  auto waves = [&](int w_tn, int64_t units, double w) {
     const int S = w_tn == 128 ? 2 : 3;
-    const int64_t units = (Mp / kTile) * (P / w_tn) * n;
-    const double w = (w_tn / 128.0) * ((double)kstages / n + 1.5 + (n > 1 ? 0.2 * n : 0.0));
     double t = 0.0;
     for (int64_t left = units; left > 0;) {
       const int64_t u = std::min<int64_t>(left, (int64_t)sms * S);
@@ -2438,30 +2371,53 @@ static double dense_step_plan(int64_t Mp, int64_t P, int sms, int tile_force, in
       const int L = (int)((u + sms - 1) / sms);
       t += L * w / (w_tn == 128 ? v128[L] : v64[L]);
     }
+    return t;
+  };
+  auto work = [&](int w_tn, int n) { return (w_tn / 128.0) * ((double)kstages / n + 1.5 + (n > 1 ? 0.2 * n : 0.0)); };
+  // tail = 0: every tile split n ways; tail = 1: the whole waves unsplit, the remaining tiles
+  // split n ways (< 0: not applicable)
+  auto cost = [&](int w_tn, int n, int tail) {
+    const int64_t tiles = (Mp / kTile) * (P / w_tn);
+    double t;
+    if (!tail) {
+      t = waves(w_tn, tiles * n, work(w_tn, n));
+    } else {
+      const int64_t slots = (int64_t)sms * (w_tn == 128 ? 2 : 3);
+      const int64_t full = tiles / slots * slots;
+      if (full == 0 || full == tiles) return -1.0;
+      t = waves(w_tn, full, work(w_tn, 1)) + waves(w_tn, (tiles - full) * n, work(w_tn, n));
+    }
     if (w_tn == 128 && n == 1 && kstages >= 128 && tma) t *= 0.99;
     return t;
   };
   double best = -1.0;
   *tn_out = 128;
   *n_out = 1;
+  *tail_out = 0;
   for (int w_tn : {128, 64}) {
     if (tile_force && w_tn != tile_force) continue;
     for (int n = 1; n <= 8 && (n == 1 || kstages >= 2 * n); ++n) {
       if (no_split && n > 1) break;
       if (split_force && n != std::min<int64_t>(split_force, std::max<int64_t>(1, kstages / 2))) continue;
-      const double t = cost(w_tn, n);
-      if (best < 0.0 || t < best) { best = t; *tn_out = w_tn; *n_out = n; }
+      for (int tail = 0; tail <= (n > 1 ? 1 : 0); ++tail) {
+        if (tail ? tail_mode == 0 : (tail_mode == 2 && n > 1)) continue;
+        const double t = cost(w_tn, n, tail);
+        if (t < 0.0) continue;
+        if (best < 0.0 || t < best) { best = t; *tn_out = w_tn; *n_out = n; *tail_out = tail; }
+      }
     }
   }
   return best;
 }
 
-extern "C" int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, double *cost) try {
+extern "C" int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, int *tail, double *cost) try {
   rd_enter();
   if (rows < 1 || N < 1 || rows > N || sms < 1 || !tile || !nsplit)
     return fail(RD_EINVAL, "rd_dense_step_plan: need 1 <= rows <= N, sms >= 1, non-NULL outputs");
+  int tl = 0;
   const double t = dense_step_plan(round_up(rows, kTile), round_up(N, kTile), sms, g_gemm_tile, g_split_k_off ? 1 : 0,
-                                   g_split_force, g_gemm_tma == 1 || g_gemm_tma == 3, tile, nsplit);
+                                   g_split_force, g_split_tail, g_gemm_tma == 1 || g_gemm_tma == 3, tile, nsplit, &tl);
+  if (tail) *tail = tl;
   if (cost) *cost = t;
   return RD_OK;
 } RD_ABI_CATCH("rd_dense_step_plan")
@@ -2628,6 +2584,16 @@ extern "C" double rd_chain_terms_per_step(const rd_chain *c) {
   return c->method == 0 ? (double)c->Mr * (double)c->N * (double)c->N : (double)c->Mr * (double)c->nnz;
 }
 
+// per-tile tickets of the in-kernel fixup (split-K / stream-K), zeroed once; the kernel's last
+// piece of each tile resets its counter
+static int chain_tile_counters(rd_chain *c) {
+  if (c->tile_cnt) return RD_OK;
+  const int64_t max_tiles = (c->Mp / kTile) * (c->P / 64);
+  RD_CUDA_CHECK(chain_malloc(c, &c->tile_cnt, (size_t)max_tiles * 4));
+  RD_CUDA_CHECK(cudaMemsetAsync(c->tile_cnt, 0, (size_t)max_tiles * 4, c->st));
+  return RD_OK;
+}
+
 extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   rd_enter();
   NvtxRange nvtx_range(c && c->method == 1 ? "rd_chain_step structured" : "rd_chain_step");
@@ -2690,29 +2656,34 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   // (profiles/r02_wave_probe.txt): it picks the measured best or within 2% for m = 6..9 and
   // row panels of 1..8 ranks.  The TMA mainloop (tn = 128, n = 1, >= 128 stages) counts 1% faster.
   //
-  // Stream-K remainder (g_stream_k, off by default: measured slower on every shape): the whole
-  // waves of 128-tiles run as usual and the last partial wave's k-stages are spread evenly over
-  // every CTA slot; combine_sk_kernel folds the partial tiles and computes their stats.
+  // Stream-K (g_stream_k): CTAs share contiguous k-stage ranges that cross tile boundaries;
+  // a tile computed in pieces is finished in-kernel by its last piece (partials in c->ws,
+  // tickets in c->tile_cnt).  Hybrid (mode 2): the whole waves of 128-tiles run one tile per
+  // CTA and only the last partial wave's k-stages are spread over every CTA slot.  Full
+  // (mode 3): every k-stage of the step is spread over the 2 x SMs CTA slots.  Mode 1 = the
+  // cheaper of the wave model's plan and full stream-K by the same stage-cost model.
   const int64_t ntiles = (c->Mp / kTile) * (c->P / kTile);
   const int64_t kstages = (c->P / 2) / kBK2;
-  int nsplit = 1, sk_nfull = 0, sk_nsk = 0, tn = 128;
+  int nsplit = 1, sk_nfull = 0, sk_nsk = 0, tn = 128, tail = 0, sms = 148;
   {
-    int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const double best = dense_step_plan(c->Mp, c->P, sms, g_gemm_tile, g_split_k_off ? 1 : 0, g_split_force,
-                                        g_gemm_tma == 1 || g_gemm_tma == 3, &tn, &nsplit);
+                                        g_split_tail, g_gemm_tma == 1 || g_gemm_tma == 3, &tn, &nsplit, &tail);
     const int64_t slots = 2 * (int64_t)sms;
     const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
-    if (g_stream_k && rem > 0) {
-      const double t_stage = 8.2e-6, bw = 6.0e12, tile_bytes = 4.0 * kTile * kTile / 2;
-      const int64_t R = rem * kstages;
-      const int nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, R / 4));   // >= 4 stages each
-      const double per = (double)((R + nsk - 1) / nsk);
+    if (g_stream_k == 2 && rem > 0) {
+      nsplit = 1; tn = 128; tail = 0; sk_nfull = (int)(full_waves * slots);
+      sk_nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, rem * kstages / 4));   // >= 4 stages each
+    } else if (g_stream_k == 3 || (g_stream_k == 1 && ntiles > 1)) {
+      // full stream-K: per CTA ceil(T / slots) stages, a fill + fixup per segment (<= 3)
+      const int64_t T = ntiles * kstages;
+      const int nsk = (int)std::max<int64_t>(1, std::min<int64_t>(slots, T / 4));
+      const double per = (double)((T + nsk - 1) / nsk);
       const double segs = std::min(3.0, 1.0 + per / (double)kstages + 1.0);
-      double t = (double)full_waves * ((double)kstages + 1.5) + per + 2.0 * segs;
-      t += (double)rem * tile_bytes * (segs + 2 + epi.nprev) / bw / t_stage;
-      if (g_stream_k == 2 || t < best) {
-        nsplit = 1; tn = 128; sk_nfull = (int)(full_waves * slots); sk_nsk = nsk;
+      const int L = (int)((nsk + sms - 1) / sms);   // resident CTAs on the busiest SM (<= 2)
+      const double t = L * (per + 1.7 * segs) / (L == 1 ? 0.676 : 1.0);   // dense_step_plan's units
+      if (g_stream_k == 3 || t < best * 0.97) {
+        nsplit = 1; tn = 128; tail = 0; sk_nfull = 0; sk_nsk = nsk;
       }
     }
   }
@@ -2733,17 +2704,15 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
       RD_CUDA_CHECK(chain_malloc(c, &c->ws, (size_t)maxseg * c->slot_words * 4));
       c->nsplit = maxseg;
     }
+    if (int rc = chain_tile_counters(c)) return rc;
     epi.sk_nfull = sk_nfull;
     epi.sk_nsk = sk_nsk;
-    epi.sk_ws = c->ws;
-    epi.sk_stride = c->slot_words;
+    epi.split_ws = c->ws;
+    epi.split_stride = c->slot_words;
+    epi.split_cnt = c->tile_cnt;
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
                                      c->N, c->Mp, c->P, epi, c->st, 1, tma);
     if (rc != RD_OK) return rc;
-    combine_sk_kernel<<<(unsigned)(ntiles - sk_nfull), 256, 0, c->st>>>(
-        c->ws, c->slot_words, c->slot(knew), c->Mp, (int)(c->Mp / kTile), (int)(c->P / kTile), g_raster_group,
-        (int)kstages, epi);
-    RD_CUDA_CHECK(cudaGetLastError());
   } else if (nsplit == 1) {
     // the DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
     // §5), so a chain of long TMA steps times one step with each and keeps the faster
@@ -2779,16 +2748,17 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
       RD_CUDA_CHECK(chain_malloc(c, &c->ws, (size_t)nsplit * c->slot_words * 4));
       c->nsplit = nsplit;
     }
-    const int64_t max_tiles = (c->Mp / kTile) * (c->P / 64);
-    if (!c->tile_cnt) {
-      RD_CUDA_CHECK(chain_malloc(c, &c->tile_cnt, (size_t)max_tiles * 4));
-      RD_CUDA_CHECK(cudaMemsetAsync(c->tile_cnt, 0, (size_t)max_tiles * 4, c->st));
-    }
+    if (int rc = chain_tile_counters(c)) return rc;
     epi.split_stride = c->slot_words;
     epi.split_ws = c->ws;
     epi.split_cnt = c->tile_cnt;
+    if (tail) {   // the whole waves unsplit, the remaining tiles split nsplit ways
+      const int64_t tiles = (c->Mp / kTile) * (c->P / tn), slots = (int64_t)sms * (tn == 128 ? 2 : 3);
+      epi.tail_nfull = (int)(tiles / slots * slots);
+      epi.tail_split = nsplit;
+    }
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st, nsplit, tma, tn);
+                                     c->N, c->Mp, c->P, epi, c->st, tail ? 1 : nsplit, tma, tn);
     if (rc != RD_OK) return rc;
   }
   c->k = knew;

@@ -62,16 +62,17 @@ struct EpiArgs {
   // (store into C, fused stats).  The counters reset themselves.
   uint32_t *split_ws;
   int *split_cnt;
+  // tail split (classic CTAs, split_cnt set, tail_split >= 2): CTAs [0, tail_nfull) compute
+  // whole tiles 0..tail_nfull-1 (the whole waves); the tiles after them are split tail_split
+  // ways, CTA tail_nfull + u computing split u % tail_split of tile tail_nfull + u / tail_split
+  int tail_nfull, tail_split;
   const int *spread_in;    // structured step: 1 if some row of X has a finite spread > 254 (nullable)
   int *spread_out;         // ... the same flag for the output, for the next step (nullable)
-  // Stream-K remainder (PM output, DESIGN.md §5 "Wave quantisation"): CTAs [0, sk_nfull)
-  // compute whole tiles 0..sk_nfull-1 (fused stats); the sk_nsk CTAs after them share the
-  // R = (ntiles - sk_nfull) * KBt k-stages of the remaining tiles in equal contiguous ranges,
-  // writing partial tiles (segment s of a tile to sk_ws + s * sk_stride, at the tile's PM
-  // offsets) that combine_sk_kernel folds.  sk_nsk = 0: every CTA computes one whole tile.
+  // Stream-K (PM output with stats, DESIGN.md §5 "Wave quantisation"): CTAs [0, sk_nfull)
+  // compute whole tiles 0..sk_nfull-1; the sk_nsk CTAs after them share the R = (ntiles -
+  // sk_nfull) * KBt k-stages of the remaining tiles in equal contiguous ranges, finishing each
+  // tile in-kernel through split_ws / split_cnt.  sk_nsk = 0: every CTA computes one whole tile.
   int sk_nfull, sk_nsk;
-  uint32_t *sk_ws;
-  int64_t sk_stride;
 };
 
 // Tile t of the grid in rasterised order (groups of kgroup row-tiles share right-operand

@@ -10,7 +10,7 @@ namespace rd {
 #endif
 constexpr int kTUnroll = RD_T_UNROLL;
 #ifndef RD_DPX_ROW_SHIFT
-#define RD_DPX_ROW_SHIFT 0   // which accumulators take the DPX form: (r * shift + r * NC + c) mod 8 < d
+#define RD_DPX_ROW_SHIFT 1   // which accumulators take the DPX form: (r * shift + r * NC + c) mod 8 < d
 #endif
 constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
 
@@ -230,70 +230,90 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       }
   };
 
+  // Work units.  Classic CTA: one whole tile (split-K: the k-range blockIdx.y of gridDim.y).
+  // Stream-K CTA (SK, blockIdx.x >= sk_nfull): an equal contiguous share of the remaining
+  // tiles' k-stages, walked segment by segment (a segment = the part of the range inside one
+  // tile).  A tile computed in several pieces (split-K splits or stream-K segments) is finished
+  // in-kernel: every piece stores its partial tile to split_ws + seg * split_stride and takes a
+  // ticket on split_cnt[tile]; the last one folds the others' partials into its registers and
+  // runs the ordinary epilogue (store into C, fused stats).  The counters reset themselves.
+  __shared__ int s_last;
+  __shared__ int32_t red[kThreads / 32][1 + 4 * kMaxAlpha];
   int64_t i0, j0;
-  if constexpr (SK && OUT == kOutPM) {
-    if ((int)blockIdx.x >= epi.sk_nfull) {
-      // stream-K CTA: its share of the remainder's k-stage iterations, one partial tile per
-      // segment (a segment = the part of the range inside one tile)
-      const int c = (int)blockIdx.x - epi.sk_nfull;
-      const int64_t R = (int64_t)(nti * ntj - epi.sk_nfull) * KBt;
-      const int64_t e0 = sk_begin(c, R, epi.sk_nsk), e1 = sk_begin(c + 1, R, epi.sk_nsk);
-      uint32_t it = 0;
-      for (int64_t e = e0; e < e1;) {
-        const int r = (int)(e / KBt);
-        const int kb0 = (int)(e - (int64_t)r * KBt);
-        const int KB = (int)((e1 - e) < (int64_t)(KBt - kb0) ? (e1 - e) : (int64_t)(KBt - kb0));
-        const int seg = c - sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
-        tile_origin(epi.sk_nfull + r, nti, ntj, kgroup, i0, j0);   // SK: TN = 128
-        if (it > 0 && !TMA) __syncthreads();   // every warp is done with the previous segment's stages
-        mainloop(i0, j0, kb0, KB, it);
-        fold();
-        store_pm(epi.sk_ws + (int64_t)seg * epi.sk_stride, i0, j0);
-        it += (uint32_t)KB;
-        e += KB;
+  const bool skc = SK && (int)blockIdx.x >= epi.sk_nfull;
+  int64_t ke = 0, ke1 = 0, R = 0;
+  int skid = 0;
+  if (skc) {
+    skid = (int)blockIdx.x - epi.sk_nfull;
+    R = (int64_t)(nti * ntj - epi.sk_nfull) * KBt;
+    ke = sk_begin(skid, R, epi.sk_nsk);
+    ke1 = sk_begin(skid + 1, R, epi.sk_nsk);
+  }
+  uint32_t it = 0;
+  for (;;) {
+    int kb0, KB, seg, nseg, tile;
+    if (skc) {
+      if (ke >= ke1) return;
+      const int r = (int)(ke / KBt);
+      kb0 = (int)(ke - (int64_t)r * KBt);
+      KB = (int)((ke1 - ke) < (int64_t)(KBt - kb0) ? (ke1 - ke) : (int64_t)(KBt - kb0));
+      const int own0 = sk_owner((int64_t)r * KBt, R, epi.sk_nsk);
+      seg = skid - own0;
+      nseg = sk_owner((int64_t)r * KBt + KBt - 1, R, epi.sk_nsk) - own0 + 1;
+      tile = epi.sk_nfull + r;
+      tile_origin(tile, nti, ntj, kgroup, i0, j0);   // SK: TN = 128
+      if (it > 0 && !TMA) __syncthreads();   // every warp is done with the previous segment's stages
+    } else {
+      tile = (int)blockIdx.x;
+      seg = (int)blockIdx.y;
+      nseg = (int)gridDim.y;
+      if (epi.tail_split > 1 && tile >= epi.tail_nfull) {   // a split of a tail tile
+        const int u = tile - epi.tail_nfull;
+        tile = epi.tail_nfull + u / epi.tail_split;
+        seg = u - (tile - epi.tail_nfull) * epi.tail_split;
+        nseg = epi.tail_split;
       }
-      return;
+      tile_origin(tile, nti, ntj, kgroup, i0, j0);
+      if constexpr (TN != kTile) j0 = j0 / kTile * TN;
+      kb0 = (int)((int64_t)KBt * seg / nseg);
+      KB = (int)((int64_t)KBt * (seg + 1) / nseg) - kb0;
     }
-  }
-  // classic CTA: one whole tile (or, split-K, the k-range blockIdx.y of gridDim.y)
-  tile_origin((int)blockIdx.x, nti, ntj, kgroup, i0, j0);
-  if constexpr (TN != kTile) j0 = j0 / kTile * TN;
-  {
-    const int kb0 = (int)((int64_t)KBt * blockIdx.y / gridDim.y);
-    const int KB = (int)((int64_t)KBt * (blockIdx.y + 1) / gridDim.y) - kb0;
-    mainloop(i0, j0, kb0, KB, 0);
-  }
-  fold();
-  bool fixed_up = false;
-  if constexpr (OUT == kOutPM && STATS) {
-    if (gridDim.y > 1 && epi.split_cnt) {   // split-K: the last CTA of the tile finishes it
-      __shared__ int s_last;
-      store_pm(epi.split_ws + (int64_t)blockIdx.y * epi.split_stride, i0, j0);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) s_last = atomicAdd(&epi.split_cnt[blockIdx.x], 1) == (int)gridDim.y - 1;
-      __syncthreads();
-      if (!s_last) return;
-      __threadfence();
-      for (int sp = 0; sp < (int)gridDim.y; ++sp) {
-        if (sp == (int)blockIdx.y) continue;
-        const uint32_t *W = epi.split_ws + (int64_t)sp * epi.split_stride;
+    mainloop(i0, j0, kb0, KB, it);
+    it += (uint32_t)KB;
+    ke += KB;
+    fold();
+    bool fixed_up = false;
+    if constexpr (OUT == kOutPM && STATS) {
+      if (nseg > 1 && epi.split_cnt) {   // the last piece of the tile finishes it
+        store_pm(epi.split_ws + (int64_t)seg * epi.split_stride, i0, j0);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(&epi.split_cnt[tile], 1) == nseg - 1;
+        __syncthreads();
+        if (!s_last) {
+          if (skc) continue;
+          return;
+        }
+        __threadfence();
+        for (int sp = 0; sp < nseg; ++sp) {
+          if (sp == seg) continue;
+          const uint32_t *W = epi.split_ws + (int64_t)sp * epi.split_stride;
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
+          for (int g = 0; g < 2; ++g)
 #pragma unroll
-          for (int p = 0; p < NC / 2; ++p) {
-            const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-            const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(W + jp * ldc + i0 + g * 64 + ty * 4));
-            out[g * 4 + 0][p] = __vmins2(out[g * 4 + 0][p], w.x);
-            out[g * 4 + 1][p] = __vmins2(out[g * 4 + 1][p], w.y);
-            out[g * 4 + 2][p] = __vmins2(out[g * 4 + 2][p], w.z);
-            out[g * 4 + 3][p] = __vmins2(out[g * 4 + 3][p], w.w);
-          }
+            for (int p = 0; p < NC / 2; ++p) {
+              const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
+              const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(W + jp * ldc + i0 + g * 64 + ty * 4));
+              out[g * 4 + 0][p] = __vmins2(out[g * 4 + 0][p], w.x);
+              out[g * 4 + 1][p] = __vmins2(out[g * 4 + 1][p], w.y);
+              out[g * 4 + 2][p] = __vmins2(out[g * 4 + 2][p], w.z);
+              out[g * 4 + 3][p] = __vmins2(out[g * 4 + 3][p], w.w);
+            }
+        }
+        if (tid == 0) epi.split_cnt[tile] = 0;   // ready for the next step
+        fixed_up = true;
       }
-      if (tid == 0) epi.split_cnt[blockIdx.x] = 0;   // ready for the next step
-      fixed_up = true;
     }
-  }
 
   // RP word (rows 2q', 2q'+1 of row group g; columns h*64 + tx*4 + e) from the folded pairs
   auto rp_word = [&](int g, int q, int h, int e) -> uint32_t {
@@ -337,7 +357,6 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
   if (!STATS) return;
 
   // ---- fused reductions over this tile (MIN-reducible; see rd.h rd_chain_step) ----
-  __shared__ int32_t red[kThreads / 32][1 + 4 * kMaxAlpha];
   const int warp = tid >> 5, lane = tid & 31;
 
   // diagonal min (Cor 7): global row diag_row0 + i == column j
@@ -493,6 +512,9 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
     for (int w = 1; w < kThreads / 32; ++w) v = min(v, red[w][e]);
     atomicMin(epi.stats + e, v);
   }
+  if (!skc) return;
+  __syncthreads();   // red[] and the stage buffers are reused by the next segment
+  }
 }
 
 // ----------------------------------------------------------- 32-bit GEMM --
@@ -626,7 +648,10 @@ int launch_gemm_v(const uint32_t *XT, int64_t ldx, const uint32_t *BP, int64_t l
   TmaOps t{};
   if (tma) t = *tma;
   // stream-K steps: sk_nfull whole-tile CTAs, then sk_nsk CTAs sharing the remaining tiles
-  const unsigned gx = SK ? (unsigned)(epi.sk_nfull + epi.sk_nsk) : (unsigned)(nti * ntj);
+  // tail-split steps: tail_nfull whole-tile CTAs, then tail_split CTAs per remaining tile
+  const unsigned gx = SK ? (unsigned)(epi.sk_nfull + epi.sk_nsk)
+                    : epi.tail_split > 1 ? (unsigned)(epi.tail_nfull + (nti * ntj - epi.tail_nfull) * epi.tail_split)
+                                         : (unsigned)(nti * ntj);
   minplus_gemm_kernel<OUT, STATS, DPXC, TMA, SK, TN><<<dim3(gx, (unsigned)nsplit), kThreads, smem, st>>>(
       XT, ldx, BP, ldb, (int)kpairs, C, ldc, M, N, nti, ntj, 1u, epi, g_raster_group, pb, t);
   RD_CUDA_CHECK(cudaGetLastError());

@@ -544,16 +544,48 @@ def test_split_k_equals_single_pass(m, r0, r1):
     assert (outs[0][1] == outs[1][1]).all()
 
 
+@pytest.mark.parametrize("m,r0,r1,tn,n", [(7, 0, 2507, 128, 2), (7, 0, 2507, 64, 3), (8, 0, 1024, 128, 5),
+                                         (8, 0, 1024, 64, 2)])
+def test_tail_split_equals_single_pass(m, r0, r1, tn, n):
+    """Tail splits (rd_set_split_tail(2): the whole waves unsplit, the last partial wave's tiles
+    split n ways and finished in-kernel by their last split) give every power and stats vector of
+    the plain step, and the powers equal the oracle's for m <= 7."""
+    outs = []
+    try:
+        for tail in (True, False):
+            rd.rd_set_gemm_tile(tn)
+            rd.rd_set_split_tail(2 if tail else 0)
+            rd.rd_set_split_k(n if tail else 0)
+            if tail:
+                assert rd.rd_dense_step_plan(r1 - r0, rd.count_words(m))[:3] == (tn, n, True)
+            ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
+            st = [ch.step().cpu().numpy() for _ in range(2, 13)]
+            outs.append((st, {k: ch.read_rows(k) for k in (8, 12)}))
+            ch.close()
+    finally:
+        rd.rd_set_gemm_tile(0)
+        rd.rd_set_split_tail(1)
+        rd.rd_set_split_k(True)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert (a == b).all()
+    for k in outs[0][1]:
+        assert (outs[0][1][k] == outs[1][1][k]).all(), k
+    if m <= 7:
+        P = {k: X for k, X in O.powers(m, 12) if k == 12}
+        assert (outs[0][1][12] == to_inf(P[12][r0:r1], OINF, RINF, np.int16)).all()
+
+
 @pytest.mark.parametrize("m,r0,r1", [(3, 0, 33), (5, 0, 287), (6, 0, 848), (7, 0, 2507), (7, 128, 1000),
                                      (8, 3712, 4736)])
 def test_stream_k_equals_oracle_and_single_pass(m, r0, r1):
-    """Stream-K remainder (rd_set_stream_k(2): forced whenever the last wave is partial): every
-    power and every stats vector equal the plain one-tile-per-CTA step, and the powers equal the
+    """Stream-K steps with the in-kernel fixup — hybrid (rd_set_stream_k(2): the partial last
+    wave's stages spread over every CTA slot) and full (3: every stage of the step) — give every
+    power and every stats vector of the plain one-tile-per-CTA step, and the powers equal the
     oracle's on the full matrix for m <= 7."""
     outs = []
     rd.rd_set_split_k(False)
     try:
-        for mode in (2, 0):
+        for mode in (2, 3, 0):
             rd.rd_set_stream_k(mode)
             ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
             st, rows = [], {}
@@ -566,10 +598,11 @@ def test_stream_k_equals_oracle_and_single_pass(m, r0, r1):
     finally:
         rd.rd_set_stream_k(0)
         rd.rd_set_split_k(True)
-    for a, b in zip(outs[0][0], outs[1][0]):
-        assert (a == b).all()
-    for k in outs[0][1]:
-        assert (outs[0][1][k] == outs[1][1][k]).all(), k
+    for o in outs[:2]:
+        for a, b in zip(o[0], outs[2][0]):
+            assert (a == b).all()
+        for k in o[1]:
+            assert (o[1][k] == outs[2][1][k]).all(), k
     if m <= 7:
         P = {k: X for k, X in O.powers(m, 12) if k in (2, 5, 12)}
         for k, X in P.items():

@@ -1,6 +1,6 @@
 """Dense step time (median of 10, CUDA events) per order and row panel under the wave
-strategies: plain (one tile per CTA), split-K (uniform), stream-K remainder (forced), and the
-library's default model choice."""
+strategies: plain (one tile per CTA), split-K (wave model's count), 64-wide tiles, stream-K
+hybrid (mode 2) and full (mode 3) with the in-kernel fixup, and the library's default plan."""
 import statistics
 import sys
 
@@ -24,8 +24,9 @@ def med(m, r0, r1, reps=10):
     return statistics.median(a.elapsed_time(b) for a, b in ev)
 
 
-MODES = {"plain": (False, 0, 128), "splitk": (True, 0, 128), "t64": (False, 0, 64), "t64split": (True, 0, 64)}
-cases = [(6, 1), (7, 1), (7, 2), (8, 1), (8, 2), (8, 4), (8, 8), (9, 1), (9, 8)]
+MODES = {"plain": (False, 0, 128), "splitk": (True, 0, 128), "t64": (False, 0, 64), "t64split": (True, 0, 64),
+         "sk_hybrid": (False, 2, 128), "sk_full": (False, 3, 128), "default": (True, 0, 0)}
+cases = [(6, 1), (7, 1), (7, 2), (7, 4), (8, 1), (8, 2), (8, 4), (8, 8), (9, 8)]
 if len(sys.argv) > 1:
     cases = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]]
 for m, parts in cases:

@@ -1,6 +1,8 @@
 """Dense chain step time (median of 10, CUDA events) per order / row panel under forced tile
-widths (128, 64) and split-K counts (1..4, in-kernel fixup), plus the library's default choice:
-the data behind the wave model of rd_chain_step (DESIGN.md §5 "Wave quantisation")."""
+widths (128, 64), split-K counts (1..4, every tile split; in-kernel fixup) and tail splits
+(2..6: the whole waves unsplit, the last partial wave's tiles split), plus the library's
+default choice: the data behind the wave model of rd_chain_step (DESIGN.md §5 "Wave
+quantisation")."""
 import statistics
 import sys
 
@@ -35,12 +37,19 @@ for m, parts in cases:
     for tn in (128, 64):
         rd.rd_set_gemm_tile(tn)
         rd.rd_set_gemm_tma(0)
+        rd.rd_set_split_tail(0)
         for n in (1, 2, 3, 4):
             rd.rd_set_split_k(0 if n == 1 else n)
             res[f"t{tn}/s{n}"] = med(m, r0, r1, reps=10 if m < 9 else 3)
+        rd.rd_set_split_tail(2)
+        for n in (2, 3, 4, 5, 6):
+            rd.rd_set_split_k(n)
+            if rd.rd_dense_step_plan(r1 - r0, N)[2]:   # a tail exists
+                res[f"t{tn}/tail{n}"] = med(m, r0, r1, reps=10 if m < 9 else 3)
     rd.rd_set_gemm_tile(0)
     rd.rd_set_gemm_tma(1)
     rd.rd_set_split_k(1)
+    rd.rd_set_split_tail(1)
     res["default"] = med(m, r0, r1, reps=10 if m < 9 else 3)
     best = min(res, key=res.get)
     print(f"m={m} p={parts} rows=[{r0},{r1}) best {best} " +
