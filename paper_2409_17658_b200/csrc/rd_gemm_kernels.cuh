@@ -13,6 +13,9 @@ constexpr int kTUnroll = RD_T_UNROLL;
 #define RD_DPX_ROW_SHIFT 1   // which accumulators take the DPX form: (r * shift + r * NC + c) mod 8 < d
 #endif
 constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
+#ifndef RD_EPI_OPAQUE
+#define RD_EPI_OPAQUE 1   // 1: the TMA epilogue re-reads `out` per alpha (nothing hoisted: no spills)
+#endif
 
 // TN = tile width (columns of C): 128 (thread tile 8 x 8, 2 CTAs/SM) or 64 (8 x 4, 3 CTAs/SM,
 // twice the tiles for the same work: finer wave quantisation).  Accumulator (r, c) of a
@@ -422,14 +425,23 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       // profiles/r02i_epilogue_fastpath_ab.txt)
       if (a > 0) {
         const uint32_t *Pa = epi.prev[a];
+        const int64_t ldc_a = ldc;
 #pragma unroll
         for (int g = 0; g < 2; ++g)
 #pragma unroll
           for (int p = 0; p < NC / 2; ++p) {
             const int64_t jp = (j0 + (p >> 1) * 64 + tx * 4 + (p & 1) * 2) >> 1;
-            pv[g][p] = __ldg(reinterpret_cast<const uint4 *>(Pa + jp * ldc + i0 + g * 64 + ty * 4));
+            pv[g][p] = __ldg(reinterpret_cast<const uint4 *>(Pa + jp * ldc_a + i0 + g * 64 + ty * 4));
           }
       }
+#if RD_EPI_OPAQUE
+      // keep ptxas from hoisting the slow path's per-word inf masks of `out` out of the alpha
+      // loop (32 loop-invariant registers, spilled at the 128-register cap)
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int p = 0; p < NC / 2; ++p) asm volatile("" : "+r"(out[r][p]));
+#endif
       // all-finite fast path (every power from k = 4 on): one inf test over this alpha's chunks,
       // then 3 instructions per word instead of stats_pair's 8
       uint32_t iw = out_inf;
