@@ -13,6 +13,10 @@ constexpr int kTUnroll = RD_T_UNROLL;
 #define RD_DPX_ROW_SHIFT 1   // which accumulators take the DPX form: (r * shift + r * NC + c) mod 8 < d
 #endif
 constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
+#ifndef RD_EPI_FAST_ALL
+#define RD_EPI_FAST_ALL 1   // 0: the cp.async instances keep the next-alpha prefetch form (A/B)
+#endif
+constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
 #ifndef RD_EPI_OPAQUE
 #define RD_EPI_OPAQUE 1   // 1: the TMA epilogue re-reads `out` per alpha (nothing hoisted: no spills)
 #endif
@@ -385,8 +389,8 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 
   // periodicity stats against A^{k+1-a}: same PM address in the previous slots
   uint4 pv[2][NC / 2];
-  uint32_t out_inf = 0;   // some lane of this thread's output is inf (TMA instance's fast path)
-  if constexpr (TMA) {
+  uint32_t out_inf = 0;   // some lane of this thread's output is inf (the fast path's test)
+  if constexpr (TMA || kEpiFastAll) {
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -419,10 +423,11 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
             for (int e = 0; e < 4; ++e) stats_pair(rp_word(g, q, h, e), pw[e], lo2, hi2, mis, fin);
           }
-    } else if constexpr (TMA) {
-      // (the TMA instance: one load batch per alpha and an all-finite fast path; the cp.async
-      // instances keep the next-alpha prefetch — each form measured best for its instance,
-      // profiles/r02i_epilogue_fastpath_ab.txt)
+    } else if constexpr (TMA || kEpiFastAll) {
+      // one load batch per alpha and an all-finite fast path, `out` kept opaque per alpha
+      // (RD_EPI_OPAQUE).  Without the opaque marks this form cost the cp.async instances 4.6 %
+      // (profiles/r02i_epilogue_fastpath_ab.txt); with them it gains 1.0 % (TMA, m = 9) and
+      // 1.1 % (cp.async, m = 8): profiles/r02l_epi_opaque_ab.txt, r02l_epi_fastall_ab.txt
       if (a > 0) {
         const uint32_t *Pa = epi.prev[a];
         const int64_t ldc_a = ldc;
