@@ -106,6 +106,10 @@ def test_argument_validation_host_paths():
     assert L.rd_chain_create_ex(12, 10, 0, 10, 0, None, ctypes.byref(h)) == rd.RD_EINVAL        # m=12 dense
     assert L.rd_set_gemm_tma(4) == rd.RD_EINVAL and L.rd_set_gemm_tma(-1) == rd.RD_EINVAL
     assert L.rd_set_gemm_tma(1) == rd.RD_OK
+    assert L.rd_set_split_tail(3) == rd.RD_EINVAL and L.rd_set_split_tail(-1) == rd.RD_EINVAL
+    assert L.rd_set_split_tail(1) == rd.RD_OK
+    assert L.rd_set_stream_k(4) == rd.RD_EINVAL and L.rd_set_stream_k(-1) == rd.RD_EINVAL
+    assert L.rd_set_stream_k(0) == rd.RD_OK
     assert L.rd_stats_len(10) == 41
     assert L.rd_set_sparse_bytes(3) == rd.RD_EINVAL and L.rd_set_sparse_bytes(-1) == rd.RD_EINVAL
     assert L.rd_set_sparse_bytes(2) == rd.RD_OK
