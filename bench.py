@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 37686883000}   # profiles/r02b_gemm_ncu_summary.txt (TMA mainloop): 36.583 GB read + 1.104 GB write
+TRAFFIC = {9: 37889665864}   # profiles/r02l_gemm_ncu_summary.txt (TMA mainloop, d = 4): 36.908 GB read + 0.982 GB write
 
 
 def parse():
