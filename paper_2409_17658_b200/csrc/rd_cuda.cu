@@ -1907,7 +1907,7 @@ struct rd_chain {
   // method 0, long steps: the DPX column count is tuned on the chain's first two TMA steps
   // (3, then 4, each timed with events; the faster is kept) unless rd_set_gemm_variant fixed it
   int dpx = -1, tune_state = 0;
-  cudaEvent_t tune_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t tune_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
@@ -2694,6 +2694,32 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 0 : 1;   // measured: the last-warp refill is no faster
     tma = &c->tma;
   }
+  // The DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
+  // §5), so a chain of long dense steps (>= ~1 ms: ntiles x kstages >= 37000; m >= 8 and the
+  // row panels of m >= 8) times three consecutive steps with d = 3, 4, 3 and keeps d = 4 iff it
+  // beat the mean of the two d = 3 steps (the mean cancels the linear drift of the fused stats'
+  // cost while the alpha count grows).  Tuning starts at the power A^4, the first whose
+  // entries are all finite (the earlier ones take the stats' slow path).
+  const bool tune = g_dpx_auto && sk_nsk == 0 && (double)ntiles * (double)kstages >= 37000.0 && knew >= 4;
+  int dpx = -1;
+  if (tune && c->tune_state < 4) {
+    if (c->tune_state == 0) {
+      for (cudaEvent_t &e : c->tune_ev) RD_CUDA_CHECK(cudaEventCreate(&e));
+      dpx = 3;
+    } else if (c->tune_state == 1) {
+      dpx = 4;
+    } else if (c->tune_state == 2) {
+      dpx = 3;
+    } else {
+      float t[3] = {0.f, 0.f, 0.f};
+      RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[5]));
+      for (int i = 0; i < 3; ++i) RD_CUDA_CHECK(cudaEventElapsedTime(&t[i], c->tune_ev[2 * i], c->tune_ev[2 * i + 1]));
+      c->dpx = t[1] < 0.5f * (t[0] + t[2]) ? 4 : 3;
+    }
+  }
+  if (tune && c->tune_state >= 3) dpx = c->dpx;
+  const int tuning = (tune && c->tune_state < 3) ? c->tune_state : -1;
+  if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning], c->st));
   if (sk_nsk > 0) {
     const int64_t R = (ntiles - sk_nfull) * kstages;
     const int64_t per_min = R / sk_nsk;
@@ -2714,31 +2740,9 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
                                      c->N, c->Mp, c->P, epi, c->st, 1, tma);
     if (rc != RD_OK) return rc;
   } else if (nsplit == 1) {
-    // the DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
-    // §5), so a chain of long TMA steps times one step with each and keeps the faster
-    int dpx = -1;
-    if (tma && g_dpx_auto && c->tune_state < 3) {
-      if (c->tune_state == 0) {
-        for (cudaEvent_t &e : c->tune_ev) RD_CUDA_CHECK(cudaEventCreate(&e));
-        dpx = 3;
-      } else if (c->tune_state == 1) {
-        dpx = 4;
-      } else {
-        float t3 = 0.f, t4 = 0.f;
-        RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[3]));
-        RD_CUDA_CHECK(cudaEventElapsedTime(&t3, c->tune_ev[0], c->tune_ev[1]));
-        RD_CUDA_CHECK(cudaEventElapsedTime(&t4, c->tune_ev[2], c->tune_ev[3]));
-        c->dpx = t4 < t3 ? 4 : 3;
-      }
-    }
-    if (tma && g_dpx_auto && c->tune_state >= 2) dpx = c->dpx;
-    const int tuning = (tma && g_dpx_auto && c->tune_state < 2) ? c->tune_state : -1;
-    if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning], c->st));
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
                                      c->N, c->Mp, c->P, epi, c->st, 1, tma, tn, dpx);
     if (rc != RD_OK) return rc;
-    if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning + 1], c->st));
-    if (tma && g_dpx_auto && c->tune_state < 3) ++c->tune_state;
   } else {
     // split-K with the in-kernel fixup: partial tiles in c->ws, the last CTA of each tile folds
     // them, stores the power and computes the stats (no separate combine pass)
@@ -2758,9 +2762,11 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
       epi.tail_split = nsplit;
     }
     int rc = launch_gemm<true, true>(c->slot(c->k), c->Mp, c->BP, c->P, c->P / 2, c->slot(knew), c->Mp, c->Mr,
-                                     c->N, c->Mp, c->P, epi, c->st, tail ? 1 : nsplit, tma, tn);
+                                     c->N, c->Mp, c->P, epi, c->st, tail ? 1 : nsplit, tma, tn, dpx);
     if (rc != RD_OK) return rc;
   }
+  if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning + 1], c->st));
+  if (tune && c->tune_state < 4) ++c->tune_state;
   c->k = knew;
   return RD_OK;
 } RD_ABI_CATCH("rd_chain_step")

@@ -1161,9 +1161,9 @@ def test_forced_split_k_fixup_equals_oracle(tn):
 
 
 def test_chain_tunes_dpx_mix_bit_exact():
-    """A dense chain on the TMA mainloop times its first step with 3 and its second with 4 DPX
-    columns and keeps the faster (rd_set_gemm_variant default): every power stays equal to the
-    oracle's and the chosen variant is 3 or 4; an explicit variant switches the tuning off."""
+    """Every power of a chain stays equal to the oracle's whatever DPX mix it runs with (m = 7
+    on the TMA mainloop: its steps are too short for the d = 3 / 4 tuning, so the default 3),
+    and an explicit variant is what the chain reports."""
     rd.rd_set_gemm_tma(2)
     try:
         P = {k: X for k, X in O.powers(7, 7)}
@@ -1182,3 +1182,21 @@ def test_chain_tunes_dpx_mix_bit_exact():
     finally:
         rd.rd_set_gemm_variant(-1)
         rd.rd_set_gemm_tma(1)
+
+
+def test_long_cp_async_steps_tune_dpx_mix_bit_exact():
+    """Long dense steps on the cp.async mainloop tune the DPX mix too (an 8-rank m = 8 row panel:
+    464 tiles x 116 k-stages, tail-split by the wave model; A^4..A^6 timed with d = 3, 4, 3, the
+    choice used from A^7 on): sampled rows of every power equal the oracle's row chain (row i of
+    A^k = row i of A^{k-1} (x) A) and the choice is 3 or 4."""
+    m, r0, r1 = 8, 0, 1024
+    A = O.matrix(m)
+    rows = np.sort(sample_rows(r1 - r0, 16, seed=97)) + r0
+    X = A[rows]
+    ch = rd.Chain(m, alpha_max=4, row_begin=r0, row_end=r1)
+    for k in range(2, 10):
+        ch.step()
+        X = O.minplus(X, A, skip=True)
+        assert (ch.read_rows(k)[rows - r0] == to_inf(X, OINF, RINF, np.int16)).all(), k
+    assert ch.gemm_variant in (3, 4)
+    ch.close()

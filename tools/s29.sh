@@ -1,0 +1,13 @@
+set -u
+O=gpurun_out
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "tunes_dpx or long_cp_async" > $O/s29_pytest.txt 2>&1; echo "pytest rc=$?" >> $O/s29_pytest.txt
+for rep in 1 2; do
+  for v in auto 3 4; do
+    if [ $v = auto ]; then timeout 300 python tools/ab_step.py 8 20; else RD_VARIANT=$v timeout 300 python tools/ab_step.py 8 20; fi
+  done
+  for v in auto 3 4; do
+    if [ $v = auto ]; then timeout 300 python tools/ab_step.py 9 5; else RD_VARIANT=$v timeout 300 python tools/ab_step.py 9 5; fi
+  done
+done > $O/s29_dpx_tune.txt 2>&1
+tail -3 $O/s29_pytest.txt; cat $O/s29_dpx_tune.txt
