@@ -348,9 +348,10 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * use two IMAD packed adds (fma pipe) + one VIMNMX3.S16x2 (alu) per two k-pairs
  * (DESIGN.md §5).  Every variant computes the identical result.  By default (or after
  * dpx_cols = -1) a dense chain with long steps (tiles x k-stages >= 37000, i.e. >= ~1 ms: m >= 8
- * and their row panels; not stream-K steps) times the steps producing A^4, A^5, A^6 with 3, 4
- * and 3 DPX columns and keeps 4 iff it beat the mean of the two 3s (the two trade places by
- * ~1.5 % from one B200 to the next); any explicit value turns that off.  Errors: RD_EINVAL. */
+ * and their row panels; not stream-K steps) times the steps producing A^4 .. A^7 with 3, 4, 4
+ * and 3 DPX columns and keeps 4 iff its two steps took less than the two with 3 (the two
+ * trade places by ~1.5 % from one B200 to the next); any explicit value turns that off.
+ * Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 /* The DPX column count a chain's steps use (after its tuning steps), or -1 for NULL. */
 int rd_chain_gemm_variant(const rd_chain *c);
@@ -373,13 +374,14 @@ int rd_set_gemm_tile(int tn);
 int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, int *nsplit, int *tail, double *cost);
 
 /* rd_set_gemm_tma — process-wide choice of the dense chain step's mainloop loads: with TMA,
- * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor, completion
- * counted on an mbarrier; the warps release stages on a second mbarrier); without, every
- * thread issues cp.async and the CTA meets at __syncthreads.  mode 0 = cp.async always;
- * 1 (default) = TMA for single-pass steps of >= 128 stages (the m >= 9 orders); 2 = TMA
- * always; 3 = as 1 but the last warp to release a stage refills it (the default: thread 0
- * waits until every warp has released the stage, then refills it; measured equal within 0.6 %
- * at m = 9), for A/B timing.  Identical results.  RD_EINVAL outside 0..3. */
+ * one thread streams each stage (32 k-pairs = 64 k) of both operands (cp.async.bulk.tensor,
+ * completion counted on an mbarrier; the warps release stages on a second mbarrier); without,
+ * every thread issues cp.async and the CTA meets at __syncthreads.  mode 0 = cp.async always;
+ * 1 (default) = TMA for every 128-wide step (whole or split) of >= 64 k-stages (m >= 8 and
+ * their row panels); 2 = TMA for every 128-wide step; 3 = as 1 but the last warp to release a
+ * stage refills it (the default: thread 0 waits until every warp has released the stage, then
+ * refills it; measured equal within 0.6 % at m = 9), for A/B timing.  The
+ * 64-wide tiles always use cp.async.  Identical results.  RD_EINVAL outside 0..3. */
 int rd_set_gemm_tma(int mode);
 
 /* rd_set_split_k — process-wide split-K policy of dense chain steps: 1 (default) = split the

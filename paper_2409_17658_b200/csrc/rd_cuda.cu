@@ -1907,7 +1907,7 @@ struct rd_chain {
   // method 0, long steps: the DPX column count is tuned on the chain's first two TMA steps
   // (3, then 4, each timed with events; the faster is kept) unless rd_set_gemm_variant fixed it
   int dpx = -1, tune_state = 0;
-  cudaEvent_t tune_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t tune_ev[8] = {};
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
@@ -2340,10 +2340,12 @@ extern "C" int rd_set_stream_k(int mode) try {
   g_stream_k = mode;
   return RD_OK;
 } RD_ABI_CATCH("rd_set_stream_k")
-// rd_set_gemm_tma: 0 = cp.async mainloop always; 1 (default) = TMA mainloop for single-pass
-// steps of >= 128 pipeline stages (measured: m = 9 274.2 vs 277.0 ms; with fewer stages per
-// CTA — split-K, m <= 8 — the single-thread issue costs 3-8 %); 2 = TMA always.
+// rd_set_gemm_tma: 0 = cp.async mainloop always; 1 (default) = TMA mainloop for every 128-wide
+// step of >= kTmaMinStages k-stages, whole or split (measured: m = 9 1 %, m = 8
+// 1.7 %, m = 9 8-rank panel with tail splits 3.9 % faster; m = 7, 40 stages, equal — round 1's
+// 3-8 % loss for short CTAs no longer shows with the current kernel); 2 = TMA for every 128-wide step.
 static int g_gemm_tma = 1;
+constexpr int64_t kTmaMinStages = 64;
 
 extern "C" int rd_set_gemm_tma(int mode) try {
   rd_enter();
@@ -2387,7 +2389,7 @@ static double dense_step_plan(int64_t Mp, int64_t P, int sms, int tile_force, in
       if (full == 0 || full == tiles) return -1.0;
       t = waves(w_tn, full, work(w_tn, 1)) + waves(w_tn, (tiles - full) * n, work(w_tn, n));
     }
-    if (w_tn == 128 && n == 1 && kstages >= 128 && tma) t *= 0.99;
+    if (w_tn == 128 && kstages >= kTmaMinStages && tma) t *= 0.98;   // TMA mainloop (measured 1.5-4 %)
     return t;
   };
   double best = -1.0;
@@ -2416,7 +2418,7 @@ extern "C" int rd_dense_step_plan(int64_t rows, int64_t N, int sms, int *tile, i
     return fail(RD_EINVAL, "rd_dense_step_plan: need 1 <= rows <= N, sms >= 1, non-NULL outputs");
   int tl = 0;
   const double t = dense_step_plan(round_up(rows, kTile), round_up(N, kTile), sms, g_gemm_tile, g_split_k_off ? 1 : 0,
-                                   g_split_force, g_split_tail, g_gemm_tma == 1 || g_gemm_tma == 3, tile, nsplit, &tl);
+                                   g_split_force, g_split_tail, g_gemm_tma != 0, tile, nsplit, &tl);
   if (tail) *tail = tl;
   if (cost) *cost = t;
   return RD_OK;
@@ -2668,7 +2670,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const double best = dense_step_plan(c->Mp, c->P, sms, g_gemm_tile, g_split_k_off ? 1 : 0, g_split_force,
-                                        g_split_tail, g_gemm_tma == 1 || g_gemm_tma == 3, &tn, &nsplit, &tail);
+                                        g_split_tail, g_gemm_tma != 0, &tn, &nsplit, &tail);
     const int64_t slots = 2 * (int64_t)sms;
     const int64_t full_waves = ntiles / slots, rem = ntiles - full_waves * slots;
     if (g_stream_k == 2 && rem > 0) {
@@ -2688,7 +2690,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     }
   }
   const TmaOps *tma = nullptr;
-  if (tn == 128 && (g_gemm_tma == 2 || ((g_gemm_tma == 1 || g_gemm_tma == 3) && nsplit == 1 && kstages >= 128))) {
+  if (tn == 128 && (g_gemm_tma == 2 || ((g_gemm_tma == 1 || g_gemm_tma == 3) && kstages >= kTmaMinStages))) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
     c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 0 : 1;   // measured: the last-warp refill is no faster
@@ -2696,29 +2698,27 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   }
   // The DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
   // §5), so a chain of long dense steps (>= ~1 ms: ntiles x kstages >= 37000; m >= 8 and the
-  // row panels of m >= 8) times three consecutive steps with d = 3, 4, 3 and keeps d = 4 iff it
-  // beat the mean of the two d = 3 steps (the mean cancels the linear drift of the fused stats'
-  // cost while the alpha count grows).  Tuning starts at the power A^4, the first whose
-  // entries are all finite (the earlier ones take the stats' slow path).
+  // row panels of m >= 8) times four consecutive steps with d = 3, 4, 4, 3 and keeps d = 4 iff
+  // its two steps took less than the two d = 3 ones (the bracket cancels the linear drift of the
+  // fused stats' cost while the alpha count grows).  Tuning starts at the power A^4, the first
+  // whose entries are all finite (the earlier ones take the stats' slow path).
   const bool tune = g_dpx_auto && sk_nsk == 0 && (double)ntiles * (double)kstages >= 37000.0 && knew >= 4;
+  static const int kTuneD[4] = {3, 4, 4, 3};
   int dpx = -1;
-  if (tune && c->tune_state < 4) {
-    if (c->tune_state == 0) {
+  if (tune && c->tune_state < 5) {
+    if (c->tune_state == 0)
       for (cudaEvent_t &e : c->tune_ev) RD_CUDA_CHECK(cudaEventCreate(&e));
-      dpx = 3;
-    } else if (c->tune_state == 1) {
-      dpx = 4;
-    } else if (c->tune_state == 2) {
-      dpx = 3;
+    if (c->tune_state < 4) {
+      dpx = kTuneD[c->tune_state];
     } else {
-      float t[3] = {0.f, 0.f, 0.f};
-      RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[5]));
-      for (int i = 0; i < 3; ++i) RD_CUDA_CHECK(cudaEventElapsedTime(&t[i], c->tune_ev[2 * i], c->tune_ev[2 * i + 1]));
-      c->dpx = t[1] < 0.5f * (t[0] + t[2]) ? 4 : 3;
+      float t[4] = {0.f, 0.f, 0.f, 0.f};
+      RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[7]));
+      for (int i = 0; i < 4; ++i) RD_CUDA_CHECK(cudaEventElapsedTime(&t[i], c->tune_ev[2 * i], c->tune_ev[2 * i + 1]));
+      c->dpx = t[1] + t[2] < t[0] + t[3] ? 4 : 3;
     }
   }
-  if (tune && c->tune_state >= 3) dpx = c->dpx;
-  const int tuning = (tune && c->tune_state < 3) ? c->tune_state : -1;
+  if (tune && c->tune_state >= 4) dpx = c->dpx;
+  const int tuning = (tune && c->tune_state < 4) ? c->tune_state : -1;
   if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning], c->st));
   if (sk_nsk > 0) {
     const int64_t R = (ntiles - sk_nfull) * kstages;
@@ -2766,7 +2766,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     if (rc != RD_OK) return rc;
   }
   if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning + 1], c->st));
-  if (tune && c->tune_state < 4) ++c->tune_state;
+  if (tune && c->tune_state < 5) ++c->tune_state;
   c->k = knew;
   return RD_OK;
 } RD_ABI_CATCH("rd_chain_step")

@@ -962,12 +962,14 @@ def test_minplus_mul32_large_sampled_rows():
     assert (C[rows] == want).all()
 
 
-@pytest.mark.parametrize("m,r0,r1", [(6, 0, 848), (7, 0, 2507), (8, 1000, 2999)])
-def test_tma_mainloop_bit_identical(m, r0, r1):
-    # the TMA + mbarrier mainloop (forced on, incl. split-K steps) = the cp.async mainloop,
-    # powers and stats, for whole and partial panels
+@pytest.mark.parametrize("m,r0,r1,tile", [(6, 0, 848, 0), (7, 0, 2507, 0), (8, 1000, 2999, 0), (7, 0, 2507, 128),
+                                          (8, 0, 1024, 128), (8, 0, 7411, 128)])
+def test_tma_mainloop_bit_identical(m, r0, r1, tile):
+    # the TMA + mbarrier mainloop (forced on, incl. uniform and tail split-K steps: the 128-wide
+    # plans of m = 7 / 8) = the cp.async mainloop, powers and stats, for whole and partial panels
     def run(mode):
         rd.rd_set_gemm_tma(mode)
+        rd.rd_set_gemm_tile(tile)
         try:
             ch = rd.Chain(m, alpha_max=6, row_begin=r0, row_end=r1)
             st = [ch.step().cpu().numpy().copy() for _ in range(7)]
@@ -975,6 +977,7 @@ def test_tma_mainloop_bit_identical(m, r0, r1):
             ch.close()
         finally:
             rd.rd_set_gemm_tma(1)
+            rd.rd_set_gemm_tile(0)
         return np.stack(st), rows
     s0, x0 = run(0)
     s2, x2 = run(2)
