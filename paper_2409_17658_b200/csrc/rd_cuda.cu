@@ -2693,6 +2693,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   if (tn == 128 && (g_gemm_tma == 2 || ((g_gemm_tma == 1 || g_gemm_tma == 3) && kstages >= kTmaMinStages))) {
     if (int rc = chain_tma_prepare(c)) return rc;
     c->tma.xslot = c->k % (c->alpha_max + 1);
+    c->tma.nslots = c->alpha_max + 1;
     c->tma.refill_by_thread0 = g_gemm_tma == 3 ? 0 : 1;   // measured: the last-warp refill is no faster
     tma = &c->tma;
   }

@@ -146,7 +146,8 @@ static __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap 
 // ({Mp, P/2, slots} u32, box 128 x 32 x 1), B = the packed operand ({P, P/2} u32, box 128 x 32).
 struct TmaOps {
   CUtensorMap x, b;
-  int xslot;
+  int xslot;               // ring slot of the left operand A^k (the earlier powers: xslot - a mod nslots)
+  int nslots;              // ring slots (alpha_max + 1)
   int refill_by_thread0;   // 1 (default): thread 0 waits on empty_bar, then refills; 0: the last warp to release refills
 };
 

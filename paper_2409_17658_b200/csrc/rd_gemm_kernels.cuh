@@ -17,6 +17,10 @@ constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
 #define RD_EPI_FAST_ALL 1   // 0: the cp.async instances keep the next-alpha prefetch form (A/B)
 #endif
 constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
+#ifndef RD_EPI_TMA
+#define RD_EPI_TMA 0   // 1: the TMA instance streams the earlier powers' tiles through the stage ring (A/B: slower)
+#endif
+constexpr bool kEpiTma = RD_EPI_TMA;
 #ifndef RD_EPI_OPAQUE
 #define RD_EPI_OPAQUE 1   // 1: the TMA epilogue re-reads `out` per alpha (nothing hoisted: no spills)
 #endif
@@ -396,7 +400,26 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
       for (int p = 0; p < NC / 2; ++p) out_inf |= __vcmpeq2(out[r][p], kInf2);
   }
-  if constexpr (OUT != kOutRP) {
+  // TMA instance: the earlier powers' tiles (A^{k+1-a} at this tile's PM address: 64 column
+  // pairs x 128 rows = two 32 x 128 boxes of the ring's tensor map, 32 KB = one stage) stream
+  // through the freed stage ring, numbered after the mainloop's stages so the full / empty
+  // barrier phases carry on; thread 0 issues them as the warps release the stages.
+  constexpr bool kStream = TMA && kEpiTma && OUT == kOutPM;
+  auto epi_issue = [&](int a) {
+    const uint32_t g = it + (uint32_t)a;
+    const int s = (int)(g % kStages);
+    if (g >= (uint32_t)kStages) mbar_wait(&empty_bar[s], ((g / kStages) - 1) & 1);
+    uint32_t *dst = smem + s * SW;
+    const int sl = (tma.xslot - a + tma.nslots) % tma.nslots;
+    mbar_expect_tx(&full_bar[s], (uint32_t)(SW * 4));
+    tma_load_3d(dst, &tma.x, &full_bar[s], (int)i0, (int)(j0 / 2), sl);
+    tma_load_3d(dst + kBK2 * kTile, &tma.x, &full_bar[s], (int)i0, (int)(j0 / 2) + kBK2, sl);
+  };
+  if constexpr (kStream) {
+    if (tid == 0)
+      for (int a = 0; a < kStages && a < epi.nprev; ++a) epi_issue(a);
+  }
+  if constexpr (OUT != kOutRP && !kStream) {
     if (epi.nprev > 0) {
 #pragma unroll
       for (int g = 0; g < 2; ++g)
@@ -428,7 +451,20 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       // (RD_EPI_OPAQUE).  Without the opaque marks this form cost the cp.async instances 4.6 %
       // (profiles/r02i_epilogue_fastpath_ab.txt); with them it gains 1.0 % (TMA, m = 9) and
       // 1.1 % (cp.async, m = 8): profiles/r02l_epi_opaque_ab.txt, r02l_epi_fastall_ab.txt
-      if (a > 0) {
+      if constexpr (kStream) {
+        const uint32_t g = it + (uint32_t)a;
+        const int s = (int)(g % kStages);
+        mbar_wait(&full_bar[s], (g / kStages) & 1);
+        const uint32_t *T = smem + s * SW;
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2)
+#pragma unroll
+          for (int p = 0; p < NC / 2; ++p)
+            pv[g2][p] = *reinterpret_cast<const uint4 *>(T + ((p >> 1) * 32 + tx * 2 + (p & 1)) * kTile + g2 * 64 + ty * 4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+        if (tid == 0 && a + kStages < epi.nprev) epi_issue(a + kStages);
+      } else if (a > 0) {
         const uint32_t *Pa = epi.prev[a];
         const int64_t ldc_a = ldc;
 #pragma unroll
@@ -521,6 +557,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       red[warp][1 + 4 * a + 3] = v3;
     }
   }
+  if constexpr (kStream) it += (uint32_t)epi.nprev;   // the epilogue's stages
   __syncthreads();
   const int nval = 1 + 4 * epi.nprev;
   for (int e = tid; e < nval; e += kThreads) {
