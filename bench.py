@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 37889665864}   # profiles/r02l_gemm_ncu_summary.txt (TMA mainloop, d = 4): 36.908 GB read + 0.982 GB write
+TRAFFIC = {9: 36800737568}   # profiles/r02n_gemm_ncu_summary.txt (TMA mainloop): 35.816 GB read + 0.985 GB write
 
 
 def parse():
@@ -565,8 +565,9 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                          # C, and the alpha_max earlier powers the fused periodicity test reads
                          "algorithmic_bytes": int(2 * N * N + (2 + am) * 2 * (r1 - r0) * N),
                          "kernel": "minplus_gemm_kernel<RP,STATS,3> (peer B)" if args.form == "peer"
-                                   else ("minplus_gemm_kernel<PM,STATS,3,TMA>" if (N + 127) // 128 * 64 // 32 >= 128
-                                         else "minplus_gemm_kernel<PM,STATS,3>"),
+                                   else "minplus_gemm_kernel<PM,STATS,%s%s>" % (
+                                       dpx_used if dpx_used is not None else 3,
+                                       ",TMA" if (N + 127) // 128 * 64 // 32 >= 64 else ""),
                          "peak_basis": "unit-count bound: 148 SMs x 192 (min,+)/clk/SM x 1965 MHz (alu 2 + fma 2 warp-instr/clk/SM, issue 4; "
                                        "best mix 1 VIADDMNMX.S16x2 : 1 [2 IMAD + 1 VIMNMX3.S16x2]; DESIGN.md 5)",
                          "dpx_issue_peak": round(dpx_peak, 1), "frac_of_dpx_issue_peak": round(achieved / dpx_peak, 4),

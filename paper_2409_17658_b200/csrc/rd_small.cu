@@ -331,15 +331,26 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t P = round_up(N, kST);
   const int slen = 1 + 4 * alpha_max;
+  // one non-blocking stream per host thread and device, kept for the process: creating and
+  // destroying a stream per call cost more than the whole chain at m = 3
+  static thread_local cudaStream_t s_st[64] = {};
+  int sdev = 0;
+  RD_CUDA_CHECK(cudaGetDevice(&sdev));
   cudaStream_t st;
-  RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  if (sdev >= 0 && sdev < 64) {
+    if (!s_st[sdev]) RD_CUDA_CHECK(cudaStreamCreateWithFlags(&s_st[sdev], cudaStreamNonBlocking));
+    st = s_st[sdev];
+  } else {
+    RD_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  }
+  const bool own_stream = !(sdev >= 0 && sdev < 64);
   // one workspace: A, BP, ring, stats, result, barrier (16-byte aligned pieces)
   const size_t bA = round_up(N * N * 2, 256), bBP = (size_t)(P / 2 * P * 4), bR = (size_t)((alpha_max + 1) * P * P * 2);
   const size_t bS = round_up((int64_t)(kmax + 1) * slen * 4, 256), bRes = round_up((6 + kmax + 1) * 4, 256);
   char *ws = nullptr;
   cudaError_t e = ws_malloc((void **)&ws, bA + bBP + bR + bS + bRes + 256, st);
   if (e != cudaSuccess) {
-    cudaStreamDestroy(st);
+    if (own_stream) cudaStreamDestroy(st);
     (void)cudaGetLastError();
     return fail(RD_ENOMEM, "small_power_sequence: %s", cudaGetErrorString(e));
   }
@@ -353,7 +364,7 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
       h_res = nullptr;
       (void)cudaGetLastError();
       cudaFreeAsync(ws, st);
-      cudaStreamDestroy(st);
+      if (own_stream) cudaStreamDestroy(st);
       return fail(RD_ENOMEM, "small_power_sequence: pinned result buffer");
     }
     h_cap = 6 + kmax + 1;
@@ -368,8 +379,10 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
   sa.bar = reinterpret_cast<unsigned *>(ws + bA + bBP + bR + bS + bRes);
   sa.kmax = kmax; sa.alpha_max = alpha_max; sa.policy = policy;
   int rc = RD_OK;
+  // the upload is enqueued, not waited for (a pageable copy returns once the data is staged):
+  // "build" ends here and the chain's time includes the copy's execution
   if ((e = cudaMemcpyAsync(ws, Ahost, (size_t)(N * N * 2), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (e = cudaMemsetAsync(sa.bar, 0, 8, st)) != cudaSuccess || (e = cudaStreamSynchronize(st)) != cudaSuccess)
+      (e = cudaMemsetAsync(sa.bar, 0, 8, st)) != cudaSuccess)
     rc = fail(RD_ECUDA, "small_power_sequence: upload: %s", cudaGetErrorString(e));
   const auto t1 = std::chrono::steady_clock::now();
   if (rc == RD_OK) {
@@ -402,9 +415,11 @@ int small_power_sequence(const int16_t *Ahost, int64_t N, int kmax, int alpha_ma
       rc = fail(RD_ECUDA, "small_power_sequence: %s", cudaGetErrorString(e));
   }
   const auto t2 = std::chrono::steady_clock::now();
-  cudaFreeAsync(ws, st);
-  cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
+  cudaFreeAsync(ws, st);   // stream-ordered: the pool reuses it for the next call, no wait
+  if (own_stream) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
   if (t_build) *t_build = std::chrono::duration<double>(t1 - t0).count();
   if (t_chain) *t_chain = std::chrono::duration<double>(t2 - t1).count();
   if (rc != RD_OK) return rc;

@@ -18,12 +18,13 @@ echo "bench rc=$?"
 kill $SMI
 python bench.py --impl reference --steps 3 --warmup 1 > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err
 echo "ref rc=$?"
-CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > $O/${TAG}_plain.log 2>&1 &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv $CMD > $O/${TAG}_ncu_launches.log 2>&1
 echo "launches rc=$?"
 $CMD > $O/${TAG}_plain2.log 2>&1 &&
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:minplus_gemm -s 1 -c 1 -o $O/${TAG}_gemm $CMD > $O/${TAG}_ncu_full.log 2>&1
+# launch 7 = the power A^9, after the chain's DPX tuning (A^4..A^7) has chosen its mix
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:minplus_gemm -s 7 -c 1 -o $O/${TAG}_gemm $CMD > $O/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:panel_stats -s 2 -c 1 -o $O/${TAG}_panel_stats python tools/time_panel_stats.py > $O/${TAG}_ncu_ps.log 2>&1
 echo "ps full rc=$?"
