@@ -1,7 +1,7 @@
 """Median m-order dense chain step (CUDA events) for the librd build named by RD_LIB (A/B of
 compile variants, tools/build_ab.sh; RD_VARIANT=d forces the DPX column count, RD_TMA /
-RD_SPLIT_TAIL / RD_SPLIT_K / RD_TILE set rd_set_gemm_tma / rd_set_split_tail / rd_set_split_k /
-rd_set_gemm_tile).
+RD_SPLIT_TAIL / RD_SPLIT_K / RD_TILE / RD_STREAM_K set rd_set_gemm_tma / rd_set_split_tail /
+rd_set_split_k / rd_set_gemm_tile / rd_set_stream_k).
 python tools/ab_step.py [m] [steps]"""
 import os
 import statistics
@@ -24,6 +24,8 @@ if os.environ.get("RD_SPLIT_K"):
     rd.rd_set_split_k(int(os.environ["RD_SPLIT_K"]))
 if os.environ.get("RD_TILE"):
     rd.rd_set_gemm_tile(int(os.environ["RD_TILE"]))
+if os.environ.get("RD_STREAM_K"):
+    rd.rd_set_stream_k(int(os.environ["RD_STREAM_K"]))
 st = torch.cuda.current_stream()
 ch = rd.Chain(m, alpha_max=10, stream=st)
 for _ in range(5):
@@ -33,7 +35,7 @@ for a, b in ev:
     a.record(st); ch.step(); b.record(st)
 torch.cuda.synchronize()
 t = statistics.median(a.elapsed_time(b) for a, b in ev)
-tag = " ".join(f"{k}={os.environ[k]}" for k in ("RD_VARIANT", "RD_TMA", "RD_SPLIT_TAIL", "RD_SPLIT_K", "RD_TILE") if k in os.environ)
+tag = " ".join(f"{k}={os.environ[k]}" for k in ("RD_VARIANT", "RD_TMA", "RD_SPLIT_TAIL", "RD_SPLIT_K", "RD_TILE", "RD_STREAM_K") if k in os.environ)
 print(f"{os.path.basename(os.environ.get('RD_LIB', 'librd.so'))} {tag} m={m} d={ch.gemm_variant} step {t:.3f} ms "
       f"({float(ch.N) ** 3 / t / 1e9:.1f} T)", flush=True)
 ch.close()
