@@ -17,6 +17,9 @@ constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
 #define RD_EPI_FAST_ALL 1   // 0: the cp.async instances keep the next-alpha prefetch form (A/B)
 #endif
 constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
+#ifndef RD_DPX8_AS
+#define RD_DPX8_AS 8   // A/B builds only: the d = 8 instances compile with this many DPX columns
+#endif
 #ifndef RD_EPI_TMA
 #define RD_EPI_TMA 0   // 1: the TMA instance streams the earlier powers' tiles through the stage ring (A/B: slower)
 #endif
@@ -145,7 +148,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
       }
       const uint32_t *sx = smem + slot * SW;
       const uint32_t *sb = sx + kBK2 * kTile;
-      if (DPXC >= 8) {
+      if (DPXC >= 8 && RD_DPX8_AS >= 8) {
 #pragma unroll
         for (int t = 0; t < kBK2; ++t) {
           const uint4 xa = *reinterpret_cast<const uint4 *>(sx + t * kTile + ty * 4);
@@ -185,7 +188,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           for (int r = 0; r < 8; ++r)
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-              if ((r * kDpxRowShift + r * NC + c) % 8 < DPXC) {
+              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC)) {
                 acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
                 acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
               } else {
