@@ -17,6 +17,16 @@ constexpr int kDpxRowShift = RD_DPX_ROW_SHIFT;
 #define RD_EPI_FAST_ALL 1   // 0: the cp.async instances keep the next-alpha prefetch form (A/B)
 #endif
 constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
+#ifndef RD_LOOP_CR
+#define RD_LOOP_CR 0   // A/B builds: 1 visits the accumulators column-major in the stage body
+#endif
+#ifndef RD_DPX_SPLIT
+// the stage body's two k-pairs as two passes over the accumulators (every DPX accumulator's
+// first k-pair, then the second with the IMAD/VIMNMX3 ones) instead of one: -1 (default) = for
+// the TMA instances with d = 3 only (measured best there: m = 9 272.7 vs 278.5 ms, while d = 4
+// is faster in one pass, profiles/r02m_stage_order_ab.txt), 0 = never, 1 = always (A/B)
+#define RD_DPX_SPLIT -1
+#endif
 #ifndef RD_DPX8_AS
 #define RD_DPX8_AS 8   // A/B builds only: the d = 8 instances compile with this many DPX columns
 #endif
@@ -184,10 +194,30 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             b0[4 * h] = p.x; b0[4 * h + 1] = p.y; b0[4 * h + 2] = p.z; b0[4 * h + 3] = p.w;
             b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
+          constexpr bool kSplitPasses = RD_DPX_SPLIT < 0 ? (TMA && DPXC == 3) : RD_DPX_SPLIT != 0;
+          if constexpr (kSplitPasses) {
 #pragma unroll
-          for (int r = 0; r < 8; ++r)
+            for (int q = 0; q < 8 * NC; ++q) {
+              const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
+              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC))
+                acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
+            }
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
+            for (int q = 0; q < 8 * NC; ++q) {
+              const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
+              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC)) {
+                acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+              } else {
+                const uint32_t s0 = x0[r] * one + b0[c];
+                const uint32_t s1 = x1[r] * one + b1[c];
+                acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              // accumulator visit order: row-major (default) or column-major (RD_LOOP_CR, A/B)
+              const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
               if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC)) {
                 acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
                 acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
@@ -197,6 +227,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                 acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
               }
             }
+          }
         }
       }
       if constexpr (TMA) {   // release this stage; the last warp to release it refills it
