@@ -20,12 +20,11 @@ constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
 #ifndef RD_LOOP_CR
 #define RD_LOOP_CR 0   // A/B builds: 1 visits the accumulators column-major in the stage body
 #endif
-#ifndef RD_DPX_SPLIT
-// the stage body's two k-pairs as two passes over the accumulators (every DPX accumulator's
-// first k-pair, then the second with the IMAD/VIMNMX3 ones) instead of one: -1 (default) = for
-// the TMA instances with d = 3 only (measured best there: m = 9 272.7 vs 278.5 ms, while d = 4
-// is faster in one pass, profiles/r02m_stage_order_ab.txt), 0 = never, 1 = always (A/B)
-#define RD_DPX_SPLIT -1
+#ifndef RD_STAGE_ORDER
+// order of the stage body (see the mainloop): -1 (default) = two passes for the TMA instances
+// with d = 3 (m = 9 272.7 vs 278.5 ms one-pass), one pass otherwise (d = 4 is faster in one
+// pass: profiles/r02m_stage_order_ab.txt); 0..3 force an order in every instance (A/B)
+#define RD_STAGE_ORDER -1
 #endif
 #ifndef RD_DPX8_AS
 #define RD_DPX8_AS 8   // A/B builds only: the d = 8 instances compile with this many DPX columns
@@ -194,39 +193,63 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
             b0[4 * h] = p.x; b0[4 * h + 1] = p.y; b0[4 * h + 2] = p.z; b0[4 * h + 3] = p.w;
             b1[4 * h] = u.x; b1[4 * h + 1] = u.y; b1[4 * h + 2] = u.z; b1[4 * h + 3] = u.w;
           }
-          constexpr bool kSplitPasses = RD_DPX_SPLIT < 0 ? (TMA && DPXC == 3) : RD_DPX_SPLIT != 0;
-          if constexpr (kSplitPasses) {
-#pragma unroll
-            for (int q = 0; q < 8 * NC; ++q) {
-              const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
-              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC))
-                acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
-            }
-#pragma unroll
-            for (int q = 0; q < 8 * NC; ++q) {
-              const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
-              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC)) {
-                acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
-              } else {
-                const uint32_t s0 = x0[r] * one + b0[c];
-                const uint32_t s1 = x1[r] * one + b1[c];
-                acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
-              }
-            }
-          } else {
+          // stage-body order (RD_STAGE_ORDER): 0 = one pass, each accumulator's two k-pairs
+          // together; 1 = two passes (every DPX accumulator's first k-pair, then its second with
+          // the IMAD/VIMNMX3 accumulators); 2 = DPX first k-pairs, IMAD/VIMNMX3 accumulators, DPX
+          // second k-pairs; 3 = IMAD/VIMNMX3 accumulators, then the DPX ones (both k-pairs).
+          // Default: 1 for the TMA instance with d = 3, else 0 (measured).
+          constexpr int kOrder = RD_STAGE_ORDER >= 0 ? RD_STAGE_ORDER : ((TMA && DPXC == 3) ? 1 : 0);
+          constexpr int kD = DPXC == 8 ? RD_DPX8_AS : DPXC;
+          auto is_dpx = [&](int r, int c) { return (r * kDpxRowShift + r * NC + c) % 8 < kD; };
+          auto dpx_k = [&](int r, int c, int h) {
+            acc[r][c] = __viaddmin_s16x2(h ? x1[r] : x0[r], h ? b1[c] : b0[c], acc[r][c]);
+          };
+          auto imad_grp = [&](int r, int c) {
+            const uint32_t s0 = x0[r] * one + b0[c];
+            const uint32_t s1 = x1[r] * one + b1[c];
+            acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
+          };
+          if constexpr (kOrder == 0) {
 #pragma unroll
             for (int q = 0; q < 8 * NC; ++q) {
               // accumulator visit order: row-major (default) or column-major (RD_LOOP_CR, A/B)
               const int r = RD_LOOP_CR ? q % 8 : q / NC, c = RD_LOOP_CR ? q / 8 : q % NC;
-              if ((r * kDpxRowShift + r * NC + c) % 8 < (DPXC == 8 ? RD_DPX8_AS : DPXC)) {
-                acc[r][c] = __viaddmin_s16x2(x0[r], b0[c], acc[r][c]);
-                acc[r][c] = __viaddmin_s16x2(x1[r], b1[c], acc[r][c]);
+              if (is_dpx(r, c)) {
+                dpx_k(r, c, 0);
+                dpx_k(r, c, 1);
               } else {
-                const uint32_t s0 = x0[r] * one + b0[c];
-                const uint32_t s1 = x1[r] * one + b1[c];
-                acc[r][c] = __vimin3_s16x2(acc[r][c], s0, s1);
+                imad_grp(r, c);
               }
             }
+          } else if constexpr (kOrder == 1) {
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 0);
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
+              else imad_grp(q / NC, q % NC);
+            }
+          } else if constexpr (kOrder == 2) {
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 0);
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (!is_dpx(q / NC, q % NC)) imad_grp(q / NC, q % NC);
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (!is_dpx(q / NC, q % NC)) imad_grp(q / NC, q % NC);
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) {
+                dpx_k(q / NC, q % NC, 0);
+                dpx_k(q / NC, q % NC, 1);
+              }
           }
         }
       }
