@@ -21,10 +21,14 @@ constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
 #define RD_LOOP_CR 0   // A/B builds: 1 visits the accumulators column-major in the stage body
 #endif
 #ifndef RD_STAGE_ORDER
-// order of the stage body (see the mainloop): -1 (default) = two passes for the TMA instances
-// with d = 3 (m = 9 272.7 vs 278.5 ms one-pass), one pass otherwise (d = 4 is faster in one
-// pass: profiles/r02m_stage_order_ab.txt); 0..3 force an order in every instance (A/B)
+// order of the stage body (see the mainloop): -1 (default) = order 2 for the TMA instances
+// with d = 3 (m = 9 270.3 vs 278.5 ms one-pass, 272.7 two-pass), RD_STAGE_ORDER_CP (2) for the
+// cp.async instances with d = 3, one pass otherwise (d = 4 is fastest in one pass:
+// profiles/r02m_stage_order_ab.txt); 0..5 force an order in every instance (A/B)
 #define RD_STAGE_ORDER -1
+#endif
+#ifndef RD_STAGE_ORDER_CP
+#define RD_STAGE_ORDER_CP 2   // cp.async d = 3: m = 7 0.560 vs 0.564 ms, m = 8 11.10 vs 11.17 (profiles/r02m_stage_order_ab.txt)
 #endif
 #ifndef RD_DPX8_AS
 #define RD_DPX8_AS 8   // A/B builds only: the d = 8 instances compile with this many DPX columns
@@ -196,9 +200,11 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           // stage-body order (RD_STAGE_ORDER): 0 = one pass, each accumulator's two k-pairs
           // together; 1 = two passes (every DPX accumulator's first k-pair, then its second with
           // the IMAD/VIMNMX3 accumulators); 2 = DPX first k-pairs, IMAD/VIMNMX3 accumulators, DPX
-          // second k-pairs; 3 = IMAD/VIMNMX3 accumulators, then the DPX ones (both k-pairs).
-          // Default: 1 for the TMA instance with d = 3, else 0 (measured).
-          constexpr int kOrder = RD_STAGE_ORDER >= 0 ? RD_STAGE_ORDER : ((TMA && DPXC == 3) ? 1 : 0);
+          // second k-pairs; 3 = IMAD/VIMNMX3 accumulators, then the DPX ones (both k-pairs);
+          // 4 = 2 in two halves of rows; 5 = 2 row by row.
+          // Default: 2 for the instances with d = 3, else 0 (measured).
+          constexpr int kOrder = RD_STAGE_ORDER >= 0 ? RD_STAGE_ORDER
+                                 : DPXC != 3 ? 0 : TMA ? 2 : RD_STAGE_ORDER_CP;
           constexpr int kD = DPXC == 8 ? RD_DPX8_AS : DPXC;
           auto is_dpx = [&](int r, int c) { return (r * kDpxRowShift + r * NC + c) % 8 < kD; };
           auto dpx_k = [&](int r, int c, int h) {
@@ -240,7 +246,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
             for (int q = 0; q < 8 * NC; ++q)
               if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
-          } else {
+          } else if constexpr (kOrder == 3) {
 #pragma unroll
             for (int q = 0; q < 8 * NC; ++q)
               if (!is_dpx(q / NC, q % NC)) imad_grp(q / NC, q % NC);
@@ -250,6 +256,32 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
                 dpx_k(q / NC, q % NC, 0);
                 dpx_k(q / NC, q % NC, 1);
               }
+          } else if constexpr (kOrder == 4) {   // 2 in two halves of rows
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 0);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+              for (int q = hh * 4 * NC; q < (hh + 1) * 4 * NC; ++q)
+                if (!is_dpx(q / NC, q % NC)) imad_grp(q / NC, q % NC);
+#pragma unroll
+              for (int q = hh * 4 * NC; q < (hh + 1) * 4 * NC; ++q)
+                if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
+            }
+          } else {   // 2 row by row
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+#pragma unroll
+              for (int c = 0; c < NC; ++c)
+                if (is_dpx(r, c)) dpx_k(r, c, 0);
+#pragma unroll
+              for (int c = 0; c < NC; ++c)
+                if (!is_dpx(r, c)) imad_grp(r, c);
+#pragma unroll
+              for (int c = 0; c < NC; ++c)
+                if (is_dpx(r, c)) dpx_k(r, c, 1);
+            }
           }
         }
       }
