@@ -201,7 +201,8 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           // together; 1 = two passes (every DPX accumulator's first k-pair, then its second with
           // the IMAD/VIMNMX3 accumulators); 2 = DPX first k-pairs, IMAD/VIMNMX3 accumulators, DPX
           // second k-pairs; 3 = IMAD/VIMNMX3 accumulators, then the DPX ones (both k-pairs);
-          // 4 = 2 in two halves of rows; 5 = 2 row by row.
+          // 4 = 2 in two halves of rows; 5 = 2 row by row; 6 = 2 with the IMAD pass column-major;
+          // 7 = 2 with the second DPX pass in reverse.
           // Default: 2 for the instances with d = 3, else 0 (measured).
           constexpr int kOrder = RD_STAGE_ORDER >= 0 ? RD_STAGE_ORDER
                                  : DPXC != 3 ? 0 : TMA ? 2 : RD_STAGE_ORDER_CP;
@@ -268,6 +269,20 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
 #pragma unroll
               for (int q = hh * 4 * NC; q < (hh + 1) * 4 * NC; ++q)
                 if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
+            }
+          } else if constexpr (kOrder == 6 || kOrder == 7) {   // 2, IMAD pass column-major / DPX k1 reversed
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 0);
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              const int r = kOrder == 6 ? q % 8 : q / NC, c = kOrder == 6 ? q / 8 : q % NC;
+              if (!is_dpx(r, c)) imad_grp(r, c);
+            }
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              const int qq = kOrder == 7 ? 8 * NC - 1 - q : q;
+              if (is_dpx(qq / NC, qq % NC)) dpx_k(qq / NC, qq % NC, 1);
             }
           } else {   // 2 row by row
 #pragma unroll
