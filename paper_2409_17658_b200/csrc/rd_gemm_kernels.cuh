@@ -27,6 +27,9 @@ constexpr bool kEpiFastAll = RD_EPI_FAST_ALL;
 // profiles/r02m_stage_order_ab.txt); 0..5 force an order in every instance (A/B)
 #define RD_STAGE_ORDER -1
 #endif
+#ifndef RD_STAGE_ORDER32
+#define RD_STAGE_ORDER32 2   // the 32-bit GEMM's stage body: 2 three passes (N = 7411 21.79 vs 22.25 ms one pass), 0 (A/B)
+#endif
 #ifndef RD_STAGE_ORDER_CP
 #define RD_STAGE_ORDER_CP 2   // cp.async d = 3: m = 7 0.560 vs 0.564 ms, m = 8 11.10 vs 11.17 (profiles/r02m_stage_order_ab.txt)
 #endif
@@ -758,19 +761,38 @@ minplus_gemm32_kernel(const int32_t *__restrict__ XT, int64_t ldx, const int32_t
         b0[0] = p.x; b0[1] = p.y; b0[2] = p.z; b0[3] = p.w; b0[4] = q.x; b0[5] = q.y; b0[6] = q.z; b0[7] = q.w;
         b1[0] = u.x; b1[1] = u.y; b1[2] = u.z; b1[3] = u.w; b1[4] = v.x; b1[5] = v.y; b1[6] = v.z; b1[7] = v.w;
       }
+      if constexpr (RD_STAGE_ORDER32 == 2) {   // DPX first k | IMAD/VIMNMX3 | DPX second k (A/B)
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < DPXC) {
-            acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
-            acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
-          } else {
+          for (int c = 0; c < DPXC; ++c) acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = DPXC; c < 8; ++c) {
             const int32_t s0 = x0[r] * one + b0[c];
             const int32_t s1 = x1[r] * one + b1[c];
             acc[r][c] = __vimin3_s32(acc[r][c], s0, s1);
           }
-        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < DPXC; ++c) acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (c < DPXC) {
+              acc[r][c] = __viaddmin_s32(x0[r], b0[c], acc[r][c]);
+              acc[r][c] = __viaddmin_s32(x1[r], b1[c], acc[r][c]);
+            } else {
+              const int32_t s0 = x0[r] * one + b0[c];
+              const int32_t s1 = x1[r] * one + b1[c];
+              acc[r][c] = __vimin3_s32(acc[r][c], s0, s1);
+            }
+          }
+      }
     }
   }
   cp_async_wait<0>();
