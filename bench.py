@@ -357,9 +357,10 @@ def run_ours(args, rank, world, local_rank, backend="nccl"):
                "seconds": round(te, 3), "k_stop": res["k_stop"],
                "triple": [res["n0"], res["alpha"], res["beta"]]}
 
-    # dense power-step Gop/s at every order N = C_m (SURVEY §8(d) shapes and protocol: 3 warm-up
-    # steps, then median and best of 10 individually event-timed steps A^(k-1) (x) A, k = 5..14)
-    def timed(fn, warm=3, reps=10):
+    # dense power-step Gop/s at every order N = C_m (SURVEY §8(d) shapes and protocol: warm-up
+    # steps through the chain's DPX tuning (A^4..A^11 at m = 8), then median and best of 10
+    # individually event-timed steps A^(k-1) (x) A, k = 12..21)
+    def timed(fn, warm=10, reps=10):
         with torch.cuda.stream(stream):
             for _ in range(warm):
                 fn()

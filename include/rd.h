@@ -348,10 +348,10 @@ int64_t rd_agchain_order(const rd_agchain *c);
  * use two IMAD packed adds (fma pipe) + one VIMNMX3.S16x2 (alu) per two k-pairs
  * (DESIGN.md §5).  Every variant computes the identical result.  By default (or after
  * dpx_cols = -1) a dense chain with long steps (tiles x k-stages >= 37000, i.e. >= ~1 ms: m >= 8
- * and their row panels; not stream-K steps) times the steps producing A^4 .. A^7 with 3, 4, 4
- * and 3 DPX columns and keeps 4 iff its two steps took less than the two with 3 (the two
- * trade places by ~1.5 % from one B200 to the next); any explicit value turns that off.
- * Errors: RD_EINVAL. */
+ * and their row panels; not stream-K steps) times the steps producing A^4 .. A^7 (A^4 .. A^11
+ * for steps of < 2e6 tile-stages, e.g. m = 8) with 3, 4, 4, 3 (twice) DPX columns and keeps 4
+ * iff its steps took less in total than those with 3 (the two trade places by ~1.5 % from one
+ * B200 to the next); any explicit value turns that off.  Errors: RD_EINVAL. */
 int rd_set_gemm_variant(int dpx_cols);
 /* The DPX column count a chain's steps use (after its tuning steps), or -1 for NULL. */
 int rd_chain_gemm_variant(const rd_chain *c);

@@ -1907,7 +1907,7 @@ struct rd_chain {
   // method 0, long steps: the DPX column count is tuned on the chain's first two TMA steps
   // (3, then 4, each timed with events; the faster is kept) unless rd_set_gemm_variant fixed it
   int dpx = -1, tune_state = 0;
-  cudaEvent_t tune_ev[8] = {};
+  cudaEvent_t tune_ev[16] = {};
   int nsplit = 1;
   int *spread = nullptr;     // method 1 byte path: flags[k & 1] = "some row of A^k spreads > 254"
   // method 1 slab layout (build_slab_layout): columns of the powers permuted, inv = state ->
@@ -2699,27 +2699,34 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   }
   // The DPX/IMAD mix: d = 3 and d = 4 trade places by ~1.5 % from one B200 to the next (DESIGN.md
   // §5), so a chain of long dense steps (>= ~1 ms: ntiles x kstages >= 37000; m >= 8 and the
-  // row panels of m >= 8) times four consecutive steps with d = 3, 4, 4, 3 and keeps d = 4 iff
-  // its two steps took less than the two d = 3 ones (the bracket cancels the linear drift of the
-  // fused stats' cost while the alpha count grows).  Tuning starts at the power A^4, the first
-  // whose entries are all finite (the earlier ones take the stats' slow path).
+  // row panels of m >= 8) times brackets of four consecutive steps with d = 3, 4, 4, 3 and keeps
+  // d = 4 iff its steps took less in total than the d = 3 ones (the bracket cancels the linear
+  // drift of the fused stats' cost while the alpha count grows).  Steps under ~40 ms (m = 8)
+  // run two brackets: their d = 3 / 4 gap (~1 %) is near the step-to-step noise.  Tuning starts
+  // at the power A^4, the first whose entries are all finite (the earlier ones take the stats'
+  // slow path).
   const bool tune = g_dpx_auto && sk_nsk == 0 && (double)ntiles * (double)kstages >= 37000.0 && knew >= 4;
+  const int tune_steps = (double)ntiles * (double)kstages < 2.0e6 ? 8 : 4;
   static const int kTuneD[4] = {3, 4, 4, 3};
   int dpx = -1;
-  if (tune && c->tune_state < 5) {
+  if (tune && c->tune_state <= tune_steps) {
     if (c->tune_state == 0)
       for (cudaEvent_t &e : c->tune_ev) RD_CUDA_CHECK(cudaEventCreate(&e));
-    if (c->tune_state < 4) {
-      dpx = kTuneD[c->tune_state];
+    if (c->tune_state < tune_steps) {
+      dpx = kTuneD[c->tune_state % 4];
     } else {
-      float t[4] = {0.f, 0.f, 0.f, 0.f};
-      RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[7]));
-      for (int i = 0; i < 4; ++i) RD_CUDA_CHECK(cudaEventElapsedTime(&t[i], c->tune_ev[2 * i], c->tune_ev[2 * i + 1]));
-      c->dpx = t[1] + t[2] < t[0] + t[3] ? 4 : 3;
+      float t3 = 0.f, t4 = 0.f;
+      RD_CUDA_CHECK(cudaEventSynchronize(c->tune_ev[2 * tune_steps - 1]));
+      for (int i = 0; i < tune_steps; ++i) {
+        float t = 0.f;
+        RD_CUDA_CHECK(cudaEventElapsedTime(&t, c->tune_ev[2 * i], c->tune_ev[2 * i + 1]));
+        (kTuneD[i % 4] == 4 ? t4 : t3) += t;
+      }
+      c->dpx = t4 < t3 ? 4 : 3;
     }
   }
-  if (tune && c->tune_state >= 4) dpx = c->dpx;
-  const int tuning = (tune && c->tune_state < 4) ? c->tune_state : -1;
+  if (tune && c->tune_state >= tune_steps) dpx = c->dpx;
+  const int tuning = (tune && c->tune_state < tune_steps) ? c->tune_state : -1;
   if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning], c->st));
   if (sk_nsk > 0) {
     const int64_t R = (ntiles - sk_nfull) * kstages;
@@ -2767,7 +2774,7 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
     if (rc != RD_OK) return rc;
   }
   if (tuning >= 0) RD_CUDA_CHECK(cudaEventRecord(c->tune_ev[2 * tuning + 1], c->st));
-  if (tune && c->tune_state < 5) ++c->tune_state;
+  if (tune && c->tune_state <= tune_steps) ++c->tune_state;
   c->k = knew;
   return RD_OK;
 } RD_ABI_CATCH("rd_chain_step")

@@ -1189,15 +1189,15 @@ def test_chain_tunes_dpx_mix_bit_exact():
 
 def test_long_cp_async_steps_tune_dpx_mix_bit_exact():
     """Long dense steps on the cp.async mainloop tune the DPX mix too (an 8-rank m = 8 row panel:
-    464 tiles x 116 k-stages, tail-split by the wave model; A^4..A^6 timed with d = 3, 4, 3, the
-    choice used from A^7 on): sampled rows of every power equal the oracle's row chain (row i of
-    A^k = row i of A^{k-1} (x) A) and the choice is 3 or 4."""
+    464 tiles x 116 k-stages, tail-split by the wave model; A^4..A^11 timed as two d = 3, 4, 4, 3
+    brackets, the choice used from A^12 on): sampled rows of every power equal the oracle's row
+    chain (row i of A^k = row i of A^{k-1} (x) A) and the choice is 3 or 4."""
     m, r0, r1 = 8, 0, 1024
     A = O.matrix(m)
     rows = np.sort(sample_rows(r1 - r0, 16, seed=97)) + r0
     X = A[rows]
     ch = rd.Chain(m, alpha_max=4, row_begin=r0, row_end=r1)
-    for k in range(2, 10):
+    for k in range(2, 14):
         ch.step()
         X = O.minplus(X, A, skip=True)
         assert (ch.read_rows(k)[rows - r0] == to_inf(X, OINF, RINF, np.int16)).all(), k
