@@ -205,7 +205,7 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
           // the IMAD/VIMNMX3 accumulators); 2 = DPX first k-pairs, IMAD/VIMNMX3 accumulators, DPX
           // second k-pairs; 3 = IMAD/VIMNMX3 accumulators, then the DPX ones (both k-pairs);
           // 4 = 2 in two halves of rows; 5 = 2 row by row; 6 = 2 with the IMAD pass column-major;
-          // 7 = 2 with the second DPX pass in reverse.
+          // 7 = 2 with the second DPX pass in reverse; 8..10 further variants of 2 (A/B).
           // Default: 2 for the instances with d = 3, else 0 (measured).
           constexpr int kOrder = RD_STAGE_ORDER >= 0 ? RD_STAGE_ORDER
                                  : DPXC != 3 ? 0 : TMA ? 2 : RD_STAGE_ORDER_CP;
@@ -287,6 +287,24 @@ minplus_gemm_kernel(const uint32_t *__restrict__ XT, int64_t ldx, const uint32_t
               const int qq = kOrder == 7 ? 8 * NC - 1 - q : q;
               if (is_dpx(qq / NC, qq % NC)) dpx_k(qq / NC, qq % NC, 1);
             }
+          } else if constexpr (kOrder >= 8 && kOrder <= 10) {
+            // 8: 2 with the first DPX pass reversed; 9: 2 with the IMAD pass's rows from both ends
+            // inwards; 10: 2 with the IMAD pass's columns descending
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              const int qq = kOrder == 8 ? 8 * NC - 1 - q : q;
+              if (is_dpx(qq / NC, qq % NC)) dpx_k(qq / NC, qq % NC, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q) {
+              int r = q / NC, c = q % NC;
+              if (kOrder == 9) r = (r & 1) ? 7 - (r >> 1) : (r >> 1);
+              if (kOrder == 10) c = NC - 1 - c;
+              if (!is_dpx(r, c)) imad_grp(r, c);
+            }
+#pragma unroll
+            for (int q = 0; q < 8 * NC; ++q)
+              if (is_dpx(q / NC, q % NC)) dpx_k(q / NC, q % NC, 1);
           } else {   // 2 row by row
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
