@@ -36,7 +36,7 @@ PIPE_MINPLUS_PER_CLK_SM = 192
 SM_MAX_MHZ = 1965.0
 # dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch from `ncu --set full`
 # (profiles/), by m; None where not captured for the current kernel
-TRAFFIC = {9: 46642241224}   # profiles/r02o_gemm_ncu_summary.txt (TMA mainloop, d = 3): 45.659 GB read + 0.983 GB write
+TRAFFIC = {9: 46845147720}   # profiles/r02p_gemm_ncu_summary.txt (TMA mainloop, d = 3, A^9): 45.862 GB read + 0.983 GB write
 
 
 def parse():
