@@ -2656,7 +2656,8 @@ extern "C" int rd_chain_step(rd_chain *c, int32_t *stats_dev) try {
   // grows with resident warps; a 64-wide tile costs ~5% more instructions per term):
   // v128 = {0.676, 1}, v64 = {0.62, 0.90, 0.951}.  Fitted to tools/wave_probe.py
   // (profiles/r02_wave_probe.txt): it picks the measured best or within 2% for m = 6..9 and
-  // row panels of 1..8 ranks.  The TMA mainloop (tn = 128, n = 1, >= 128 stages) counts 1% faster.
+  // row panels of 1..8 ranks.  TMA plans (tn = 128, >= kTmaMinStages stages) count 2 % faster;
+  // tail splits leave the whole waves unsplit (dense_step_plan).
   //
   // Stream-K (g_stream_k): CTAs share contiguous k-stage ranges that cross tile boundaries;
   // a tile computed in pieces is finished in-kernel by its last piece (partials in c->ws,
