@@ -221,48 +221,49 @@ def test_every_status_entry_is_a_function_try_block():
 
 
 # Measured dense step times (ms, median of 10; m = 9 median of 3) of every (tile width, split)
-# configuration on one B200: "sN" every tile split N ways, "tailN" only the last partial wave's
-# tiles (profiles/r02k_wave_probe.txt; "t128/s1" is cp.async, the TMA default is ~1 % faster).
+# configuration on one B200 under the library's TMA policy (128-wide steps of >= 64 stages on
+# TMA): "sN" every tile split N ways, "tailN" only the last partial wave's tiles
+# (profiles/r02p_wave_probe_tma.txt).
 WAVE_TABLE = {
-    (6, 1): {"t128/s1": 0.0946, "t128/s2": 0.068, "t128/s3": 0.0602, "t128/s4": 0.0722, "t64/s1": 0.0546,
-             "t64/s2": 0.0623, "t64/s3": 0.0484, "t64/s4": 0.0525},
-    (7, 1): {"t128/s1": 0.5677, "t128/s2": 0.5887, "t128/s3": 0.5831, "t128/s4": 0.5549, "t128/tail2": 0.5871,
-             "t128/tail3": 0.5896, "t128/tail4": 0.5707, "t128/tail5": 0.5569, "t128/tail6": 0.5683,
-             "t64/s1": 0.5881, "t64/s2": 0.5569, "t64/s3": 0.576, "t64/s4": 0.5728, "t64/tail2": 0.5618,
-             "t64/tail3": 0.5657, "t64/tail4": 0.5669, "t64/tail5": 0.5681, "t64/tail6": 0.5713},
-    (7, 2): {"t128/s1": 0.3828, "t128/s2": 0.3077, "t128/s3": 0.3388, "t128/s4": 0.3153, "t64/s1": 0.305,
-             "t64/s2": 0.3123, "t64/s3": 0.3112, "t64/s4": 0.2953},
-    (7, 4): {"t128/s1": 0.2076, "t128/s2": 0.2206, "t128/s3": 0.2231, "t128/s4": 0.1684, "t64/s1": 0.2086,
-             "t64/s2": 0.1673, "t64/s3": 0.1831, "t64/s4": 0.1708},
-    (8, 1): {"t128/s1": 11.3724, "t128/s2": 11.4366, "t128/s3": 11.475, "t128/s4": 11.4517,
-             "t128/tail2": 11.3652, "t128/tail3": 11.3566, "t128/tail4": 11.2752, "t128/tail5": 11.2868,
-             "t128/tail6": 11.2931, "t64/s1": 12.0763, "t64/s2": 12.056, "t64/s3": 12.1472, "t64/s4": 12.1513,
-             "t64/tail2": 11.9582, "t64/tail3": 12.0272, "t64/tail4": 12.0007, "t64/tail5": 11.9724,
-             "t64/tail6": 11.9693},
-    (8, 2): {"t128/s1": 5.9499, "t128/s2": 5.7553, "t128/s3": 5.8393, "t128/s4": 5.8014, "t128/tail2": 5.7285,
-             "t128/tail3": 5.7746, "t128/tail4": 5.7175, "t128/tail5": 5.7057, "t128/tail6": 5.7102,
-             "t64/s1": 6.0596, "t64/s2": 6.0967, "t64/s3": 6.124, "t64/s4": 6.0911, "t64/tail2": 6.0614,
-             "t64/tail3": 6.0462, "t64/tail4": 6.0148, "t64/tail5": 6.0155, "t64/tail6": 6.0175},
-    (8, 4): {"t128/s1": 3.0074, "t128/s2": 3.0181, "t128/s3": 3.0288, "t128/s4": 3.0382, "t128/tail2": 3.0321,
-             "t128/tail3": 3.0361, "t128/tail4": 3.0258, "t128/tail5": 3.0213, "t128/tail6": 3.0207,
-             "t64/s1": 3.1774, "t64/s2": 3.1951, "t64/s3": 3.207, "t64/s4": 3.1985, "t64/tail2": 3.1882,
-             "t64/tail3": 3.1784, "t64/tail4": 3.1644, "t64/tail5": 3.1528, "t64/tail6": 3.1512},
-    (8, 8): {"t128/s1": 2.0124, "t128/s2": 1.7782, "t128/s3": 1.7053, "t128/s4": 1.6705, "t128/tail2": 1.7708,
-             "t128/tail3": 1.6911, "t128/tail4": 1.6583, "t128/tail5": 1.6501, "t128/tail6": 1.6654,
-             "t64/s1": 1.8671, "t64/s2": 1.7468, "t64/s3": 1.713, "t64/s4": 1.7509, "t64/tail2": 1.732,
-             "t64/tail3": 1.6879, "t64/tail4": 1.7227, "t64/tail5": 1.7054, "t64/tail6": 1.6889},
-    (9, 8): {"t128/s1": 37.1532, "t128/s2": 37.1428, "t128/s3": 36.7907, "t128/s4": 36.9268,
-             "t128/tail2": 37.0732, "t128/tail3": 36.674, "t128/tail4": 36.7436, "t128/tail5": 36.6013,
-             "t128/tail6": 36.6432, "t64/s1": 39.6353, "t64/s2": 39.3649, "t64/s3": 39.3077, "t64/s4": 39.3118,
-             "t64/tail2": 39.237, "t64/tail3": 39.109, "t64/tail4": 39.0526, "t64/tail5": 39.0353,
-             "t64/tail6": 39.0334},
+    (6, 1): {"t128/s1": 0.0943, "t128/s2": 0.0674, "t128/s3": 0.0588, "t128/s4": 0.0726, "t64/s1": 0.0561,
+             "t64/s2": 0.0634, "t64/s3": 0.0496, "t64/s4": 0.0536},
+    (7, 1): {"t128/s1": 0.56, "t128/s2": 0.5687, "t128/s3": 0.5743, "t128/s4": 0.5477, "t128/tail2": 0.5733,
+             "t128/tail3": 0.5723, "t128/tail4": 0.5497, "t128/tail5": 0.5478, "t128/tail6": 0.5595,
+             "t64/s1": 0.5887, "t64/s2": 0.5569, "t64/s3": 0.5784, "t64/s4": 0.5744, "t64/tail2": 0.561,
+             "t64/tail3": 0.5662, "t64/tail4": 0.5677, "t64/tail5": 0.5693, "t64/tail6": 0.5713},
+    (7, 2): {"t128/s1": 0.381, "t128/s2": 0.3046, "t128/s3": 0.3378, "t128/s4": 0.3137, "t64/s1": 0.3049,
+             "t64/s2": 0.3117, "t64/s3": 0.3154, "t64/s4": 0.2985},
+    (7, 4): {"t128/s1": 0.2083, "t128/s2": 0.2184, "t128/s3": 0.2211, "t128/s4": 0.169, "t64/s1": 0.2098,
+             "t64/s2": 0.1681, "t64/s3": 0.1847, "t64/s4": 0.1719},
+    (8, 1): {"t128/s1": 11.0637, "t128/s2": 11.1431, "t128/s3": 11.2156, "t128/s4": 11.3022,
+             "t128/tail2": 11.0173, "t128/tail3": 10.9731, "t128/tail4": 10.955, "t128/tail5": 10.9389,
+             "t128/tail6": 10.9459, "t64/s1": 11.9874, "t64/s2": 11.9688, "t64/s3": 12.0615, "t64/s4": 12.0999,
+             "t64/tail2": 11.8696, "t64/tail3": 11.9393, "t64/tail4": 11.9166, "t64/tail5": 11.8839,
+             "t64/tail6": 11.8776},
+    (8, 2): {"t128/s1": 5.7351, "t128/s2": 5.6232, "t128/s3": 5.661, "t128/s4": 5.6769, "t128/tail2": 5.5562,
+             "t128/tail3": 5.551, "t128/tail4": 5.5501, "t128/tail5": 5.5437, "t128/tail6": 5.5469,
+             "t64/s1": 6.0188, "t64/s2": 6.0595, "t64/s3": 6.0851, "t64/s4": 6.0697, "t64/tail2": 6.021,
+             "t64/tail3": 6.0118, "t64/tail4": 5.9795, "t64/tail5": 5.9816, "t64/tail6": 5.9827},
+    (8, 4): {"t128/s1": 2.9239, "t128/s2": 2.944, "t128/s3": 2.9649, "t128/s4": 2.9735, "t128/tail2": 2.9396,
+             "t128/tail3": 2.9639, "t128/tail4": 2.9468, "t128/tail5": 2.9562, "t128/tail6": 2.9557,
+             "t64/s1": 3.1636, "t64/s2": 3.1798, "t64/s3": 3.1922, "t64/s4": 3.2004, "t64/tail2": 3.1697,
+             "t64/tail3": 3.1614, "t64/tail4": 3.1507, "t64/tail5": 3.1426, "t64/tail6": 3.1395},
+    (8, 8): {"t128/s1": 1.9092, "t128/s2": 1.7086, "t128/s3": 1.6592, "t128/s4": 1.6296, "t128/tail2": 1.7042,
+             "t128/tail3": 1.6433, "t128/tail4": 1.6208, "t128/tail5": 1.623, "t128/tail6": 1.6142,
+             "t64/s1": 1.8614, "t64/s2": 1.7422, "t64/s3": 1.7098, "t64/s4": 1.7545, "t64/tail2": 1.7269,
+             "t64/tail3": 1.6839, "t64/tail4": 1.7812, "t64/tail5": 1.7029, "t64/tail6": 1.687},
+    (9, 8): {"t128/s1": 35.2239, "t128/s2": 35.3192, "t128/s3": 35.5107, "t128/s4": 35.7237,
+             "t128/tail2": 35.0407, "t128/tail3": 34.837, "t128/tail4": 34.8145, "t128/tail5": 34.7571,
+             "t128/tail6": 34.7664, "t64/s1": 39.3528, "t64/s2": 39.0722, "t64/s3": 39.0307, "t64/s4": 39.0456,
+             "t64/tail2": 38.9533, "t64/tail3": 38.8235, "t64/tail4": 38.7639, "t64/tail5": 38.7282,
+             "t64/tail6": 38.72},
 }
 
 
 def test_wave_model_picks_near_measured_best():
     """rd_dense_step_plan (the dense step's wave model, host only) picks, for every measured shape,
     a (tile width, split, split form) whose measured time is within 4 % of the best of the
-    measured configurations (uniform splits 1..4, tail splits 2..6; profiles/r02k_wave_probe.txt)
+    measured configurations (uniform splits 1..4, tail splits 2..6; profiles/r02p_wave_probe_tma.txt)
     (configuration-to-configuration noise is ~2 %), while the plain 128-tile step is up to 2x off."""
     from paper_2409_17658_b200 import dist as D
     worst_plain = 0.0

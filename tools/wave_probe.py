@@ -36,7 +36,7 @@ for m, parts in cases:
     res = {}
     for tn in (128, 64):
         rd.rd_set_gemm_tile(tn)
-        rd.rd_set_gemm_tma(0)
+        rd.rd_set_gemm_tma(1)   # the library's policy: TMA for 128-wide steps of >= 64 stages
         rd.rd_set_split_tail(0)
         for n in (1, 2, 3, 4):
             rd.rd_set_split_k(0 if n == 1 else n)
